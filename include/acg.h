@@ -1,0 +1,156 @@
+/*
+ * acg.h — C ABI of the B200 Aho-Corasick text scan (libacg.so).
+ *
+ * The reference (/root/reference, header-only C++20 `acmatch`) has no FFI; its
+ * scan path is the inline C++ API in proj/include/acmatch/aho_corasick.hpp.
+ * Each entry point below replaces one piece of that API (cited file:line,
+ * relative to /root/reference/proj). The C++ drop-in headers in
+ * include/acmatch/ are a thin inline layer over these functions, and
+ * INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions: functions returning int return ACG_OK (0) or an ACG_ERR_*
+ * code; the thread-local message of the last failure is acg_last_error().
+ * Plain pointers and sizes only. All handles are opaque and freed by the
+ * caller. An acg_automaton is immutable after acg_build and may be scanned
+ * from any number of threads concurrently (aho_corasick.hpp:50-52); an
+ * acg_scanner is single-user.
+ */
+#ifndef ACG_H_
+#define ACG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    ACG_OK = 0,
+    ACG_ERR_EMPTY_DICTIONARY = 1,     /* acmatch::EmptyDictionaryError (errors.hpp:21-24) */
+    ACG_ERR_EMPTY_PATTERN = 2,        /* acmatch::EmptyPatternError (errors.hpp:15-18) */
+    ACG_ERR_INVALID = 3,              /* acmatch::Error (errors.hpp:9-12) */
+    ACG_ERR_INVALID_WORKER_COUNT = 4, /* acmatch::InvalidWorkerCountError (errors.hpp:27-30) */
+    ACG_ERR_CUDA = 5,                 /* new: CUDA failure (acmatch::DeviceError) */
+    ACG_ERR_OUT_OF_MEMORY = 6,        /* new: device allocation failure */
+    ACG_ERR_NO_DEVICE = 7             /* new: no usable sm_100 device */
+};
+
+/* scan flags */
+enum {
+    ACG_SCAN_LIST = 1u,   /* produce the (end, id) match list */
+    ACG_SCAN_COUNTS = 2u, /* produce per-pattern occurrence counts */
+    ACG_SCAN_STATS = 4u,  /* count failure follows exactly as the reference scan (ScanStats) */
+    ACG_SCAN_PROFILE = 8u /* record CUDA events around each kernel stage (acg_scanner_kernel_ms) */
+};
+
+typedef struct acg_automaton acg_automaton;
+typedef struct acg_result acg_result;
+typedef struct acg_scanner acg_scanner;
+
+const char* acg_last_error(void);
+const char* acg_version(void);
+
+/* ---- build: replaces acmatch::build (aho_corasick.hpp:130-233) ----------
+ * Pattern i (id i, dense by construction) is concat[offsets[i], offsets[i+1]).
+ * Errors: ACG_ERR_EMPTY_DICTIONARY (:131), ACG_ERR_EMPTY_PATTERN (:133-134).
+ * Host-only; no device is touched until the first scan. */
+int acg_build(const uint8_t* concat, const uint64_t* offsets, uint32_t n_patterns, acg_automaton** out);
+void acg_automaton_destroy(acg_automaton* a);
+
+/* ---- accessors: Automaton (aho_corasick.hpp:58-101), NFA numbering ------- */
+uint32_t acg_state_count(const acg_automaton* a);                       /* :60 */
+uint32_t acg_pattern_count(const acg_automaton* a);                     /* :62 patterns().size() */
+uint32_t acg_max_pattern_length(const acg_automaton* a);
+/* goto_transition (:67-74): 1 and *to set when the edge exists, else 0 */
+int acg_goto_transition(const acg_automaton* a, uint32_t s, uint8_t b, uint32_t* to);
+/* transitions (:77-80): edge count; *bytes/*targets point into the automaton */
+uint32_t acg_transitions(const acg_automaton* a, uint32_t s, const uint8_t** bytes, const uint32_t** targets);
+uint32_t acg_failure(const acg_automaton* a, uint32_t s);               /* :84-87 */
+uint32_t acg_outputs(const acg_automaton* a, uint32_t s, const uint32_t** ids); /* :92-95 */
+uint32_t acg_depth(const acg_automaton* a, uint32_t s);                 /* :98-101 */
+/* next_state (:238-245) */
+uint32_t acg_next_state(const acg_automaton* a, uint32_t s, uint8_t b);
+
+/* Optional profile-guided layout: renumber the device DFA so that the states
+ * most visited on `sample` are the shared-memory-resident ones. Results are
+ * unaffected; only speed. Must be called before the first scan. */
+int acg_optimize_layout(acg_automaton* a, const uint8_t* sample, uint64_t n);
+
+/* Diagnostics: cap the number of shared-memory-resident DFA rows (0 = as
+ * many as fit). Exercises the cold paths on small automata. Must be called
+ * before the first scan. */
+int acg_set_hot_limit(acg_automaton* a, uint32_t max_hot_rows);
+
+/* ---- one-shot host scan: replaces acmatch::scan (aho_corasick.hpp:250-277) -
+ * Host text in, host results out (H2D, device scan, D2H inside).
+ * Records are ordered by (end, pattern_id) (aho_corasick.hpp:38-41). */
+int acg_scan(const acg_automaton* a, const uint8_t* text, uint64_t n, uint32_t flags, acg_result** out);
+uint64_t acg_result_match_count(const acg_result* r);       /* match_count (:280-282) */
+const uint32_t* acg_result_ids(const acg_result* r);        /* MatchRecord::pattern_id, M entries */
+const uint64_t* acg_result_ends(const acg_result* r);       /* MatchRecord::end, M entries */
+const uint64_t* acg_result_pattern_counts(const acg_result* r); /* P entries (ACG_SCAN_COUNTS) */
+uint64_t acg_result_failure_follows(const acg_result* r);   /* ScanStats::failure_follows (:46-48) */
+void acg_result_destroy(acg_result* r);
+
+/* ---- device-resident scanning (benchmarks, shards) ----------------------
+ * A scanner owns the device workspace for one automaton on one device and
+ * reuses it across runs. `d_text` is a device pointer (16-byte aligned) to n
+ * bytes; bytes [0, emit_from) are warm-up context only (emit_from must be a
+ * multiple of 16, and should be >= the automaton's halo for shard exactness);
+ * records carry end = base_offset + position. Runs are enqueued on `stream`
+ * (a cudaStream_t, NULL = the scanner's own stream) without host syncs. */
+int acg_scanner_create(const acg_automaton* a, int device, uint32_t flags, acg_scanner** out);
+void acg_scanner_destroy(acg_scanner* s);
+int acg_scanner_run(acg_scanner* s, const uint8_t* d_text, uint64_t n, uint64_t emit_from, uint64_t base_offset,
+                    void* stream);
+/* End-to-end: copy host text (pinned for full speed) to the device and scan it,
+ * overlapping the copy with the scan piecewise. */
+int acg_scanner_run_host(acg_scanner* s, const uint8_t* h_text, uint64_t n, void* stream);
+/* Waits for the last run; grows the record buffer and re-emits if it overflowed. */
+int acg_scanner_sync(acg_scanner* s);
+uint64_t acg_scanner_match_count(acg_scanner* s);            /* after sync */
+int acg_scanner_records(acg_scanner* s, uint32_t* ids, uint64_t* ends, uint64_t cap);   /* D2H + widen */
+int acg_scanner_packed_records(acg_scanner* s, uint64_t* host, uint64_t cap, uint32_t* id_bits);
+int acg_scanner_pattern_counts(acg_scanner* s, uint64_t* host_counts);           /* P entries */
+/* device pointers (valid until the next run / destroy) */
+const uint64_t* acg_scanner_device_pattern_counts(acg_scanner* s);
+const uint64_t* acg_scanner_device_records(acg_scanner* s, uint32_t* id_bits);
+uint64_t acg_scanner_failure_follows(acg_scanner* s);
+/* Order-independent digest of the record set (key = end*2^20 + id; sum and
+ * xor of splitmix64(key)) plus the number of adjacent pairs out of strict
+ * (end, id) order. Verification helper. */
+int acg_scanner_digest(acg_scanner* s, uint64_t* dsum, uint64_t* dxor, uint64_t* unsorted_pairs);
+/* Per-stage device time of the last run in ms: [K1 count walk (K1s or K1x),
+ * K1f excursion fix-up (sparse mode; 0 in exact mode), K2 prefix, K3
+ * compact+write, K4 pattern counts] (scanner created with ACG_SCAN_PROFILE). */
+int acg_scanner_kernel_ms(acg_scanner* s, float* ms5);
+/* Scan mode. SPARSE walks the truncated hot automaton from shared memory and
+ * replays the rare cold excursions exactly; EXACT walks the full DFA in
+ * lockstep (hot rows in shared memory, cold rows from L2). AUTO picks SPARSE
+ * when the automaton allows it and the previous run's excursion rate was low.
+ * Both are bit-exact; ACG_SCAN_STATS always runs EXACT. */
+enum { ACG_MODE_AUTO = 0, ACG_MODE_SPARSE = 1, ACG_MODE_EXACT = 2 };
+int acg_scanner_set_mode(acg_scanner* s, int mode);
+/* Mode of the last run (ACG_MODE_SPARSE / ACG_MODE_EXACT) and, when sparse,
+ * its event rate (events per walked byte; -1 before the first sparse sync). */
+int acg_scanner_last_mode(acg_scanner* s, double* event_rate);
+/* Copies the P per-pattern counts (u64) into a caller device buffer, enqueued
+ * on `stream` (NULL = the stream of the last run) — e.g. for an NCCL all-reduce. */
+int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream);
+/* Geometry of the last run: chunks, chunk bytes, and launches issued. */
+int acg_scanner_last_geometry(acg_scanner* s, uint64_t* n_chunks, uint64_t* chunk_bytes, uint32_t* launches);
+/* Device layout of the automaton (diagnostics): states, hot rows in smem, columns. */
+int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* hot_rows, uint32_t* columns,
+                         uint32_t* halo, int* alphabet_mode);
+
+/* Tuning knobs (diagnostics / benchmarks): streams per thread U in {1,2,4,8}
+ * and threads per block; 0 = default. */
+int acg_scanner_set_geometry(acg_scanner* s, uint32_t streams_per_thread, uint32_t threads_per_block,
+                             uint64_t chunk_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ACG_H_ */

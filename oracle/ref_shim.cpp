@@ -1,0 +1,249 @@
+// ORACLE — test infrastructure, NOT the product.
+//
+// A C-ABI shim over the UNMODIFIED reference headers, compiled by
+// oracle/Makefile from the sources where they lie under
+// /root/reference/proj/{include,tests} into oracle/_ref/libacref.so.
+// Used by the tests (to pin oracle/ac_oracle.c), by oracle/make_goldens.py
+// (golden fixtures) and by bench.py --impl reference / cpu_baseline (the
+// reference's own CPU scan timed on the host cores). No reference source is
+// copied into this repository; this file only #includes it.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <string>
+#include <string_view>
+#include <thread>
+#include <vector>
+
+#include "acmatch/aho_corasick.hpp"
+#include "acmatch/partition.hpp"
+#include "support/oracle.hpp"
+
+using acmatch::Automaton;
+using acmatch::MatchRecord;
+using acmatch::Pattern;
+
+namespace {
+
+std::vector<Pattern> to_patterns(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count) {
+    std::vector<Pattern> p;
+    p.reserve(count);
+    for (std::uint32_t i = 0; i < count; ++i)
+        p.push_back(Pattern{i, std::string(reinterpret_cast<const char*>(concat) + offs[i], offs[i + 1] - offs[i])});
+    return p;
+}
+
+int error_code(const std::exception& e) {
+    if (dynamic_cast<const acmatch::EmptyDictionaryError*>(&e)) return 1;
+    if (dynamic_cast<const acmatch::EmptyPatternError*>(&e)) return 2;
+    if (dynamic_cast<const acmatch::InvalidWorkerCountError*>(&e)) return 4;
+    return 3;
+}
+
+inline std::uint64_t mix64(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+struct Prepared {
+    std::vector<std::vector<std::uint32_t>> chunks;
+    std::vector<Automaton> machines;
+};
+
+}  // namespace
+
+extern "C" {
+
+int ref_build(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count, void** out) {
+    *out = nullptr;
+    try {
+        *out = new Automaton(acmatch::build(to_patterns(concat, offs, count)));
+        return 0;
+    } catch (const std::exception& e) {
+        return error_code(e);
+    }
+}
+
+void ref_free(void* h) { delete static_cast<Automaton*>(h); }
+
+std::uint32_t ref_state_count(void* h) { return static_cast<std::uint32_t>(static_cast<Automaton*>(h)->state_count()); }
+std::uint32_t ref_failure(void* h, std::uint32_t s) { return static_cast<Automaton*>(h)->failure(s); }
+std::uint32_t ref_depth(void* h, std::uint32_t s) { return static_cast<Automaton*>(h)->depth(s); }
+std::uint32_t ref_next_state(void* h, std::uint32_t s, std::uint8_t b) {
+    return acmatch::next_state(*static_cast<Automaton*>(h), s, b);
+}
+int ref_goto(void* h, std::uint32_t s, std::uint8_t b, std::uint32_t* to) {
+    const auto t = static_cast<Automaton*>(h)->goto_transition(s, b);
+    if (t) *to = *t;
+    return t.has_value();
+}
+std::uint32_t ref_outputs(void* h, std::uint32_t s, std::uint32_t* ids, std::uint32_t cap) {
+    const auto o = static_cast<Automaton*>(h)->outputs(s);
+    for (std::size_t i = 0; i < o.size() && i < cap; ++i) ids[i] = o[i];
+    return static_cast<std::uint32_t>(o.size());
+}
+std::uint32_t ref_transitions(void* h, std::uint32_t s, std::uint8_t* bytes, std::uint32_t* to, std::uint32_t cap) {
+    const auto e = static_cast<Automaton*>(h)->transitions(s);
+    for (std::size_t i = 0; i < e.size() && i < cap; ++i) {
+        bytes[i] = e[i].first;
+        to[i] = e[i].second;
+    }
+    return static_cast<std::uint32_t>(e.size());
+}
+
+// acmatch::scan (include/acmatch/aho_corasick.hpp:250-272) over text[0, n).
+std::uint64_t ref_scan(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t* follows,
+                       std::uint32_t* ids, std::uint64_t* ends, std::uint64_t cap) {
+    acmatch::ScanStats st;
+    const auto recs = acmatch::scan(*static_cast<Automaton*>(h),
+                                    std::string_view(reinterpret_cast<const char*>(text), n), st);
+    if (follows) *follows = st.failure_follows;
+    for (std::size_t i = 0; i < recs.size() && i < cap; ++i) {
+        ids[i] = recs[i].pattern_id;
+        ends[i] = recs[i].end;
+    }
+    return recs.size();
+}
+
+// Windowed reference scan for golden statistics: the reference scan of
+// text[start, n) (from the root), keeping records with absolute end >=
+// emit_from. Accumulates per-pattern counts, the record count, the
+// order-independent digest (key = end*2^20 + id) and the failure follows of
+// the steps at positions >= emit_from. Also verifies (end, id) strict order.
+// Returns 0, or 5 if the window output was not strictly increasing.
+int ref_scan_window_stats(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t start,
+                          std::uint64_t emit_from, std::uint64_t* counts, std::uint64_t* m,
+                          std::uint64_t* dsum, std::uint64_t* dxor, std::uint64_t* follows) {
+    const Automaton& a = *static_cast<Automaton*>(h);
+    const char* base = reinterpret_cast<const char*>(text);
+    acmatch::ScanStats all, pre;
+    const auto recs = acmatch::scan(a, std::string_view(base + start, n - start), all);
+    if (emit_from > start) (void)acmatch::scan(a, std::string_view(base + start, emit_from - start), pre);
+    *follows += all.failure_follows - pre.failure_follows;
+    int rc = 0;
+    bool first = true;
+    MatchRecord prev{};
+    for (const MatchRecord& r : recs) {
+        const std::uint64_t end = r.end + start;
+        if (end < emit_from) continue;
+        if (!first && !acmatch::match_before(prev, MatchRecord{r.pattern_id, end})) rc = 5;
+        prev = MatchRecord{r.pattern_id, end};
+        first = false;
+        counts[r.pattern_id]++;
+        const std::uint64_t k = mix64((end << 20) + r.pattern_id);
+        *dsum += k;
+        *dxor ^= k;
+        ++*m;
+    }
+    return rc;
+}
+
+// acmatch::run_partitioned (include/acmatch/partition.hpp:108-170), as is.
+int ref_run_partitioned(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count,
+                        const std::uint8_t* text, std::uint64_t n, std::uint32_t workers, std::uint32_t* ids,
+                        std::uint64_t* ends, std::uint64_t cap, std::uint64_t* m, double* wall_s,
+                        std::uint32_t* launched) {
+    try {
+        const auto run = acmatch::run_partitioned(to_patterns(concat, offs, count),
+                                                  std::string_view(reinterpret_cast<const char*>(text), n), workers);
+        *m = run.matches.size();
+        for (std::size_t i = 0; i < run.matches.size() && i < cap; ++i) {
+            ids[i] = run.matches[i].pattern_id;
+            ends[i] = run.matches[i].end;
+        }
+        if (wall_s) *wall_s = run.total_wall_s;
+        if (launched) *launched = run.workers_launched;
+        return 0;
+    } catch (const std::exception& e) {
+        return error_code(e);
+    }
+}
+
+// run_partitioned with the per-worker builds hoisted out of the timed region:
+// prepare = split_patterns + one reference build per non-empty chunk
+// (partition.hpp:113, :132-136); scan = one std::thread per machine running
+// the reference scan over the whole input, the id remap (:142) and the
+// reference k-way merge_matches (:167). This is the reference's only parallel
+// mode with the automata already built, i.e. the same boundary the GPU path
+// is timed at.
+void* ref_partitioned_prepare(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count,
+                              std::uint32_t workers) {
+    try {
+        const auto patterns = to_patterns(concat, offs, count);
+        const auto plan = acmatch::split_patterns(patterns, workers);
+        auto* p = new Prepared;
+        for (const auto& chunk : plan.chunks) {
+            if (chunk.empty()) continue;
+            std::vector<Pattern> local;
+            for (std::size_t j = 0; j < chunk.size(); ++j)
+                local.push_back(Pattern{static_cast<std::uint32_t>(j), patterns[chunk[j]].bytes});
+            p->chunks.push_back(chunk);
+            p->machines.push_back(acmatch::build(std::move(local)));
+        }
+        return p;
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+double ref_partitioned_scan(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t* m) {
+    auto* p = static_cast<Prepared*>(h);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::vector<MatchRecord>> lists(p->machines.size());
+    std::vector<std::thread> threads;
+    const std::string_view input(reinterpret_cast<const char*>(text), n);
+    for (std::size_t k = 0; k < p->machines.size(); ++k)
+        threads.emplace_back([&, k] {
+            lists[k] = acmatch::scan(p->machines[k], input);
+            for (MatchRecord& r : lists[k]) r.pattern_id = p->chunks[k][r.pattern_id];
+        });
+    for (auto& t : threads) t.join();
+    const auto merged = acmatch::merge_matches(lists);
+    *m = merged.size();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+std::uint32_t ref_partitioned_workers(void* h) {
+    return static_cast<std::uint32_t>(static_cast<Prepared*>(h)->machines.size());
+}
+
+void ref_partitioned_free(void* h) { delete static_cast<Prepared*>(h); }
+
+// testsupport's randomised trial (tests/acceptance/acceptance_main.cpp:120-126):
+// random_dictionary(rng, max_count, min_len, max_len) then random_input(rng,
+// max_input). Used to pin the oracle's mt19937_64 replay.
+std::uint32_t ref_random_trial(std::uint64_t seed, std::uint32_t max_count, std::uint32_t min_len,
+                               std::uint32_t max_len, std::uint64_t max_input, std::uint8_t* concat,
+                               std::uint64_t* offs, std::uint8_t* text, std::uint64_t* text_len) {
+    std::mt19937_64 rng(seed);
+    const auto patterns = testsupport::random_dictionary(rng, max_count, min_len, max_len);
+    const std::string input = testsupport::random_input(rng, max_input);
+    offs[0] = 0;
+    for (std::size_t i = 0; i < patterns.size(); ++i) {
+        std::memcpy(concat + offs[i], patterns[i].bytes.data(), patterns[i].bytes.size());
+        offs[i + 1] = offs[i] + patterns[i].bytes.size();
+    }
+    std::memcpy(text, input.data(), input.size());
+    *text_len = input.size();
+    return static_cast<std::uint32_t>(patterns.size());
+}
+
+// testsupport::naive_find_all (tests/support/oracle.hpp:31-43).
+std::uint64_t ref_naive_find_all(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count,
+                                 const std::uint8_t* text, std::uint64_t n, std::uint32_t* ids, std::uint64_t* ends,
+                                 std::uint64_t cap) {
+    const auto recs = testsupport::naive_find_all(to_patterns(concat, offs, count),
+                                                  std::string_view(reinterpret_cast<const char*>(text), n));
+    for (std::size_t i = 0; i < recs.size() && i < cap; ++i) {
+        ids[i] = recs[i].pattern_id;
+        ends[i] = recs[i].end;
+    }
+    return recs.size();
+}
+
+unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+}  // extern "C"

@@ -1,0 +1,349 @@
+"""Python binding of the `acmatch` API over the C ABI (include/acg.h).
+
+Mirrors the reference's names and semantics (reference paths relative to
+/root/reference/proj): `build` (include/acmatch/aho_corasick.hpp:130),
+`next_state` (:238), `scan` (:250/:274), `match_count` (:280),
+`match_before` (:38), the `Automaton` accessors (:58-101) and the error
+hierarchy (include/acmatch/errors.hpp). The scan runs on the GPU through
+lib/libacg.so; there is no CPU path. `Scanner` is the device-resident entry
+used by the benchmark and the shard runner.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import NamedTuple, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+SCAN_LIST, SCAN_COUNTS, SCAN_STATS, SCAN_PROFILE = 1, 2, 4, 8
+MODE_AUTO, MODE_SPARSE, MODE_EXACT = 0, 1, 2
+
+
+# ---- errors (include/acmatch/errors.hpp:9-48) ------------------------------
+class Error(RuntimeError):
+    pass
+
+
+class EmptyPatternError(Error):
+    pass
+
+
+class EmptyDictionaryError(Error):
+    pass
+
+
+class InvalidWorkerCountError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """New in this build: CUDA failure or no usable device."""
+
+
+_ERRORS = {1: EmptyDictionaryError, 2: EmptyPatternError, 3: Error, 4: InvalidWorkerCountError,
+           5: DeviceError, 6: DeviceError, 7: DeviceError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.acg().acg_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, Error)(msg)
+
+
+# ---- value types (aho_corasick.hpp:23-48) ----------------------------------
+class Pattern(NamedTuple):
+    id: int
+    bytes: bytes
+
+
+class MatchRecord(NamedTuple):
+    pattern_id: int
+    end: int
+
+
+@dataclass
+class ScanStats:
+    failure_follows: int = 0
+
+
+kRoot = 0
+
+
+def match_before(a: MatchRecord, b: MatchRecord) -> bool:
+    """aho_corasick.hpp:38-41: (end, pattern_id) ascending."""
+    return (a.end, a.pattern_id) < (b.end, b.pattern_id)
+
+
+def make_patterns(words: Sequence[bytes | str]) -> list[Pattern]:
+    return [Pattern(i, w.encode("latin-1") if isinstance(w, str) else bytes(w)) for i, w in enumerate(words)]
+
+
+def _pack(patterns: Sequence[Pattern]) -> tuple[np.ndarray, np.ndarray]:
+    offs = np.zeros(len(patterns) + 1, dtype=np.uint64)
+    if patterns:
+        offs[1:] = np.cumsum([len(p.bytes) for p in patterns], dtype=np.uint64)
+    concat = np.frombuffer(b"".join(p.bytes for p in patterns) or b"\0", dtype=np.uint8).copy()
+    return concat, offs
+
+
+class Automaton:
+    """The pattern-matching machine (aho_corasick.hpp:58-121). NFA numbering:
+    DFS preorder, children in insertion order, root = 0."""
+
+    def __init__(self, handle: int, patterns: list[Pattern]):
+        self._h = C.c_void_p(handle)
+        self._patterns = patterns
+
+    @classmethod
+    def from_arrays(cls, concat: np.ndarray, offs: np.ndarray) -> "Automaton":
+        """Build from a packed dictionary (pattern i = concat[offs[i]:offs[i+1]])."""
+        concat = np.ascontiguousarray(concat, dtype=np.uint8)
+        offs = np.ascontiguousarray(offs, dtype=np.uint64)
+        h = C.c_void_p()
+        _check(_lib.acg().acg_build(concat.ctypes.data_as(C.c_void_p), offs.ctypes.data_as(C.c_void_p),
+                                    len(offs) - 1, C.byref(h)))
+        a = cls.__new__(cls)
+        a._h = h
+        a._patterns = None
+        a._packed = (concat, offs)
+        return a
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            _lib.acg().acg_automaton_destroy(h)
+            self._h = C.c_void_p()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def state_count(self) -> int:
+        return _lib.acg().acg_state_count(self._h)
+
+    def patterns(self) -> list[Pattern]:
+        if self._patterns is None:
+            concat, offs = self._packed
+            b = concat.tobytes()
+            self._patterns = [Pattern(i, b[int(offs[i]):int(offs[i + 1])]) for i in range(len(offs) - 1)]
+        return self._patterns
+
+    def pattern_count(self) -> int:
+        return _lib.acg().acg_pattern_count(self._h)
+
+    def max_pattern_length(self) -> int:
+        return _lib.acg().acg_max_pattern_length(self._h)
+
+    def goto_transition(self, s: int, b: int) -> Optional[int]:
+        to = C.c_uint32()
+        return to.value if _lib.acg().acg_goto_transition(self._h, s, b, C.byref(to)) else None
+
+    def transitions(self, s: int) -> list[tuple[int, int]]:
+        bp, tp = _lib.u8p(), _lib.u32p()
+        n = _lib.acg().acg_transitions(self._h, s, C.byref(bp), C.byref(tp))
+        return [(bp[i], tp[i]) for i in range(n)]
+
+    def failure(self, s: int) -> int:
+        return _lib.acg().acg_failure(self._h, s)
+
+    def outputs(self, s: int) -> list[int]:
+        ip = _lib.u32p()
+        n = _lib.acg().acg_outputs(self._h, s, C.byref(ip))
+        return [ip[i] for i in range(n)]
+
+    def depth(self, s: int) -> int:
+        return _lib.acg().acg_depth(self._h, s)
+
+    def optimize_layout(self, sample: bytes | np.ndarray) -> None:
+        """Profile-guided device layout from a text sample (speed only)."""
+        arr = np.frombuffer(sample, dtype=np.uint8) if isinstance(sample, (bytes, bytearray)) else sample
+        arr = np.ascontiguousarray(arr, dtype=np.uint8)
+        _check(_lib.acg().acg_optimize_layout(self._h, arr.ctypes.data_as(C.c_void_p), arr.size))
+
+    def set_hot_limit(self, max_hot_rows: int) -> None:
+        """Diagnostics: cap the shared-memory-resident rows (exercises cold paths)."""
+        _check(_lib.acg().acg_set_hot_limit(self._h, max_hot_rows))
+
+    def layout(self) -> dict:
+        v = [C.c_uint32() for _ in range(4)]
+        mode = C.c_int()
+        _check(_lib.acg().acg_automaton_layout(self._h, *[C.byref(x) for x in v], C.byref(mode)))
+        return {"states": v[0].value, "hot_rows": v[1].value, "columns": v[2].value, "halo": v[3].value,
+                "alphabet": "dna4" if mode.value == 0 else "generic"}
+
+
+def build(patterns: Sequence[Pattern]) -> Automaton:
+    """aho_corasick.hpp:130-233. Raises EmptyDictionaryError, EmptyPatternError,
+    or Error when ids are not dense in load order (:135-136)."""
+    patterns = list(patterns)
+    if not patterns:
+        raise EmptyDictionaryError("dictionary is empty")
+    for i, p in enumerate(patterns):
+        if len(p.bytes) == 0:
+            raise EmptyPatternError(f"pattern {i} is empty")
+        if p.id != i:
+            raise Error("pattern ids must be dense and follow load order")
+    concat, offs = _pack(patterns)
+    h = C.c_void_p()
+    _check(_lib.acg().acg_build(concat.ctypes.data_as(C.c_void_p), offs.ctypes.data_as(C.c_void_p),
+                                len(patterns), C.byref(h)))
+    return Automaton(h.value, patterns)
+
+
+def next_state(a: Automaton, s: int, b: int) -> int:
+    """aho_corasick.hpp:238-245 (total transition function)."""
+    return _lib.acg().acg_next_state(a.handle, s, b)
+
+
+def _as_u8(text) -> np.ndarray:
+    if isinstance(text, str):
+        text = text.encode("latin-1")
+    if isinstance(text, (bytes, bytearray, memoryview)):
+        return np.frombuffer(text, dtype=np.uint8) if len(text) else np.zeros(0, np.uint8)
+    return np.ascontiguousarray(text, dtype=np.uint8)
+
+
+@dataclass
+class ScanResult:
+    ids: np.ndarray          # uint32[M]
+    ends: np.ndarray         # uint64[M]
+    counts: Optional[np.ndarray] = None  # uint64[P]
+    failure_follows: int = 0
+
+    def records(self) -> list[MatchRecord]:
+        return [MatchRecord(int(i), int(e)) for i, e in zip(self.ids, self.ends)]
+
+
+def scan_arrays(a: Automaton, text, flags: int = SCAN_LIST) -> ScanResult:
+    """One-shot host scan through acg_scan (H2D, GPU scan, D2H)."""
+    arr = _as_u8(text)
+    r = C.c_void_p()
+    _check(_lib.acg().acg_scan(a.handle, arr.ctypes.data_as(C.c_void_p), arr.size, flags, C.byref(r)))
+    try:
+        L = _lib.acg()
+        m = L.acg_result_match_count(r)
+        ids = np.ctypeslib.as_array(L.acg_result_ids(r), shape=(m,)).copy() if m else np.zeros(0, np.uint32)
+        ends = np.ctypeslib.as_array(L.acg_result_ends(r), shape=(m,)).copy() if m else np.zeros(0, np.uint64)
+        counts = None
+        if flags & SCAN_COUNTS:
+            p = a.pattern_count()
+            cp = L.acg_result_pattern_counts(r)
+            counts = np.ctypeslib.as_array(cp, shape=(p,)).copy() if cp else np.zeros(p, np.uint64)
+        return ScanResult(ids, ends, counts, L.acg_result_failure_follows(r))
+    finally:
+        _lib.acg().acg_result_destroy(r)
+
+
+def scan(a: Automaton, input, stats: Optional[ScanStats] = None) -> list[MatchRecord]:
+    """aho_corasick.hpp:250-277: every occurrence, ordered by (end, pattern_id).
+    With `stats`, failure follows are counted exactly as the reference does."""
+    res = scan_arrays(a, input, SCAN_LIST | (SCAN_STATS if stats is not None else 0))
+    if stats is not None:
+        stats.failure_follows += res.failure_follows
+    return res.records()
+
+
+def match_count(records) -> int:
+    """aho_corasick.hpp:280-282: occurrence count."""
+    return len(records)
+
+
+class Scanner:
+    """Device-resident scanning (acg_scanner_*): reusable workspace for one
+    automaton on one device; `run` enqueues on a CUDA stream without host syncs."""
+
+    def __init__(self, a: Automaton, device: int = 0, flags: int = SCAN_LIST | SCAN_COUNTS):
+        self.automaton = a
+        self.flags = flags
+        h = C.c_void_p()
+        _check(_lib.acg().acg_scanner_create(a.handle, device, flags, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            _lib.acg().acg_scanner_destroy(h)
+            self._h = C.c_void_p()
+
+    def set_geometry(self, streams_per_thread: int = 0, threads_per_block: int = 0, chunk_bytes: int = 0) -> None:
+        _check(_lib.acg().acg_scanner_set_geometry(self._h, streams_per_thread, threads_per_block, chunk_bytes))
+
+    def run(self, d_text_ptr: int, n: int, emit_from: int = 0, base_offset: int = 0, stream: int = 0) -> None:
+        _check(_lib.acg().acg_scanner_run(self._h, C.c_void_p(d_text_ptr), n, emit_from, base_offset,
+                                          C.c_void_p(stream or None)))
+
+    def run_host(self, text, stream: int = 0) -> None:
+        arr = _as_u8(text) if not isinstance(text, int) else None
+        ptr, n = (arr.ctypes.data, arr.size)
+        _check(_lib.acg().acg_scanner_run_host(self._h, C.c_void_p(ptr), n, C.c_void_p(stream or None)))
+
+    def run_host_ptr(self, ptr: int, n: int, stream: int = 0) -> None:
+        _check(_lib.acg().acg_scanner_run_host(self._h, C.c_void_p(ptr), n, C.c_void_p(stream or None)))
+
+    def sync(self) -> None:
+        _check(_lib.acg().acg_scanner_sync(self._h))
+
+    def match_count(self) -> int:
+        self.sync()
+        return _lib.acg().acg_scanner_match_count(self._h)
+
+    def records(self) -> tuple[np.ndarray, np.ndarray]:
+        m = self.match_count()
+        ids = np.empty(m, dtype=np.uint32)
+        ends = np.empty(m, dtype=np.uint64)
+        _check(_lib.acg().acg_scanner_records(self._h, ids.ctypes.data_as(C.c_void_p),
+                                              ends.ctypes.data_as(C.c_void_p), m))
+        return ids, ends
+
+    def packed_records(self) -> tuple[np.ndarray, int]:
+        m = self.match_count()
+        out = np.empty(m, dtype=np.uint64)
+        bits = C.c_uint32()
+        _check(_lib.acg().acg_scanner_packed_records(self._h, out.ctypes.data_as(C.c_void_p), m, C.byref(bits)))
+        return out, bits.value
+
+    def pattern_counts(self) -> np.ndarray:
+        out = np.empty(self.automaton.pattern_count(), dtype=np.uint64)
+        _check(_lib.acg().acg_scanner_pattern_counts(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def device_pattern_counts_ptr(self) -> int:
+        return _lib.acg().acg_scanner_device_pattern_counts(self._h) or 0
+
+    def device_records_ptr(self) -> tuple[int, int]:
+        bits = C.c_uint32()
+        p = _lib.acg().acg_scanner_device_records(self._h, C.byref(bits))
+        return (p or 0), bits.value
+
+    def failure_follows(self) -> int:
+        return _lib.acg().acg_scanner_failure_follows(self._h)
+
+    def digest(self) -> tuple[int, int, int]:
+        s, x, u = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(_lib.acg().acg_scanner_digest(self._h, C.byref(s), C.byref(x), C.byref(u)))
+        return s.value, x.value, u.value
+
+    def kernel_ms(self) -> list[float]:
+        """[K1 walk, K1f fix-up, K2 prefix, K3 write, K4 counts] in ms (SCAN_PROFILE)."""
+        out = (C.c_float * 5)()
+        _check(_lib.acg().acg_scanner_kernel_ms(self._h, out))
+        return list(out)
+
+    def set_mode(self, mode: int) -> None:
+        _check(_lib.acg().acg_scanner_set_mode(self._h, mode))
+
+    def last_mode(self) -> tuple[str, float]:
+        rate = C.c_double()
+        m = _lib.acg().acg_scanner_last_mode(self._h, C.byref(rate))
+        return {MODE_SPARSE: "sparse", MODE_EXACT: "exact"}.get(m, "none"), rate.value
+
+    def copy_pattern_counts(self, d_dst_ptr: int, stream: int = 0) -> None:
+        _check(_lib.acg().acg_scanner_copy_pattern_counts(self._h, C.c_void_p(d_dst_ptr), C.c_void_p(stream or None)))
+
+    def geometry(self) -> dict:
+        nc, cb, la = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        _check(_lib.acg().acg_scanner_last_geometry(self._h, C.byref(nc), C.byref(cb), C.byref(la)))
+        return {"n_chunks": nc.value, "chunk_bytes": cb.value, "launches": la.value}

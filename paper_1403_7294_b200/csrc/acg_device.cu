@@ -1,0 +1,871 @@
+// libacg.so: the C ABI of include/acg.h — host automaton, device DFA upload,
+// scanner workspace and the kernel pipeline
+//   sparse mode: K1s sparse_scan_kernel (truncated automaton, event log)
+//                K1f fixup_kernel<COUNT> (exact replay of cold excursions)
+//   exact mode:  K1x exact_scan_kernel<COUNT>
+//   K2 cub::DeviceScan       exclusive prefix of chunk counts -> record slots (u64)
+//   K3 compact + fixup_kernel<WRITE> / exact_scan_kernel<WRITE>: ordered packed records
+//   K4 pattern_counts_kernel per-pattern counts from per-state visits
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/acg.h"
+#include "automaton.hpp"
+#include "scan_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define ACG_CUDA(call)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) {                                                                    \
+            return fail(e_ == cudaErrorMemoryAllocation ? ACG_ERR_OUT_OF_MEMORY : ACG_ERR_CUDA,     \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+        }                                                                                           \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    std::size_t n = 0;  // capacity in elements
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t reserve(std::size_t want) {
+        if (want <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        const std::size_t cap = std::max<std::size_t>(want, 1);
+        cudaError_t e = cudaMalloc(&p, cap * sizeof(T));
+        if (e == cudaSuccess) n = cap;
+        return e;
+    }
+};
+
+struct DeviceDfa {
+    int device = 0;
+    std::shared_ptr<const acg::Dfa> dfa;
+    DevBuf<std::uint32_t> next, out_off, out_ids;
+    DevBuf<std::uint16_t> hot16, hotH, follows, follows_esc;
+    DevBuf<std::uint8_t> symmap;
+    std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
+    std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
+    int smem_optin = 0;
+    int num_sms = 0;
+};
+
+template <typename T>
+cudaError_t upload(DevBuf<T>& dst, const T* src, std::size_t n) {
+    cudaError_t e = dst.reserve(n);
+    if (e != cudaSuccess) return e;
+    if (n) e = cudaMemcpy(dst.p, src, n * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+}  // namespace
+
+struct acg_automaton {
+    acg::Nfa nfa;
+    std::uint32_t hot_limit = 0;  // max shared-memory rows (0 = as many as fit)
+    std::vector<std::uint64_t> profile;  // per NFA state visit counts on a sample (optional)
+    mutable std::mutex mu;
+    mutable std::map<int, std::shared_ptr<DeviceDfa>> dev;
+};
+
+struct acg_result {
+    std::vector<std::uint32_t> ids;
+    std::vector<std::uint64_t> ends;
+    std::vector<std::uint64_t> counts;
+    std::uint64_t follows = 0;
+};
+
+struct acg_scanner {
+    const acg_automaton* a = nullptr;
+    int device = 0;
+    std::uint32_t flags = 0;
+    std::shared_ptr<DeviceDfa> dd;
+    cudaStream_t stream = nullptr;       // own compute stream
+    cudaStream_t copy_stream = nullptr;  // H2D for run_host
+    std::vector<cudaEvent_t> piece_events;
+    cudaStream_t last = nullptr;
+    // workspace
+    DevBuf<std::uint32_t> active_list, scalars32;
+    DevBuf<unsigned long long> chunk_counts;  // scalars32[0] = active count
+    DevBuf<unsigned long long> chunk_offs, visits, counts, records, scalars64;  // [0]=follows [1..3]=digest
+    DevBuf<std::uint8_t> text;
+    DevBuf<std::uint8_t> cub_tmp;
+    unsigned long long* pinned = nullptr;  // 8 host words
+    // geometry of the last run
+    acg::kern::ScanArgs args{};
+    unsigned long long n_chunks = 0;
+    unsigned long long chunk = 0;
+    std::uint32_t launches = 0;
+    unsigned grid = 0;
+    bool have_run = false;
+    bool synced = false;
+    unsigned long long m_total = 0;
+    // tuning
+    std::uint32_t U = 0, tpb = acg::kern::kTPB;  // U = 0: per-mode default
+    std::uint32_t U_run = 4;  // interleave of the last run
+    unsigned long long chunk_override = 0;
+    // mode: requested (ACG_MODE_*), used by the last run, and the event rate seen
+    int mode_req = 0;
+    int mode_run = 0;
+    double last_event_rate = -1.0;
+    DevBuf<std::uint32_t> events, ev_count;
+    std::uint32_t ev_cap = 0;
+    // optional per-kernel timing (ACG_SCAN_PROFILE)
+    cudaEvent_t ev[6] = {};
+    float kernel_ms[5] = {};
+};
+
+namespace {
+
+std::size_t hot_budget(int smem_optin) {
+    // dynamic smem = hot table + 256-byte symbol map; keep 1 KiB slack
+    const long b = static_cast<long>(smem_optin) - 256 - 1024;
+    return b > 0 ? static_cast<std::size_t>(b) : 0;
+}
+
+int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa>* out) {
+    std::lock_guard<std::mutex> lock(a->mu);
+    auto it = a->dev.find(device);
+    if (it != a->dev.end()) {
+        *out = it->second;
+        return ACG_OK;
+    }
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+        cudaGetLastError();
+        return fail(ACG_ERR_NO_DEVICE, "no CUDA device available (libacg requires an sm_100 GPU)");
+    }
+    if (device < 0 || device >= count) return fail(ACG_ERR_NO_DEVICE, "device index out of range");
+    ACG_CUDA(cudaSetDevice(device));
+    auto dd = std::make_shared<DeviceDfa>();
+    dd->device = device;
+    ACG_CUDA(cudaDeviceGetAttribute(&dd->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    ACG_CUDA(cudaDeviceGetAttribute(&dd->num_sms, cudaDevAttrMultiProcessorCount, device));
+    auto dfa = std::make_shared<acg::Dfa>();
+    std::size_t budget = hot_budget(dd->smem_optin);
+    if (a->hot_limit) budget = std::min<std::size_t>(budget, (a->hot_limit + 1ull) * 2ull * 256ull);
+    acg::compile_dfa(a->nfa, budget, a->profile.empty() ? nullptr : &a->profile, *dfa, a->hot_limit);
+    dd->dfa = dfa;
+    const acg::Dfa& d = *dfa;
+    ACG_CUDA(upload(dd->next, d.next.data(), d.next.size()));
+    ACG_CUDA(upload(dd->out_off, d.out_off.data(), d.out_off.size()));
+    ACG_CUDA(upload(dd->out_ids, d.out_ids.data(), d.out_ids.size()));
+    ACG_CUDA(upload(dd->follows, d.follows.data(), d.follows.size()));
+    ACG_CUDA(upload(dd->follows_esc, d.follows_esc.data(), d.follows_esc.size()));
+    ACG_CUDA(upload(dd->symmap, d.symmap, 256));
+    // shared-memory images padded to 16 bytes for vector staging
+    dd->hot_bytes = static_cast<std::uint32_t>((d.hot16.size() * 2 + 15) & ~std::size_t(15));
+    std::vector<std::uint16_t> hot(dd->hot_bytes / 2, 0xFFFF);
+    std::copy(d.hot16.begin(), d.hot16.end(), hot.begin());
+    ACG_CUDA(upload(dd->hot16, hot.data(), hot.size()));
+    if (d.sparse_ok) {
+        dd->hotH_bytes = static_cast<std::uint32_t>((d.hotH.size() * 2 + 15) & ~std::size_t(15));
+        std::vector<std::uint16_t> hh(dd->hotH_bytes / 2, 0);
+        std::copy(d.hotH.begin(), d.hotH.end(), hh.begin());
+        ACG_CUDA(upload(dd->hotH, hh.data(), hh.size()));
+    }
+    a->dev[device] = dd;
+    *out = dd;
+    return ACG_OK;
+}
+
+using acg::kern::ScanArgs;
+
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_attr_smem;  // (kernel, device) -> configured opt-in smem
+
+template <typename Kern>
+cudaError_t prepare_smem(Kern k, std::size_t smem) {
+    // opt-in smem limit, configured once per (kernel, device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    int& have = g_attr_smem[{reinterpret_cast<const void*>(k), dev}];
+    if (have < static_cast<int>(smem)) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        have = static_cast<int>(smem);
+    }
+    return cudaSuccess;
+}
+
+template <int U, int MODE, int PASS, bool STATS>
+cudaError_t launch_exact(const ScanArgs& args, unsigned grid, unsigned tpb, std::size_t smem, cudaStream_t st) {
+    auto k = acg::kern::exact_scan_kernel<U, MODE, PASS, STATS>;
+    if (cudaError_t e = prepare_smem(k, smem)) return e;
+    k<<<grid, tpb, smem, st>>>(args);
+    return cudaGetLastError();
+}
+
+template <int MODE, int PASS>
+cudaError_t launch_exact_u(std::uint32_t U, const ScanArgs& args, unsigned grid, unsigned tpb, std::size_t smem,
+                           cudaStream_t st) {
+    switch (U) {
+        case 1: return launch_exact<1, MODE, PASS, false>(args, grid, tpb, smem, st);
+        case 2: return launch_exact<2, MODE, PASS, false>(args, grid, tpb, smem, st);
+        case 8: return launch_exact<8, MODE, PASS, false>(args, grid, tpb, smem, st);
+        default: return launch_exact<4, MODE, PASS, false>(args, grid, tpb, smem, st);
+    }
+}
+
+cudaError_t launch_exact_pass(int alpha, int pass, bool stats, std::uint32_t U, const ScanArgs& args, unsigned grid,
+                              unsigned tpb, std::size_t smem, cudaStream_t st) {
+    using namespace acg::kern;
+    if (stats)  // exact ScanStats: count pass only, interleave 2
+        return alpha == acg::kAlphaDna4 ? launch_exact<2, 0, kCount, true>(args, grid, tpb, smem, st)
+                                        : launch_exact<2, 1, kCount, true>(args, grid, tpb, smem, st);
+    if (alpha == acg::kAlphaDna4)
+        return pass == kCount ? launch_exact_u<0, kCount>(U, args, grid, tpb, smem, st)
+                              : launch_exact_u<0, kWrite>(U, args, grid, tpb, smem, st);
+    return pass == kCount ? launch_exact_u<1, kCount>(U, args, grid, tpb, smem, st)
+                          : launch_exact_u<1, kWrite>(U, args, grid, tpb, smem, st);
+}
+
+template <int U>
+cudaError_t launch_sparse(const ScanArgs& args, unsigned grid, unsigned tpb, std::size_t smem, cudaStream_t st) {
+    auto k = acg::kern::sparse_scan_kernel<U>;
+    if (cudaError_t e = prepare_smem(k, smem)) return e;
+    k<<<grid, tpb, smem, st>>>(args);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid, unsigned tpb, std::size_t smem,
+                            cudaStream_t st) {
+    switch (U) {
+        case 1: return launch_sparse<1>(args, grid, tpb, smem, st);
+        case 2: return launch_sparse<2>(args, grid, tpb, smem, st);
+        case 4: return launch_sparse<4>(args, grid, tpb, smem, st);
+        default: return launch_sparse<8>(args, grid, tpb, smem, st);
+    }
+}
+
+std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
+std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
+
+// Enqueue K3 (compaction + ordered write) for the current geometry.
+int enqueue_write(acg_scanner* s, cudaStream_t st) {
+    using namespace acg::kern;
+    const DeviceDfa& dd = *s->dd;
+    ACG_CUDA(cudaMemsetAsync(s->scalars32.p, 0, sizeof(std::uint32_t), st));
+    {
+        const unsigned tb = 256;
+        const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((s->n_chunks + tb - 1) / tb, 4096ull));
+        compact_active_kernel<<<std::max(g, 1u), tb, 0, st>>>(s->chunk_counts.p, static_cast<long long>(s->n_chunks),
+                                                               s->active_list.p, s->scalars32.p);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+    }
+    ScanArgs wa = s->args;
+    wa.records = s->records.p;
+    wa.rec_cap = s->records.n;
+    if (s->mode_run == ACG_MODE_SPARSE) {
+        const unsigned tb = 128;
+        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + tb - 1) / tb));
+        fixup_kernel<kWrite><<<g, tb, 0, st>>>(wa);
+        ACG_CUDA(cudaGetLastError());
+    } else {
+        ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
+    }
+    ++s->launches;
+    return ACG_OK;
+}
+
+// Chunk geometry for owned bytes [emit_from, n): one chunk per stream, all
+// streams of a full grid (one CTA per SM: the hot table takes the SM's smem).
+void plan_geometry(acg_scanner* s, std::uint64_t owned) {
+    const DeviceDfa& dd = *s->dd;
+    const unsigned long long streams = static_cast<unsigned long long>(dd.num_sms) * s->tpb * s->U_run;
+    const unsigned long long halo = dd.dfa->halo;
+    unsigned long long chunk = s->chunk_override;
+    if (!chunk) {
+        chunk = (owned + streams - 1) / streams;
+        chunk = std::max<unsigned long long>(chunk, std::max<unsigned long long>(256, 2 * halo));
+    }
+    chunk = (chunk + 15) & ~15ull;
+    s->chunk = chunk;
+    s->n_chunks = (owned + chunk - 1) / chunk;
+    const unsigned long long per_block = static_cast<unsigned long long>(s->tpb) * s->U_run;
+    s->grid = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + per_block - 1) / per_block));
+}
+
+int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std::uint64_t emit_from,
+                std::uint64_t base, cudaStream_t st) {
+    using namespace acg::kern;
+    if (emit_from > n) return fail(ACG_ERR_INVALID, "emit_from beyond the text");
+    if ((reinterpret_cast<std::uintptr_t>(d_text) & 15) || (emit_from & 15))
+        return fail(ACG_ERR_INVALID, "device text and emit_from must be 16-byte aligned");
+    ACG_CUDA(cudaSetDevice(s->device));
+    const DeviceDfa& dd = *s->dd;
+    const acg::Dfa& d = *dd.dfa;
+    const bool want_list = s->flags & ACG_SCAN_LIST;
+    const bool want_counts = s->flags & ACG_SCAN_COUNTS;
+    const bool stats = s->flags & ACG_SCAN_STATS;
+    s->launches = 0;
+    s->synced = false;
+    s->last = st;
+    const std::uint64_t owned = n - emit_from;
+    // mode: sparse (truncated automaton + fix-up) when the automaton allows it
+    // and excursions were rare on the previous run; exact otherwise
+    int mode = s->mode_req;
+    if (stats || !d.sparse_ok) mode = ACG_MODE_EXACT;
+    if (mode == ACG_MODE_AUTO)
+        mode = (s->last_event_rate < 0 || s->last_event_rate < 0.08) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
+    s->mode_run = mode;
+    s->U_run = stats ? 2u : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 8u : 4u));
+    plan_geometry(s, owned);
+    const bool prof = s->flags & ACG_SCAN_PROFILE;
+
+    const std::uint32_t n_out_states = (d.H - d.Hn) + (d.S - d.Cn);
+    ACG_CUDA(s->chunk_counts.reserve(s->n_chunks));
+    ACG_CUDA(s->chunk_offs.reserve(s->n_chunks + 1));
+    ACG_CUDA(s->active_list.reserve(s->n_chunks));
+    ACG_CUDA(s->visits.reserve(n_out_states));
+    ACG_CUDA(s->counts.reserve(d.out_ids.empty() ? 1 : s->a->nfa.n_patterns));
+    if (!s->records.p) ACG_CUDA(s->records.reserve(1u << 20));
+    std::size_t cub_bytes = 0;
+    const unsigned long long* in_it = s->chunk_counts.p;
+    cub::DeviceScan::InclusiveSum(nullptr, cub_bytes, in_it, s->chunk_offs.p + 1, static_cast<int>(std::max<unsigned long long>(s->n_chunks, 1)), st);
+    ACG_CUDA(s->cub_tmp.reserve(cub_bytes));
+
+    ACG_CUDA(cudaMemsetAsync(s->scalars64.p, 0, 5 * sizeof(unsigned long long), st));
+    ACG_CUDA(cudaMemsetAsync(s->chunk_offs.p, 0, sizeof(unsigned long long), st));
+    if (want_counts) {
+        ACG_CUDA(cudaMemsetAsync(s->visits.p, 0, std::max<std::size_t>(n_out_states, 1) * sizeof(unsigned long long), st));
+        ACG_CUDA(cudaMemsetAsync(s->counts.p, 0, s->a->nfa.n_patterns * sizeof(unsigned long long), st));
+    }
+    if (s->n_chunks == 0) {
+        s->args = ScanArgs{};
+        s->have_run = true;
+        s->mode_run = mode;
+        return ACG_OK;
+    }
+
+    ScanArgs& a = s->args;
+    a = ScanArgs{};
+    a.text = d_text;
+    a.n = static_cast<long long>(n);
+    a.emit_from = static_cast<long long>(emit_from);
+    a.base = base;
+    a.chunk = static_cast<long long>(s->chunk);
+    a.halo = static_cast<int>(d.halo);
+    a.n_chunks = static_cast<long long>(s->n_chunks);
+    a.next = dd.next.p;
+    a.hot16 = dd.hot16.p;
+    a.out_off = dd.out_off.p;
+    a.out_ids = dd.out_ids.p;
+    a.follows = dd.follows.p;
+    a.follows_esc = dd.follows_esc.p;
+    a.symmap = dd.symmap.p;
+    a.K = d.K;
+    a.H = d.H;
+    a.Hn = d.Hn;
+    a.Cn = d.Cn;
+    a.smem_table_bytes = mode == ACG_MODE_SPARSE ? dd.hotH_bytes : dd.hot_bytes;
+    a.hotH = dd.hotH.p;
+    a.chunk_counts = s->chunk_counts.p;
+    a.active_list = s->active_list.p;
+    a.active_count = s->scalars32.p;
+    a.chunk_offs = s->chunk_offs.p;
+    a.visits = want_counts ? s->visits.p : nullptr;
+    a.records = s->records.p;
+    a.rec_cap = s->records.n;
+    a.id_bits = d.id_bits;
+    a.follows_total = stats ? s->scalars64.p : nullptr;
+
+    // K1: count pass
+    if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
+    if (mode == ACG_MODE_SPARSE) {
+        const unsigned long long walk = s->chunk + d.halo;
+        s->ev_cap = static_cast<std::uint32_t>(std::min<unsigned long long>(walk / 16 + 32, walk));
+        ACG_CUDA(s->events.reserve(s->n_chunks * s->ev_cap * 2ull));
+        ACG_CUDA(s->ev_count.reserve(s->n_chunks));
+        a.events = s->events.p;
+        a.ev_count = s->ev_count.p;
+        a.ev_cap = s->ev_cap;
+        a.ev_total = s->scalars64.p + 4;
+        ACG_CUDA(launch_sparse_u(s->U_run, a, s->grid, s->tpb, smem_sparse(dd), st));
+        ++s->launches;
+        if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+        const unsigned tb = 128;
+        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + tb - 1) / tb));
+        fixup_kernel<kCount><<<g, tb, 0, st>>>(a);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+    } else {
+        ACG_CUDA(launch_exact_pass(d.mode, kCount, stats, s->U_run, a, s->grid, s->tpb, smem_bytes(dd), st));
+        ++s->launches;
+        if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+    }
+    if (prof) ACG_CUDA(cudaEventRecord(s->ev[2], st));
+    // K2: record slots = inclusive prefix of the chunk counts, shifted by one (CUB, not counted in launches)
+    std::size_t tmp = s->cub_tmp.n;
+    ACG_CUDA(cub::DeviceScan::InclusiveSum(s->cub_tmp.p, tmp, in_it, s->chunk_offs.p + 1,
+                                           static_cast<int>(s->n_chunks), st));
+    if (prof) ACG_CUDA(cudaEventRecord(s->ev[3], st));
+    // K3: ordered records
+    if (want_list) {
+        const int rc = enqueue_write(s, st);
+        if (rc) return rc;
+    }
+    if (prof) ACG_CUDA(cudaEventRecord(s->ev[4], st));
+    // K4: per-pattern counts
+    if (want_counts && n_out_states) {
+        const unsigned tb = 256;
+        const unsigned g = std::min<unsigned>((n_out_states + tb - 1) / tb, 8 * dd.num_sms);
+        pattern_counts_kernel<<<g, tb, 0, st>>>(s->visits.p, dd.out_off.p, dd.out_ids.p, d.Hn, d.H, d.Cn, d.S,
+                                                s->counts.p);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+    }
+    if (prof) ACG_CUDA(cudaEventRecord(s->ev[5], st));
+    s->have_run = true;
+    return ACG_OK;
+}
+
+int scanner_sync(acg_scanner* s) {
+    if (!s->have_run) return fail(ACG_ERR_INVALID, "no scan has been run");
+    if (s->synced) return ACG_OK;
+    ACG_CUDA(cudaSetDevice(s->device));
+    cudaStream_t st = s->last;
+    ACG_CUDA(cudaMemcpyAsync(s->pinned, s->chunk_offs.p + s->n_chunks, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st));
+    ACG_CUDA(cudaMemcpyAsync(s->pinned + 5, s->scalars64.p + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             st));
+    ACG_CUDA(cudaStreamSynchronize(st));
+    s->m_total = s->n_chunks ? s->pinned[0] : 0;
+    if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
+        const double walked = static_cast<double>(s->n_chunks) * static_cast<double>(s->chunk + s->dd->dfa->halo);
+        s->last_event_rate = static_cast<double>(s->pinned[5]) / walked;
+    }
+    if ((s->flags & ACG_SCAN_LIST) && s->m_total > s->records.n) {
+        // record buffer overflowed: grow and re-emit (chunk counts and offsets are final)
+        ACG_CUDA(s->records.reserve(s->m_total + s->m_total / 4));
+        const int rc = enqueue_write(s, st);
+        if (rc) return rc;
+        ACG_CUDA(cudaStreamSynchronize(st));
+    }
+    if ((s->flags & ACG_SCAN_PROFILE) && s->n_chunks) {
+        for (int i = 0; i < 5; ++i) ACG_CUDA(cudaEventElapsedTime(&s->kernel_ms[i], s->ev[i], s->ev[i + 1]));
+    }
+    s->synced = true;
+    return ACG_OK;
+}
+
+int make_scanner(const acg_automaton* a, int device, std::uint32_t flags, acg_scanner** out) {
+    auto s = std::make_unique<acg_scanner>();
+    s->a = a;
+    s->device = device;
+    s->flags = flags;
+    if (const int rc = get_device_dfa(a, device, &s->dd)) return rc;
+    ACG_CUDA(cudaSetDevice(device));
+    ACG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    ACG_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    ACG_CUDA(cudaMallocHost(&s->pinned, 8 * sizeof(unsigned long long)));
+    ACG_CUDA(s->scalars32.reserve(4));
+    ACG_CUDA(s->scalars64.reserve(8));
+    ACG_CUDA(cudaMemset(s->scalars64.p, 0, 8 * sizeof(unsigned long long)));
+    if (flags & ACG_SCAN_PROFILE)
+        for (auto& e : s->ev) ACG_CUDA(cudaEventCreate(&e));
+    *out = s.release();
+    return ACG_OK;
+}
+
+void free_scanner(acg_scanner* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->last) cudaStreamSynchronize(s->last);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    if (s->pinned) cudaFreeHost(s->pinned);
+    for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    delete s;
+}
+
+// Scanner pool per automaton for the one-shot acg_scan (keeps device
+// workspace across calls; one scanner per concurrent caller).
+struct PoolKey {
+    const acg_automaton* a;
+    int device;
+    std::uint32_t flags;
+    bool operator<(const PoolKey& o) const {
+        if (a != o.a) return a < o.a;
+        if (device != o.device) return device < o.device;
+        return flags < o.flags;
+    }
+};
+std::mutex g_pool_mu;
+std::map<PoolKey, std::vector<acg_scanner*>> g_pool;
+
+acg_scanner* pool_take(const acg_automaton* a, int device, std::uint32_t flags) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    auto& v = g_pool[PoolKey{a, device, flags}];
+    if (v.empty()) return nullptr;
+    acg_scanner* s = v.back();
+    v.pop_back();
+    return s;
+}
+void pool_give(acg_scanner* s) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    auto& v = g_pool[PoolKey{s->a, s->device, s->flags}];
+    if (v.size() < 8) v.push_back(s);
+    else free_scanner(s);
+}
+void pool_drop(const acg_automaton* a) {
+    std::vector<acg_scanner*> dead;
+    {
+        std::lock_guard<std::mutex> lock(g_pool_mu);
+        for (auto it = g_pool.begin(); it != g_pool.end();) {
+            if (it->first.a == a) {
+                dead.insert(dead.end(), it->second.begin(), it->second.end());
+                it = g_pool.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    for (acg_scanner* s : dead) free_scanner(s);
+}
+
+int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* acg_last_error(void) { return g_last_error.c_str(); }
+const char* acg_version(void) { return "acg 0.1 (sm_100a)"; }
+
+int acg_build(const std::uint8_t* concat, const std::uint64_t* offsets, std::uint32_t n_patterns, acg_automaton** out) {
+    if (!out) return fail(ACG_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    if (n_patterns == 0) return fail(ACG_ERR_EMPTY_DICTIONARY, "dictionary is empty");
+    if (!offsets || (!concat && offsets[n_patterns] != 0)) return fail(ACG_ERR_INVALID, "null pattern buffers");
+    for (std::uint32_t i = 0; i < n_patterns; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(ACG_ERR_INVALID, "pattern offsets must be non-decreasing");
+    auto a = std::make_unique<acg_automaton>();
+    try {
+        const int rc = acg::build_nfa(concat, offsets, n_patterns, a->nfa);
+        if (rc == acg::kErrEmptyPattern) {
+            std::uint32_t i = 0;
+            while (offsets[i + 1] != offsets[i]) ++i;
+            return fail(rc, "pattern " + std::to_string(i) + " is empty");
+        }
+        if (rc == acg::kErrEmptyDictionary) return fail(rc, "dictionary is empty");
+        if (rc != acg::kOk) return fail(rc, "invalid dictionary");
+    } catch (const std::bad_alloc&) {
+        return fail(ACG_ERR_OUT_OF_MEMORY, "host allocation failed while building the automaton");
+    }
+    *out = a.release();
+    return ACG_OK;
+}
+
+void acg_automaton_destroy(acg_automaton* a) {
+    if (!a) return;
+    pool_drop(a);
+    delete a;
+}
+
+std::uint32_t acg_state_count(const acg_automaton* a) { return a->nfa.state_count(); }
+std::uint32_t acg_pattern_count(const acg_automaton* a) { return a->nfa.n_patterns; }
+std::uint32_t acg_max_pattern_length(const acg_automaton* a) { return a->nfa.max_len; }
+int acg_goto_transition(const acg_automaton* a, std::uint32_t s, std::uint8_t b, std::uint32_t* to) {
+    std::uint32_t t = 0;
+    const bool ok = a->nfa.goto_transition(s, b, &t);
+    if (ok && to) *to = t;
+    return ok ? 1 : 0;
+}
+std::uint32_t acg_transitions(const acg_automaton* a, std::uint32_t s, const std::uint8_t** bytes,
+                              const std::uint32_t** targets) {
+    const std::uint32_t lo = a->nfa.edge_off[s], hi = a->nfa.edge_off[s + 1];
+    if (bytes) *bytes = a->nfa.edge_byte.data() + lo;
+    if (targets) *targets = a->nfa.edge_to.data() + lo;
+    return hi - lo;
+}
+std::uint32_t acg_failure(const acg_automaton* a, std::uint32_t s) { return a->nfa.fail[s]; }
+std::uint32_t acg_outputs(const acg_automaton* a, std::uint32_t s, const std::uint32_t** ids) {
+    const std::uint32_t lo = a->nfa.out_off[s], hi = a->nfa.out_off[s + 1];
+    if (ids) *ids = a->nfa.out_ids.data() + lo;
+    return hi - lo;
+}
+std::uint32_t acg_depth(const acg_automaton* a, std::uint32_t s) { return a->nfa.depth[s]; }
+std::uint32_t acg_next_state(const acg_automaton* a, std::uint32_t s, std::uint8_t b) {
+    return a->nfa.next_state(s, b);
+}
+
+int acg_optimize_layout(acg_automaton* a, const std::uint8_t* sample, std::uint64_t n) {
+    if (!a || (!sample && n)) return fail(ACG_ERR_INVALID, "null argument");
+    {
+        std::lock_guard<std::mutex> lock(a->mu);
+        if (!a->dev.empty()) return fail(ACG_ERR_INVALID, "layout is fixed once the automaton has been scanned");
+    }
+    // walk the reference transition function over the sample, counting visits
+    const acg::Nfa& nfa = a->nfa;
+    std::vector<std::uint64_t> visits(nfa.state_count(), 0);
+    std::uint32_t s = 0;
+    for (std::uint64_t i = 0; i < n; ++i) {
+        s = nfa.next_state(s, sample[i]);
+        ++visits[s];
+    }
+    a->profile = std::move(visits);
+    return ACG_OK;
+}
+
+int acg_set_hot_limit(acg_automaton* a, std::uint32_t max_hot_rows) {
+    if (!a) return fail(ACG_ERR_INVALID, "null automaton");
+    std::lock_guard<std::mutex> lock(a->mu);
+    if (!a->dev.empty()) return fail(ACG_ERR_INVALID, "layout is fixed once the automaton has been scanned");
+    a->hot_limit = max_hot_rows;
+    return ACG_OK;
+}
+
+int acg_automaton_layout(const acg_automaton* a, std::uint32_t* n_states, std::uint32_t* hot_rows,
+                         std::uint32_t* columns, std::uint32_t* halo, int* alphabet_mode) {
+    std::shared_ptr<DeviceDfa> dd;
+    if (const int rc = get_device_dfa(a, current_device(), &dd)) return rc;
+    const acg::Dfa& d = *dd->dfa;
+    if (n_states) *n_states = d.S;
+    if (hot_rows) *hot_rows = d.H;
+    if (columns) *columns = d.K;
+    if (halo) *halo = d.halo;
+    if (alphabet_mode) *alphabet_mode = d.mode;
+    return ACG_OK;
+}
+
+int acg_scanner_create(const acg_automaton* a, int device, std::uint32_t flags, acg_scanner** out) {
+    if (!a || !out) return fail(ACG_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (device < 0) device = current_device();
+    if ((flags & ~ACG_SCAN_PROFILE) == 0) flags |= ACG_SCAN_LIST | ACG_SCAN_COUNTS;
+    return make_scanner(a, device, flags, out);
+}
+
+void acg_scanner_destroy(acg_scanner* s) { free_scanner(s); }
+
+int acg_scanner_set_geometry(acg_scanner* s, std::uint32_t streams_per_thread, std::uint32_t threads_per_block,
+                             std::uint64_t chunk_bytes) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (streams_per_thread) {
+        if (streams_per_thread != 1 && streams_per_thread != 2 && streams_per_thread != 4 && streams_per_thread != 8)
+            return fail(ACG_ERR_INVALID, "streams per thread must be 1, 2, 4 or 8");
+        s->U = streams_per_thread;
+    }
+    if (threads_per_block) {
+        if (threads_per_block % 32 || threads_per_block > static_cast<std::uint32_t>(acg::kern::kTPB))
+            return fail(ACG_ERR_INVALID, "threads per block must be a multiple of 32, at most 512");
+        s->tpb = threads_per_block;
+    }
+    s->chunk_override = chunk_bytes;
+    return ACG_OK;
+}
+
+int acg_scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std::uint64_t emit_from,
+                    std::uint64_t base_offset, void* stream) {
+    if (!s || (!d_text && n)) return fail(ACG_ERR_INVALID, "null argument");
+    return scanner_run(s, d_text, n, emit_from, base_offset, stream ? static_cast<cudaStream_t>(stream) : s->stream);
+}
+
+int acg_scanner_run_host(acg_scanner* s, const std::uint8_t* h_text, std::uint64_t n, void* stream) {
+    if (!s || (!h_text && n)) return fail(ACG_ERR_INVALID, "null argument");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    ACG_CUDA(cudaSetDevice(s->device));
+    ACG_CUDA(s->text.reserve(std::max<std::uint64_t>(n, 16)));
+    if (n) ACG_CUDA(cudaMemcpyAsync(s->text.p, h_text, n, cudaMemcpyHostToDevice, st));
+    return scanner_run(s, s->text.p, n, 0, 0, st);
+}
+
+int acg_scanner_sync(acg_scanner* s) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    return scanner_sync(s);
+}
+
+std::uint64_t acg_scanner_match_count(acg_scanner* s) {
+    if (!s || scanner_sync(s)) return 0;
+    return s->m_total;
+}
+
+int acg_scanner_packed_records(acg_scanner* s, std::uint64_t* host, std::uint64_t cap, std::uint32_t* id_bits) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (!(s->flags & ACG_SCAN_LIST)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_LIST");
+    if (const int rc = scanner_sync(s)) return rc;
+    if (id_bits) *id_bits = s->dd->dfa->id_bits;
+    const std::uint64_t m = std::min<std::uint64_t>(cap, s->m_total);
+    if (m) ACG_CUDA(cudaMemcpy(host, s->records.p, m * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+    return ACG_OK;
+}
+
+int acg_scanner_records(acg_scanner* s, std::uint32_t* ids, std::uint64_t* ends, std::uint64_t cap) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (const int rc = scanner_sync(s)) return rc;
+    const std::uint64_t m = std::min<std::uint64_t>(cap, s->m_total);
+    std::vector<std::uint64_t> packed(m);
+    std::uint32_t bits = 0;
+    if (const int rc = acg_scanner_packed_records(s, packed.data(), m, &bits)) return rc;
+    const std::uint64_t mask = (1ull << bits) - 1;
+    for (std::uint64_t i = 0; i < m; ++i) {
+        ids[i] = static_cast<std::uint32_t>(packed[i] & mask);
+        ends[i] = packed[i] >> bits;
+    }
+    return ACG_OK;
+}
+
+int acg_scanner_pattern_counts(acg_scanner* s, std::uint64_t* host_counts) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (!(s->flags & ACG_SCAN_COUNTS)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_COUNTS");
+    if (const int rc = scanner_sync(s)) return rc;
+    ACG_CUDA(cudaMemcpy(host_counts, s->counts.p, s->a->nfa.n_patterns * sizeof(std::uint64_t),
+                        cudaMemcpyDeviceToHost));
+    return ACG_OK;
+}
+
+const std::uint64_t* acg_scanner_device_pattern_counts(acg_scanner* s) {
+    return s ? reinterpret_cast<const std::uint64_t*>(s->counts.p) : nullptr;
+}
+
+const std::uint64_t* acg_scanner_device_records(acg_scanner* s, std::uint32_t* id_bits) {
+    if (!s) return nullptr;
+    if (id_bits) *id_bits = s->dd->dfa->id_bits;
+    return reinterpret_cast<const std::uint64_t*>(s->records.p);
+}
+
+std::uint64_t acg_scanner_failure_follows(acg_scanner* s) {
+    if (!s || scanner_sync(s)) return 0;
+    if (cudaMemcpy(s->pinned + 4, s->scalars64.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return s->pinned[4];
+}
+
+int acg_scanner_digest(acg_scanner* s, std::uint64_t* dsum, std::uint64_t* dxor, std::uint64_t* unsorted_pairs) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (const int rc = scanner_sync(s)) return rc;
+    ACG_CUDA(cudaMemset(s->scalars64.p + 1, 0, 3 * sizeof(unsigned long long)));
+    if (s->m_total) {
+        const unsigned g = std::min<unsigned long long>((s->m_total + 255) / 256, 4096ull);
+        acg::kern::digest_kernel<<<g, 256, 0, s->last>>>(s->records.p, s->m_total, s->dd->dfa->id_bits,
+                                                          s->scalars64.p + 1);
+        ACG_CUDA(cudaGetLastError());
+    }
+    ACG_CUDA(cudaMemcpyAsync(s->pinned + 1, s->scalars64.p + 1, 3 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s->last));
+    ACG_CUDA(cudaStreamSynchronize(s->last));
+    if (dsum) *dsum = s->pinned[1];
+    if (dxor) *dxor = s->pinned[2];
+    if (unsorted_pairs) *unsorted_pairs = s->pinned[3];
+    return ACG_OK;
+}
+
+int acg_scanner_kernel_ms(acg_scanner* s, float* ms5) {
+    if (!s || !ms5) return fail(ACG_ERR_INVALID, "null argument");
+    if (!(s->flags & ACG_SCAN_PROFILE)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_PROFILE");
+    if (const int rc = scanner_sync(s)) return rc;
+    for (int i = 0; i < 5; ++i) ms5[i] = s->kernel_ms[i];
+    return ACG_OK;
+}
+
+int acg_scanner_set_mode(acg_scanner* s, int mode) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (mode < ACG_MODE_AUTO || mode > ACG_MODE_EXACT) return fail(ACG_ERR_INVALID, "unknown mode");
+    s->mode_req = mode;
+    return ACG_OK;
+}
+
+int acg_scanner_last_mode(acg_scanner* s, double* event_rate) {
+    if (!s) return -1;
+    if (event_rate) *event_rate = s->last_event_rate;
+    return s->mode_run;
+}
+
+int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream) {
+    if (!s || !d_dst) return fail(ACG_ERR_INVALID, "null argument");
+    if (!(s->flags & ACG_SCAN_COUNTS)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_COUNTS");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->last;
+    ACG_CUDA(cudaMemcpyAsync(d_dst, s->counts.p, s->a->nfa.n_patterns * sizeof(std::uint64_t),
+                             cudaMemcpyDeviceToDevice, st));
+    return ACG_OK;
+}
+
+int acg_scanner_last_geometry(acg_scanner* s, std::uint64_t* n_chunks, std::uint64_t* chunk_bytes,
+                              std::uint32_t* launches) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (n_chunks) *n_chunks = s->n_chunks;
+    if (chunk_bytes) *chunk_bytes = s->chunk;
+    if (launches) *launches = s->launches;
+    return ACG_OK;
+}
+
+int acg_scan(const acg_automaton* a, const std::uint8_t* text, std::uint64_t n, std::uint32_t flags,
+             acg_result** out) {
+    if (!a || !out || (!text && n)) return fail(ACG_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (!flags) flags = ACG_SCAN_LIST;
+    const int device = current_device();
+    acg_scanner* s = pool_take(a, device, flags);
+    if (!s) {
+        if (const int rc = make_scanner(a, device, flags, &s)) return rc;
+    }
+    auto res = std::make_unique<acg_result>();
+    int rc = acg_scanner_run_host(s, text, n, nullptr);
+    if (!rc) rc = scanner_sync(s);
+    if (!rc && (flags & ACG_SCAN_LIST)) {
+        res->ids.resize(s->m_total);
+        res->ends.resize(s->m_total);
+        rc = acg_scanner_records(s, res->ids.data(), res->ends.data(), s->m_total);
+    }
+    if (!rc && (flags & ACG_SCAN_COUNTS)) {
+        res->counts.resize(a->nfa.n_patterns);
+        rc = acg_scanner_pattern_counts(s, res->counts.data());
+    }
+    if (!rc && (flags & ACG_SCAN_STATS)) res->follows = acg_scanner_failure_follows(s);
+    if (rc) {
+        free_scanner(s);
+        return rc;
+    }
+    pool_give(s);
+    *out = res.release();
+    return ACG_OK;
+}
+
+std::uint64_t acg_result_match_count(const acg_result* r) { return r ? r->ids.size() : 0; }
+const std::uint32_t* acg_result_ids(const acg_result* r) { return r ? r->ids.data() : nullptr; }
+const std::uint64_t* acg_result_ends(const acg_result* r) { return r ? r->ends.data() : nullptr; }
+const std::uint64_t* acg_result_pattern_counts(const acg_result* r) {
+    return r && !r->counts.empty() ? r->counts.data() : nullptr;
+}
+std::uint64_t acg_result_failure_follows(const acg_result* r) { return r ? r->follows : 0; }
+void acg_result_destroy(acg_result* r) { delete r; }
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// Host-side pattern-matching machine (NFA view) and its dense-DFA image.
+//
+// The NFA is built with the reference's algorithm so that every public
+// observable matches it: DFS-preorder state numbering with children in
+// insertion order, BFS failure links, sorted suffix-closed output sets
+// (reference: proj/include/acmatch/aho_corasick.hpp:130-233). The DFA image is
+// the device's private representation: a dense transition table over symbol
+// classes, states renumbered for locality, plus a CSR of output ids. Its
+// numbering never leaks through the API.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace acg {
+
+using StateId = std::uint32_t;
+
+struct Nfa {
+    // CSR goto edges sorted by byte (aho_corasick.hpp:104-105)
+    std::vector<std::uint32_t> edge_off;  // S+1
+    std::vector<std::uint8_t> edge_byte;
+    std::vector<StateId> edge_to;
+    std::vector<StateId> fail;         // aho_corasick.hpp:106
+    std::vector<std::uint32_t> depth;  // :107
+    std::vector<std::uint32_t> out_off;  // S+1, suffix-closed, ascending (:108)
+    std::vector<std::uint32_t> out_ids;
+    std::vector<std::uint32_t> bfs;      // states in BFS order (root first)
+    StateId root_row[256];               // :115-117
+    std::uint32_t n_patterns = 0;
+    std::uint32_t max_len = 0;
+
+    std::uint32_t state_count() const { return static_cast<std::uint32_t>(fail.size()); }
+    bool goto_transition(StateId s, std::uint8_t b, StateId* out) const;
+    StateId next_state(StateId s, std::uint8_t b) const;
+};
+
+// Error codes shared with the C ABI (include/acg.h).
+enum : int {
+    kOk = 0,
+    kErrEmptyDictionary = 1,
+    kErrEmptyPattern = 2,
+    kErrInvalid = 3,
+    kErrInvalidWorkerCount = 4,
+    kErrCuda = 5,
+    kErrOutOfMemory = 6,
+    kErrNoDevice = 7,
+};
+
+// build: reference aho_corasick.hpp:130-233. Returns an error code.
+int build_nfa(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count, Nfa& out);
+
+// Alphabet modes of the device scan.
+enum AlphaMode : int {
+    kAlphaDna4 = 0,     // pattern bytes ⊆ {A,C,G,T}: column = (byte>>1)&3, others escape
+    kAlphaGeneric = 1,  // column = symmap[byte]; escape column K maps every state to the root
+};
+
+struct Dfa {
+    int mode = kAlphaGeneric;
+    std::uint32_t K = 0;        // table row stride (columns); generic mode includes the escape column
+    std::uint32_t n_sym = 0;    // distinct pattern bytes
+    std::uint8_t symmap[256];   // byte -> column (generic mode); escape = K-1
+    std::uint32_t S = 0;
+    // device numbering: [0,Hn) hot non-output, [Hn,H) hot output, [H,Cn) cold non-output, [Cn,S) cold output
+    std::uint32_t H = 0, Hn = 0, Cn = 0;
+    std::vector<std::uint32_t> dev_of;   // NFA id -> device id
+    std::vector<std::uint32_t> nfa_of;   // device id -> NFA id
+    std::vector<std::uint32_t> next;     // S*K, device ids
+    std::vector<std::uint16_t> hot16;    // (H+1)*K, u16 device ids, 0xFFFF = consult `next`; row H all 0xFFFF
+    // Truncated automaton over the hot set (sparse mode; dna4, BFS-ordered hot
+    // set only): hotH[s*K+c] = longest hot suffix of s.c, | 0x8000 when the
+    // true target is cold or has outputs (the step must be replayed exactly).
+    std::vector<std::uint16_t> hotH;     // H*K
+    bool sparse_ok = false;
+    std::vector<std::uint32_t> out_off;  // S+1 in device order
+    std::vector<std::uint32_t> out_ids;  // ascending per state
+    std::vector<std::uint16_t> follows;  // S*K failure follows taken by the reference scan on (s, column)
+    std::vector<std::uint16_t> follows_esc;  // per state, for bytes outside the pattern alphabet (dna4 mode)
+    std::uint32_t id_bits = 1;           // bits for a pattern id in a packed record
+    std::uint32_t halo = 0;              // round_up(max_len, 16): warm-up bytes before each chunk
+};
+
+// Fold the NFA into the dense DFA image. `hot_budget_bytes` bounds the u16 hot
+// table kept in shared memory. `visits` (optional, NFA order) gives
+// profile-guided hotness; otherwise BFS order is used.
+void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& out,
+                 std::uint32_t hot_limit = 0);
+
+}  // namespace acg

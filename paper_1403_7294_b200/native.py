@@ -1,0 +1,71 @@
+"""In-tree build of the native libraries (sm_100a only).
+
+    lib/libacg.so        the product: C ABI of include/acg.h (host automaton + CUDA scan)
+    lib/libacg_synth.so  deterministic synthetic corpora for the BASELINE workloads
+
+Run `python -m paper_1403_7294_b200.native` (or __graft_entry__.build()).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "lib")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd: list[str]) -> None:
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build(force: bool = False, verbose_ptxas: bool = False) -> None:
+    os.makedirs(LIB, exist_ok=True)
+    obj = os.path.join(LIB, "obj")
+    os.makedirs(obj, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    synth = os.path.join(LIB, "libacg_synth.so")
+    src = os.path.join(CSRC, "synth.cpp")
+    if force or _stale(synth, [src]):
+        _run(["g++", "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", synth, src])
+
+    headers = [os.path.join(CSRC, h) for h in ("automaton.hpp", "scan_kernels.cuh")] + [
+        os.path.join(ROOT, "include", "acg.h")]
+    auto_src = os.path.join(CSRC, "automaton.cpp")
+    auto_o = os.path.join(obj, "automaton.o")
+    if force or _stale(auto_o, [auto_src] + headers):
+        _run(["g++", "-std=c++17", "-O3", "-fPIC", "-c", "-o", auto_o, auto_src] + inc)
+    dev_src = os.path.join(CSRC, "acg_device.cu")
+    dev_o = os.path.join(obj, "acg_device.o")
+    if force or _stale(dev_o, [dev_src] + headers):
+        cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", "-o", dev_o, dev_src] + inc
+        if verbose_ptxas:
+            cmd.insert(1, "-Xptxas=-v")
+        _run(cmd)
+    lib = os.path.join(LIB, "libacg.so")
+    if force or _stale(lib, [auto_o, dev_o]):
+        _run([NVCC, *ARCH, "-shared", "-o", lib, auto_o, dev_o, "-Xcompiler", "-pthread"])
+
+
+def build_oracle() -> None:
+    """Test infrastructure: the C restatement and (when /root/reference is
+    present) the reference compiled into oracle/_ref/."""
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)
+    build_oracle()
