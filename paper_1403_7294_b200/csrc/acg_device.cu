@@ -67,7 +67,7 @@ struct DevBuf {
 struct DeviceDfa {
     int device = 0;
     std::shared_ptr<const acg::Dfa> dfa;
-    DevBuf<std::uint32_t> next, out_off, out_ids;
+    DevBuf<std::uint32_t> next, out_off, out_ids, depth;
     DevBuf<std::uint16_t> hot16, hotH, follows, follows_esc;
     DevBuf<std::uint8_t> symmap;
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
@@ -129,6 +129,7 @@ struct acg_scanner {
     // tuning
     std::uint32_t U = 0, tpb = acg::kern::kTPB;  // U = 0: per-mode default
     std::uint32_t U_run = 4;  // interleave of the last run
+    std::uint32_t tpb_run = acg::kern::kTPB;
     unsigned long long chunk_override = 0;
     // mode: requested (ACG_MODE_*), used by the last run, and the event rate seen
     int mode_req = 0;
@@ -176,6 +177,7 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
     ACG_CUDA(upload(dd->next, d.next.data(), d.next.size()));
     ACG_CUDA(upload(dd->out_off, d.out_off.data(), d.out_off.size()));
     ACG_CUDA(upload(dd->out_ids, d.out_ids.data(), d.out_ids.size()));
+    ACG_CUDA(upload(dd->depth, d.depth.data(), d.depth.size()));
     ACG_CUDA(upload(dd->follows, d.follows.data(), d.follows.size()));
     ACG_CUDA(upload(dd->follows_esc, d.follows_esc.data(), d.follows_esc.size()));
     ACG_CUDA(upload(dd->symmap, d.symmap, 256));
@@ -247,11 +249,34 @@ cudaError_t launch_exact_pass(int alpha, int pass, bool stats, std::uint32_t U, 
                           : launch_exact_u<1, kWrite>(U, args, grid, tpb, smem, st);
 }
 
+constexpr unsigned sparse_tpb(unsigned U) { return U == 1 ? 1024u : 512u; }
+
 template <int U>
 cudaError_t launch_sparse(const ScanArgs& args, unsigned grid, unsigned tpb, std::size_t smem, cudaStream_t st) {
-    auto k = acg::kern::sparse_scan_kernel<U>;
+    auto k = acg::kern::sparse_scan_kernel<U, (U <= 2 ? 4 : 2), sparse_tpb(U)>;
     if (cudaError_t e = prepare_smem(k, smem)) return e;
     k<<<grid, tpb, smem, st>>>(args);
+    return cudaGetLastError();
+}
+
+constexpr unsigned kFixupTPB = 1024;  // 32 warps, one chunk per warp
+
+cudaError_t launch_fixup(int pass, const ScanArgs& args, unsigned long long n_work_max, std::size_t smem,
+                         cudaStream_t st) {
+    using namespace acg::kern;
+    const unsigned long long warps = kFixupTPB / 32;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = static_cast<unsigned>(
+        std::max<unsigned long long>(1, std::min<unsigned long long>((n_work_max + warps - 1) / warps, sms)));
+    if (pass == kCount) {
+        if (cudaError_t e = prepare_smem(fixup_kernel<kCount>, smem)) return e;
+        fixup_kernel<kCount><<<g, kFixupTPB, smem, st>>>(args);
+    } else {
+        if (cudaError_t e = prepare_smem(fixup_kernel<kWrite>, smem)) return e;
+        fixup_kernel<kWrite><<<g, kFixupTPB, smem, st>>>(args);
+    }
     return cudaGetLastError();
 }
 
@@ -282,13 +307,13 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         ++s->launches;
     }
     ScanArgs wa = s->args;
-    wa.records = s->records.p;
-    wa.rec_cap = s->records.n;
+    const bool want_list = s->flags & ACG_SCAN_LIST;
+    wa.records = want_list ? s->records.p : nullptr;
+    wa.rec_cap = want_list ? s->records.n : 0;
+    // exact mode counts visits in its count pass; sparse mode in this emit pass
+    wa.visits = (s->mode_run == ACG_MODE_SPARSE && (s->flags & ACG_SCAN_COUNTS)) ? s->visits.p : nullptr;
     if (s->mode_run == ACG_MODE_SPARSE) {
-        const unsigned tb = 128;
-        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + tb - 1) / tb));
-        fixup_kernel<kWrite><<<g, tb, 0, st>>>(wa);
-        ACG_CUDA(cudaGetLastError());
+        ACG_CUDA(launch_fixup(kWrite, wa, s->n_chunks, smem_sparse(dd), st));
     } else {
         ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
     }
@@ -300,7 +325,7 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
 // streams of a full grid (one CTA per SM: the hot table takes the SM's smem).
 void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     const DeviceDfa& dd = *s->dd;
-    const unsigned long long streams = static_cast<unsigned long long>(dd.num_sms) * s->tpb * s->U_run;
+    const unsigned long long streams = static_cast<unsigned long long>(dd.num_sms) * s->tpb_run * s->U_run;
     const unsigned long long halo = dd.dfa->halo;
     unsigned long long chunk = s->chunk_override;
     if (!chunk) {
@@ -310,7 +335,7 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     chunk = (chunk + 15) & ~15ull;
     s->chunk = chunk;
     s->n_chunks = (owned + chunk - 1) / chunk;
-    const unsigned long long per_block = static_cast<unsigned long long>(s->tpb) * s->U_run;
+    const unsigned long long per_block = static_cast<unsigned long long>(s->tpb_run) * s->U_run;
     s->grid = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + per_block - 1) / per_block));
 }
 
@@ -337,7 +362,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if (mode == ACG_MODE_AUTO)
         mode = (s->last_event_rate < 0 || s->last_event_rate < 0.08) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
     s->mode_run = mode;
-    s->U_run = stats ? 2u : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 8u : 4u));
+    s->U_run = stats ? 2u : (s->U ? s->U : 4u);
+    s->tpb_run = mode == ACG_MODE_SPARSE ? sparse_tpb(s->U_run) : s->tpb;
     plan_geometry(s, owned);
     const bool prof = s->flags & ACG_SCAN_PROFILE;
 
@@ -379,6 +405,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     a.hot16 = dd.hot16.p;
     a.out_off = dd.out_off.p;
     a.out_ids = dd.out_ids.p;
+    a.depth = dd.depth.p;
     a.follows = dd.follows.p;
     a.follows_esc = dd.follows_esc.p;
     a.symmap = dd.symmap.p;
@@ -392,7 +419,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     a.active_list = s->active_list.p;
     a.active_count = s->scalars32.p;
     a.chunk_offs = s->chunk_offs.p;
-    a.visits = want_counts ? s->visits.p : nullptr;
+    a.visits = (want_counts && mode != ACG_MODE_SPARSE) ? s->visits.p : nullptr;
     a.records = s->records.p;
     a.rec_cap = s->records.n;
     a.id_bits = d.id_bits;
@@ -401,21 +428,20 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     // K1: count pass
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
     if (mode == ACG_MODE_SPARSE) {
+        // one 8-byte event per flagged 4-step sub-block; room for half of them
+        // (a fuller log overflows into an exact walk of that chunk)
         const unsigned long long walk = s->chunk + d.halo;
-        s->ev_cap = static_cast<std::uint32_t>(std::min<unsigned long long>(walk / 16 + 32, walk));
+        s->ev_cap = static_cast<std::uint32_t>(walk / 8 + 8);
         ACG_CUDA(s->events.reserve(s->n_chunks * s->ev_cap * 2ull));
         ACG_CUDA(s->ev_count.reserve(s->n_chunks));
         a.events = s->events.p;
         a.ev_count = s->ev_count.p;
         a.ev_cap = s->ev_cap;
         a.ev_total = s->scalars64.p + 4;
-        ACG_CUDA(launch_sparse_u(s->U_run, a, s->grid, s->tpb, smem_sparse(dd), st));
+        ACG_CUDA(launch_sparse_u(s->U_run, a, s->grid, s->tpb_run, smem_sparse(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
-        const unsigned tb = 128;
-        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + tb - 1) / tb));
-        fixup_kernel<kCount><<<g, tb, 0, st>>>(a);
-        ACG_CUDA(cudaGetLastError());
+        ACG_CUDA(launch_fixup(kCount, a, s->n_chunks, smem_sparse(dd), st));
         ++s->launches;
     } else {
         ACG_CUDA(launch_exact_pass(d.mode, kCount, stats, s->U_run, a, s->grid, s->tpb, smem_bytes(dd), st));
@@ -428,8 +454,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     ACG_CUDA(cub::DeviceScan::InclusiveSum(s->cub_tmp.p, tmp, in_it, s->chunk_offs.p + 1,
                                            static_cast<int>(s->n_chunks), st));
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[3], st));
-    // K3: ordered records
-    if (want_list) {
+    // K3: ordered records (sparse mode: also the per-state visits)
+    if (want_list || (want_counts && mode == ACG_MODE_SPARSE)) {
         const int rc = enqueue_write(s, st);
         if (rc) return rc;
     }

@@ -319,8 +319,10 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
     d.follows.resize(static_cast<std::size_t>(S) * K);
     d.follows_esc.resize(S);
     d.out_off.assign(S + 1, 0);
+    d.depth.resize(S);
     for (std::uint32_t i = 0; i < S; ++i) {
         const std::uint32_t s = d.nfa_of[i];
+        d.depth[i] = nfa.depth[s];
         for (std::uint32_t c = 0; c < K; ++c) {
             d.next[static_cast<std::size_t>(i) * K + c] = d.dev_of[delta[static_cast<std::size_t>(s) * K + c]];
             const std::uint32_t f = fol[static_cast<std::size_t>(s) * K + c];

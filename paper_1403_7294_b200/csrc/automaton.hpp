@@ -76,6 +76,7 @@ struct Dfa {
     // true target is cold or has outputs (the step must be replayed exactly).
     std::vector<std::uint16_t> hotH;     // H*K
     bool sparse_ok = false;
+    std::vector<std::uint32_t> depth;    // S, device order
     std::vector<std::uint32_t> out_off;  // S+1 in device order
     std::vector<std::uint32_t> out_ids;  // ascending per state
     std::vector<std::uint16_t> follows;  // S*K failure follows taken by the reference scan on (s, column)

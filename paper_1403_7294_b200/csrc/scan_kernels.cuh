@@ -62,6 +62,7 @@ struct ScanArgs {
     const std::uint16_t* hotH;     // H*K truncated-automaton rows: id | 0x8000 attention
     const std::uint32_t* out_off;  // S+1
     const std::uint32_t* out_ids;
+    const std::uint32_t* depth;    // S: trie depth per device state (sparse-mode dedup)
     const std::uint16_t* follows;      // S*K (stats only)
     const std::uint16_t* follows_esc;  // S (stats only, dna4 mode)
     const std::uint8_t* symmap;        // 256 (generic mode)
@@ -77,9 +78,7 @@ struct ScanArgs {
     unsigned long long rec_cap;
     std::uint32_t id_bits;
     unsigned long long* follows_total;      // COUNT with stats (optional)
-    // sparse-mode event log: per chunk `ev_cap` events of two u32 words:
-    // (offset << 15 | exact previous state) and the 16 packed 2-bit symbols of
-    // the event's block (0xFFFFFFFF: block had escapes, re-read the text)
+    // sparse-mode event log: per chunk `ev_cap` 16-byte events (see K1s)
     std::uint32_t* events;
     std::uint32_t* ev_count;                // per chunk (may exceed ev_cap: overflow)
     std::uint32_t ev_cap;
@@ -88,7 +87,7 @@ struct ScanArgs {
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
     return v;
@@ -149,9 +148,10 @@ template <int PASS>
 __device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned long long& cnt, unsigned long long& wr,
                                      const ScanArgs& a) {
     const std::uint32_t lo = __ldg(a.out_off + s), hi = __ldg(a.out_off + s + 1);
+    // per-state visits are recorded by whichever pass the host enables them for
+    if (a.visits) atomicAdd(a.visits + out_rank(s, a), 1ull);
     if (PASS == kCount) {
         cnt += hi - lo;
-        if (a.visits) atomicAdd(a.visits + out_rank(s, a), 1ull);
     } else {
         const unsigned long long endk = (a.base + static_cast<unsigned long long>(pos)) << a.id_bits;
         for (std::uint32_t j = lo; j < hi; ++j) {
@@ -302,111 +302,144 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
 
 // ===================================================================== K1s ==
 // Truncated-automaton fast pass (dna4 alphabet). Per step and stream: one
-// shared u16 load and a flag test; flagged steps log an event.
-template <int U>
-__global__ void __launch_bounds__(kTPB, 1) sparse_scan_kernel(const ScanArgs a) {
+// shared u16 load and an OR into the sub-block flag accumulator. Text is read
+// in 16*RB-byte refills per stream (RB 16-byte vector loads of one span,
+// prefetched one refill ahead), so every DRAM sector is consumed whole.
+// Every flagged 4-step sub-block logs one 8-byte event:
+//   w0 = walk offset of the sub-block << 15 | A_H state at its start
+//   w1 = the block's 16 packed 2-bit symbols (0xFFFFFFFF: escapes/edges)
+template <int U, int RB, int TPB>  // RB = 16-byte blocks per refill (64-byte refills at RB=4)
+__global__ void __launch_bounds__(TPB, 1) sparse_scan_kernel(const ScanArgs a) {
     extern __shared__ __align__(16) std::uint8_t smem[];
     const std::uint32_t tab = smem_u32(smem);
     const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (static_cast<long long>(blockIdx.x) * blockDim.x * U >= a.n_chunks) return;
-
-    long long chunk_id[U];
-    bool act[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        chunk_id[u] = tid * U + u;
-        act[u] = chunk_id[u] < a.n_chunks;
-    }
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
         uint4* dst = reinterpret_cast<uint4*>(smem);
         for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     __syncthreads();
-    if (!act[0]) return;
+    const long long c0 = tid * U;  // streams walk chunks c0 .. c0+U-1
+    if (c0 >= a.n_chunks) return;
+    const int n_act = static_cast<int>(min(static_cast<long long>(U), a.n_chunks - c0));
+    const long long p0 = a.emit_from + c0 * a.chunk - a.halo;  // stream u starts at p0 + u*chunk
+    const std::uint32_t cap = a.ev_cap;
+    uint2* evbase = reinterpret_cast<uint2*>(a.events) + static_cast<unsigned long long>(c0) * cap;
 
-    std::uint32_t st[U];
-    std::uint32_t* evp[U];
-    std::uint32_t nev[U];
-    long long pos0[U];
+    std::uint32_t st[U], nev[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         st[u] = 0;
         nev[u] = 0;
-        pos0[u] = a.emit_from + chunk_id[u] * a.chunk - a.halo;
-        evp[u] = a.events + static_cast<unsigned long long>(act[u] ? chunk_id[u] : 0) * a.ev_cap * 2u;
     }
-    const std::uint32_t cap = a.ev_cap;
     const long long steps = a.halo + a.chunk;
 
-    uint4 w[U];
+    uint4 w[U][RB];
     auto load = [&](long long off) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const long long p = pos0[u] + off;
-            w[u] = (act[u] && p >= 0 && p + 16 <= a.n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
+                const long long p = p0 + u * a.chunk + off + 16 * b;
+                if (u < n_act && p >= 0 && p + 16 <= a.n && off + 16 * b < steps) {
+                    asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(w[u][b].x), "=r"(w[u][b].y), "=r"(w[u][b].z), "=r"(w[u][b].w)
+                                 : "l"(a.text + p));
+                } else {
+                    w[u][b] = make_uint4(0, 0, 0, 0);
+                }
+            }
         }
     };
     load(0);
-    for (long long off = 0; off < steps; off += 16) {
-        uint4 cur[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = w[u];
-        if (off + 16 < steps) load(off + 16);
-        bool fast = true;
-        std::uint32_t pk[U];
+    for (long long off64 = 0; off64 < steps; off64 += 16 * RB) {
+        std::uint32_t pk[U][RB];
+        std::uint32_t fastm = (1u << RB) - 1;  // per block: every active stream in range and valid
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const long long p = pos0[u] + off;
-            std::uint32_t bad = 0;
-            pk[u] = dna4_pack(cur[u], bad);
-            fast = fast && (!act[u] || (p >= 0 && p + 16 <= a.n && bad == 0));
-        }
-        const std::uint32_t offw = static_cast<std::uint32_t>(off) << 15;
-        if (fast) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                std::uint32_t v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const std::uint32_t c2 = k ? (pk[u] >> (2 * k - 1)) & 6u : (pk[u] << 1) & 6u;
-                    v[u] = lds_u16(tab + (st[u] << 3) + c2);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (v[u] & 0x8000u) {  // flagged: the true next state is cold or has outputs
-                        if (nev[u] < cap) {
-                            evp[u][2 * nev[u]] = offw | (static_cast<std::uint32_t>(k) << 15) | st[u];
-                            evp[u][2 * nev[u] + 1] = pk[u];
-                        }
-                        ++nev[u];
-                    }
-                    st[u] = v[u] & 0x7FFFu;
-                }
+            for (int b = 0; b < RB; ++b) {
+                const long long p = p0 + u * a.chunk + off64 + 16 * b;
+                std::uint32_t bad = 0;
+                pk[u][b] = dna4_pack(w[u][b], bad);
+                if (u < n_act && !(p >= 0 && p + 16 <= a.n && bad == 0)) fastm &= ~(1u << b);
             }
-        } else {
-            // block with escapes or text edges: per byte; escapes reset to the
-            // root (exact in both automata: the root is hot and has no outputs)
+        }
+        if (off64 + 16 * RB < steps) load(off64 + 16 * RB);
+        const int nblk = static_cast<int>(min(static_cast<long long>(RB), (steps - off64) >> 4));
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (!act[u]) continue;
-#pragma unroll 1
-                for (int k = 0; k < 16; ++k) {
-                    const long long p = pos0[u] + off + k;
-                    const std::uint32_t b = (p >= 0 && p < a.n) ? a.text[p] : 0u;
-                    if (!(b == 'A' || b == 'C' || b == 'G' || b == 'T')) {
-                        st[u] = 0;
-                        continue;
+        for (int b = 0; b < RB; ++b) {
+            if (b >= nblk) break;
+            const long long off = off64 + 16 * b;
+            std::uint32_t pkb[U];
+            const std::uint32_t offw = static_cast<std::uint32_t>(off);
+            if ((fastm >> b) & 1u) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) pkb[u] = pk[u][b];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    std::uint32_t acc[U], ss[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        ss[u] = st[u];
+                        acc[u] = 0;
                     }
-                    const std::uint32_t v = lds_u16(tab + (st[u] << 3) + (((b >> 1) & 3u) << 1));
-                    if (v & 0x8000u) {
-                        if (nev[u] < cap) {
-                            evp[u][2 * nev[u]] = offw | (static_cast<std::uint32_t>(k) << 15) | st[u];
-                            evp[u][2 * nev[u] + 1] = 0xFFFFFFFFu;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int k = 4 * j + kk;
+                        std::uint32_t v[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const std::uint32_t c2 = k ? (pkb[u] >> (2 * k - 1)) & 6u : (pkb[u] << 1) & 6u;
+                            v[u] = lds_u16(tab + (st[u] << 3) + c2);
                         }
-                        ++nev[u];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            acc[u] |= v[u];
+                            st[u] = v[u] & 0x7FFFu;
+                        }
                     }
-                    st[u] = v & 0x7FFFu;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (acc[u] & 0x8000u) {
+                            if (nev[u] < cap)
+                                evbase[static_cast<unsigned long long>(u) * cap + nev[u]] =
+                                    make_uint2(((offw + 4u * j) << 15) | ss[u], pkb[u]);
+                            ++nev[u];
+                        }
+                    }
+                }
+            } else {
+                // block with escapes or text edges: per byte; escapes reset to the
+                // root (exact in both automata: the root is hot and has no outputs)
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (u >= n_act) continue;
+                    const long long pb = p0 + u * a.chunk + off;
+                    std::uint32_t ss = st[u], acc = 0;
+#pragma unroll 1
+                    for (int k = 0; k < 16; ++k) {
+                        if ((k & 3) == 0) {
+                            ss = st[u];
+                            acc = 0;
+                        }
+                        const long long p = pb + k;
+                        const std::uint32_t bb = (p >= 0 && p < a.n) ? a.text[p] : 0u;
+                        if (bb == 'A' || bb == 'C' || bb == 'G' || bb == 'T') {
+                            const std::uint32_t v = lds_u16(tab + (st[u] << 3) + (((bb >> 1) & 3u) << 1));
+                            acc |= v;
+                            st[u] = v & 0x7FFFu;
+                        } else {
+                            st[u] = 0;
+                        }
+                        if ((k & 3) == 3 && (acc & 0x8000u)) {
+                            if (nev[u] < cap)
+                                evbase[static_cast<unsigned long long>(u) * cap + nev[u]] =
+                                    make_uint2(((offw + static_cast<std::uint32_t>(k - 3)) << 15) | ss, 0xFFFFFFFFu);
+                            ++nev[u];
+                        }
+                    }
                 }
             }
         }
@@ -414,63 +447,215 @@ __global__ void __launch_bounds__(kTPB, 1) sparse_scan_kernel(const ScanArgs a) 
     unsigned long long tot = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        if (!act[u]) continue;
-        a.ev_count[chunk_id[u]] = nev[u];
+        if (u >= n_act) continue;
+        a.ev_count[c0 + u] = nev[u];
         tot += nev[u];
     }
     if (a.ev_total && tot) atomicAdd(a.ev_total, tot);
 }
 
 // ===================================================================== K1f ==
-// Replays one chunk's events (one thread per chunk): from each event's exact
-// previous state, walk the full DFA until the true state is hot again,
-// emitting outputs at owned positions. Events at offsets already covered by
-// an excursion came from proxy states and are skipped. An overflowed event
-// log falls back to an exact walk of the whole chunk.
+// Event replay, one warp per chunk, lanes over the chunk's flagged
+// sub-blocks. Every flagged step is walked INDEPENDENTLY: re-walk A_H over
+// the 4-step sub-block from its recorded start state (reproducing the fast
+// pass's states exactly), and from every flagged transition (s, c) walk the
+// full DFA until the state is hot again, collecting candidate outputs
+// (offset, state).
+//
+// Exactness without ordering: a flagged transition taken from a PROXY state
+// (inside a true cold excursion) starts a walk whose state is, at every
+// offset, a node-suffix of the text - a suffix of the true state - so its
+// outputs are a subset of the true outputs there, and it only reaches offsets
+// the true excursion covers (while its state is cold, the true state is at
+// least as deep). Every true excursion starts with an exact flagged
+// transition. Hence out(deepest candidate at each offset) is exactly the true
+// output set: per chunk, keep for each offset the deepest candidate.
+// Candidates are rare in sparse mode; a lane holding more than kCand falls
+// back to an exact walk of the chunk.
+constexpr int kCand = 4;
+
+struct Cands {
+    std::uint32_t off[kCand];
+    std::uint32_t st[kCand];
+    int n;  // may exceed kCand (overflow)
+};
+
+__device__ __forceinline__ void walk_event(const uint2 e, long long pos0, long long steps, std::uint32_t tab,
+                                           Cands& cd, const ScanArgs& a) {
+    const long long sb = e.x >> 15;
+    const std::uint32_t pk = e.y;
+    const bool pk_ok = pk != 0xFFFFFFFFu;
+    const std::uint32_t H = a.H;
+    auto col_at = [&](long long o) -> int {
+        if (pk_ok && (o >> 4) == (sb >> 4)) return static_cast<int>((pk >> (2 * (o & 15))) & 3u);
+        const long long p = pos0 + o;
+        const std::uint32_t b = (p >= 0 && p < a.n) ? a.text[p] : 0u;
+        return column_of<0>(b, nullptr, a);
+    };
+    std::uint32_t s = e.x & 0x7FFFu;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        const long long i = sb + kk;
+        const int col = col_at(i);
+        if (col < 0) {
+            s = 0;
+            continue;
+        }
+        const std::uint32_t v = lds_u16(tab + (s << 3) + (static_cast<std::uint32_t>(col) << 1));
+        if (v & 0x8000u) {
+            // independent walk of the full DFA from (s, col) at offset i
+            std::uint32_t x = __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
+            long long k = i;
+            for (;;) {
+                if (k >= a.halo && has_out(x, a)) {
+                    if (cd.n < kCand) {
+                        cd.off[cd.n] = static_cast<std::uint32_t>(k);
+                        cd.st[cd.n] = x;
+                    }
+                    ++cd.n;
+                }
+                if (x < H || k + 1 >= steps) break;
+                ++k;
+                const int cc = col_at(k);
+                x = cc < 0 ? 0u : __ldg(a.next + x * 4u + static_cast<std::uint32_t>(cc));
+            }
+        }
+        s = v & 0x7FFFu;
+    }
+}
+
+// Exact walk of a whole chunk window by one lane (event-log or candidate overflow).
 template <int PASS>
-__global__ void fixup_kernel(const ScanArgs a) {
-    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long n_work = PASS == kWrite ? static_cast<long long>(*a.active_count) : a.n_chunks;
-    if (t >= n_work) return;
-    const long long c = PASS == kWrite ? static_cast<long long>(a.active_list[t]) : t;
+__device__ __noinline__ void exact_chunk_walk(long long c, const ScanArgs& a) {
     const long long pos0 = a.emit_from + c * a.chunk - a.halo;
     const long long steps = a.halo + a.chunk;
-    const std::uint32_t K = a.K, H = a.H;
     unsigned long long cnt = 0, wr = PASS == kWrite ? a.chunk_offs[c] : 0ull;
-    const std::uint32_t ne = a.ev_count[c];
-
-    auto step_full = [&](std::uint32_t s, long long p) -> std::uint32_t {
-        const std::uint32_t b = (p >= 0 && p < a.n) ? a.text[p] : 0u;
-        const int col = column_of<0>(b, nullptr, a);
-        return col < 0 ? 0u : __ldg(a.next + s * K + static_cast<std::uint32_t>(col));
-    };
-
-    if (ne > a.ev_cap) {
-        std::uint32_t s = 0;
-        for (long long o = 0; o < steps; ++o) {
-            s = step_full(s, pos0 + o);
-            if (o >= a.halo && has_out(s, a)) emit<PASS>(s, pos0 + o, cnt, wr, a);
-        }
-    } else {
-        const std::uint32_t* ev = a.events + static_cast<unsigned long long>(c) * a.ev_cap * 2u;
-        long long covered = -1;
-        for (std::uint32_t j = 0; j < ne; ++j) {
-            const std::uint32_t e0 = ev[2 * j], pk = ev[2 * j + 1];
-            const long long o = e0 >> 15;
-            if (o <= covered) continue;
-            std::uint32_t s = e0 & 0x7FFFu;
-            long long i = o;
-            const long long blk_end = (o | 15) + 1;
-            do {
-                if (pk != 0xFFFFFFFFu && i < blk_end) s = __ldg(a.next + s * K + ((pk >> (2 * (i & 15))) & 3u));
-                else s = step_full(s, pos0 + i);
-                if (i >= a.halo && has_out(s, a)) emit<PASS>(s, pos0 + i, cnt, wr, a);
-                ++i;
-            } while (s >= H && i < steps);
-            covered = i - 1;
-        }
+    std::uint32_t s = 0;
+    for (long long o = 0; o < steps; ++o) {
+        const long long p = pos0 + o;
+        const int col = column_of<0>((p >= 0 && p < a.n) ? a.text[p] : 0u, nullptr, a);
+        s = col < 0 ? 0u : __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
+        if (o >= a.halo && has_out(s, a)) emit<PASS>(s, p, cnt, wr, a);
     }
     if (PASS == kCount) a.chunk_counts[c] = cnt;
+}
+
+// Per-offset deepest-candidate selection and output (count or ordered write).
+template <int PASS>
+__device__ __noinline__ void resolve_candidates(long long c, Cands cd, int lane, const ScanArgs& a) {
+    const long long pos0 = a.emit_from + c * a.chunk - a.halo;
+    bool keep[kCand];
+    std::uint32_t dep[kCand];
+#pragma unroll
+    for (int q = 0; q < kCand; ++q) {
+        keep[q] = q < cd.n;
+        dep[q] = q < cd.n ? __ldg(a.depth + cd.st[q]) : 0u;
+    }
+    for (int src = 0; src < 32; ++src) {
+        const int nsrc = __shfl_sync(0xffffffffu, cd.n, src);
+        for (int r = 0; r < nsrc; ++r) {
+            std::uint32_t o_r = 0, s_r = 0;
+#pragma unroll
+            for (int q = 0; q < kCand; ++q)
+                if (q == r) {
+                    o_r = cd.off[q];
+                    s_r = cd.st[q];
+                }
+            o_r = __shfl_sync(0xffffffffu, o_r, src);
+            s_r = __shfl_sync(0xffffffffu, s_r, src);
+            const std::uint32_t d_r = __ldg(a.depth + s_r);
+#pragma unroll
+            for (int q = 0; q < kCand; ++q) {
+                if (!keep[q] || o_r != cd.off[q]) continue;
+                const bool me = src == lane && r == q;
+                const bool earlier = src < lane || (src == lane && r < q);
+                if (!me && (d_r > dep[q] || (d_r == dep[q] && earlier))) keep[q] = false;
+            }
+        }
+    }
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int q = 0; q < kCand; ++q)
+        if (keep[q]) mine += __ldg(a.out_off + cd.st[q] + 1) - __ldg(a.out_off + cd.st[q]);
+    if (PASS == kCount) {
+        unsigned long long sum = mine;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) a.chunk_counts[c] = sum;
+        return;
+    }
+    const unsigned long long wr0 = a.chunk_offs[c];
+#pragma unroll
+    for (int q = 0; q < kCand; ++q) {
+        // slot = outputs of kept candidates at smaller offsets (kept offsets are distinct)
+        unsigned long long before = 0;
+        for (int src = 0; src < 32; ++src) {
+            const int nsrc = __shfl_sync(0xffffffffu, cd.n, src);
+            for (int r = 0; r < nsrc; ++r) {
+                std::uint32_t o_r = 0, s_r = 0;
+                int k_r = 0;
+#pragma unroll
+                for (int z = 0; z < kCand; ++z)
+                    if (z == r) {
+                        o_r = cd.off[z];
+                        s_r = cd.st[z];
+                        k_r = keep[z];
+                    }
+                o_r = __shfl_sync(0xffffffffu, o_r, src);
+                s_r = __shfl_sync(0xffffffffu, s_r, src);
+                k_r = __shfl_sync(0xffffffffu, k_r, src);
+                if (k_r && keep[q] && o_r < cd.off[q])
+                    before += __ldg(a.out_off + s_r + 1) - __ldg(a.out_off + s_r);
+            }
+        }
+        if (keep[q]) {
+            unsigned long long w2 = wr0 + before, dummy = 0;
+            emit<PASS>(cd.st[q], pos0 + cd.off[q], dummy, w2, a);
+        }
+    }
+}
+
+template <int PASS>
+__device__ __forceinline__ void fixup_chunk(long long c, std::uint32_t tab, int lane, const ScanArgs& a) {
+    const long long pos0 = a.emit_from + c * a.chunk - a.halo;
+    const long long steps = a.halo + a.chunk;
+    const std::uint32_t ne = a.ev_count[c];
+    const uint2* ev = reinterpret_cast<const uint2*>(a.events) + static_cast<unsigned long long>(c) * a.ev_cap;
+    Cands cd;
+    cd.n = 0;
+    if (ne <= a.ev_cap)
+        for (std::uint32_t j = lane; j < ne; j += 32) walk_event(ev[j], pos0, steps, tab, cd, a);
+    const bool overflow = __any_sync(0xffffffffu, cd.n > kCand) || ne > a.ev_cap;
+    if (overflow) {
+        if (lane == 0) exact_chunk_walk<PASS>(c, a);
+        return;
+    }
+    if (!__any_sync(0xffffffffu, cd.n > 0)) {
+        if (PASS == kCount && lane == 0) a.chunk_counts[c] = 0;
+        return;
+    }
+    resolve_candidates<PASS>(c, cd, lane, a);
+}
+
+// Persistent: one CTA per SM stages the truncated table once; warps stride
+// over the chunks (COUNT: all; WRITE: the compacted chunks with matches).
+template <int PASS>
+__global__ void __launch_bounds__(1024, 1) fixup_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    const std::uint32_t tab = smem_u32(smem);
+    const int lane = threadIdx.x & 31;
+    const long long n_work = PASS == kWrite ? static_cast<long long>(*a.active_count) : a.n_chunks;
+    const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if ((static_cast<long long>(blockIdx.x) * blockDim.x >> 5) >= n_work) return;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    for (long long w = w0; w < n_work; w += warps)
+        fixup_chunk<PASS>(PASS == kWrite ? static_cast<long long>(a.active_list[w]) : w, tab, lane, a);
 }
 
 // Compacts the ids of chunks with at least one match (order is irrelevant:
