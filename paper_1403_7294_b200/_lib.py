@@ -10,7 +10,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
-LIBACG = os.path.join(LIB_DIR, "libacg.so")
+LIBACG = os.environ.get("ACG_LIBRARY_OVERRIDE") or os.path.join(LIB_DIR, "libacg.so")  # experiments only
 LIBSYNTH = os.path.join(LIB_DIR, "libacg_synth.so")
 
 u8p = C.POINTER(C.c_uint8)

@@ -135,7 +135,7 @@ struct acg_scanner {
     int mode_req = 0;
     int mode_run = 0;
     double last_event_rate = -1.0;
-    DevBuf<std::uint32_t> events, ev_count;
+    DevBuf<std::uint32_t> events, ev_count, cands, cand_n;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
     cudaEvent_t ev[6] = {};
@@ -259,25 +259,28 @@ cudaError_t launch_sparse(const ScanArgs& args, unsigned grid, unsigned tpb, std
     return cudaGetLastError();
 }
 
-constexpr unsigned kFixupTPB = 1024;  // 32 warps, one chunk per warp
+constexpr unsigned kFixupTPB = 1024;  // 32 warps, one K1s warp buffer per warp at a time
 
-cudaError_t launch_fixup(int pass, const ScanArgs& args, unsigned long long n_work_max, std::size_t smem,
-                         cudaStream_t st) {
-    using namespace acg::kern;
-    const unsigned long long warps = kFixupTPB / 32;
+template <int U>
+cudaError_t launch_fixup_u(const ScanArgs& args, std::size_t smem, cudaStream_t st) {
+    auto k = acg::kern::fixup_kernel<U>;
+    if (cudaError_t e = prepare_smem(k, smem)) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned long long bufs = (args.n_chunks + 32ull * U - 1) / (32ull * U);
     const unsigned g = static_cast<unsigned>(
-        std::max<unsigned long long>(1, std::min<unsigned long long>((n_work_max + warps - 1) / warps, sms)));
-    if (pass == kCount) {
-        if (cudaError_t e = prepare_smem(fixup_kernel<kCount>, smem)) return e;
-        fixup_kernel<kCount><<<g, kFixupTPB, smem, st>>>(args);
-    } else {
-        if (cudaError_t e = prepare_smem(fixup_kernel<kWrite>, smem)) return e;
-        fixup_kernel<kWrite><<<g, kFixupTPB, smem, st>>>(args);
-    }
+        std::max<unsigned long long>(1, std::min<unsigned long long>((bufs + 31) / 32, sms)));
+    k<<<g, kFixupTPB, smem, st>>>(args);
     return cudaGetLastError();
+}
+
+cudaError_t launch_fixup(std::uint32_t U, const ScanArgs& args, std::size_t smem, cudaStream_t st) {
+    switch (U) {
+        case 1: return launch_fixup_u<1>(args, smem, st);
+        case 2: return launch_fixup_u<2>(args, smem, st);
+        default: return launch_fixup_u<4>(args, smem, st);
+    }
 }
 
 cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid, unsigned tpb, std::size_t smem,
@@ -285,8 +288,7 @@ cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid
     switch (U) {
         case 1: return launch_sparse<1>(args, grid, tpb, smem, st);
         case 2: return launch_sparse<2>(args, grid, tpb, smem, st);
-        case 4: return launch_sparse<4>(args, grid, tpb, smem, st);
-        default: return launch_sparse<8>(args, grid, tpb, smem, st);
+        default: return launch_sparse<4>(args, grid, tpb, smem, st);
     }
 }
 
@@ -310,10 +312,15 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     const bool want_list = s->flags & ACG_SCAN_LIST;
     wa.records = want_list ? s->records.p : nullptr;
     wa.rec_cap = want_list ? s->records.n : 0;
-    // exact mode counts visits in its count pass; sparse mode in this emit pass
-    wa.visits = (s->mode_run == ACG_MODE_SPARSE && (s->flags & ACG_SCAN_COUNTS)) ? s->visits.p : nullptr;
+    wa.visits = nullptr;  // both modes count visits in their count pass
     if (s->mode_run == ACG_MODE_SPARSE) {
-        ACG_CUDA(launch_fixup(kWrite, wa, s->n_chunks, smem_sparse(dd), st));
+        wa.visits = nullptr;  // counted with the candidates in the count pass
+        auto k = acg::kern::sparse_emit_kernel;
+        ACG_CUDA(prepare_smem(k, smem_sparse(dd)));
+        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
+            1, std::min<unsigned long long>((s->n_chunks + 255) / 256, static_cast<unsigned long long>(dd.num_sms))));
+        k<<<g, 256, smem_sparse(dd), st>>>(wa);
+        ACG_CUDA(cudaGetLastError());
     } else {
         ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
     }
@@ -333,6 +340,12 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
         chunk = std::max<unsigned long long>(chunk, std::max<unsigned long long>(256, 2 * halo));
     }
     chunk = (chunk + 15) & ~15ull;
+    // sparse mode: walk length (halo + chunk) a multiple of the 64-byte refill
+    // (an explicit chunk override is kept as is: odd walks take the per-byte path)
+    if (s->mode_run == ACG_MODE_SPARSE) {
+        chunk = std::min<unsigned long long>(chunk, (1ull << 17) - halo - 64);  // event offsets are 17-bit
+        if (!s->chunk_override) chunk = ((chunk + halo + 63) & ~63ull) - halo;
+    }
     s->chunk = chunk;
     s->n_chunks = (owned + chunk - 1) / chunk;
     const unsigned long long per_block = static_cast<unsigned long long>(s->tpb_run) * s->U_run;
@@ -362,7 +375,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if (mode == ACG_MODE_AUTO)
         mode = (s->last_event_rate < 0 || s->last_event_rate < 0.08) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
     s->mode_run = mode;
-    s->U_run = stats ? 2u : (s->U ? s->U : 4u);
+    s->U_run = stats ? 2u : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 1u : 4u));
+    if (mode == ACG_MODE_SPARSE && s->U_run > 4) s->U_run = 4;
     s->tpb_run = mode == ACG_MODE_SPARSE ? sparse_tpb(s->U_run) : s->tpb;
     plan_geometry(s, owned);
     const bool prof = s->flags & ACG_SCAN_PROFILE;
@@ -419,7 +433,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     a.active_list = s->active_list.p;
     a.active_count = s->scalars32.p;
     a.chunk_offs = s->chunk_offs.p;
-    a.visits = (want_counts && mode != ACG_MODE_SPARSE) ? s->visits.p : nullptr;
+    a.visits = want_counts ? s->visits.p : nullptr;
     a.records = s->records.p;
     a.rec_cap = s->records.n;
     a.id_bits = d.id_bits;
@@ -428,20 +442,25 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     // K1: count pass
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
     if (mode == ACG_MODE_SPARSE) {
-        // one 8-byte event per flagged 4-step sub-block; room for half of them
-        // (a fuller log overflows into an exact walk of that chunk)
+        // per K1s warp: one 16-byte event per flagged (block, stream) -> no overflow
         const unsigned long long walk = s->chunk + d.halo;
-        s->ev_cap = static_cast<std::uint32_t>(walk / 8 + 8);
-        ACG_CUDA(s->events.reserve(s->n_chunks * s->ev_cap * 2ull));
-        ACG_CUDA(s->ev_count.reserve(s->n_chunks));
+        const unsigned long long per_warp = 32ull * s->U_run;
+        const unsigned long long n_warps = (s->n_chunks + per_warp - 1) / per_warp;
+        s->ev_cap = static_cast<std::uint32_t>(per_warp * (walk / 16));
+        ACG_CUDA(s->events.reserve(n_warps * s->ev_cap * 4ull));
+        ACG_CUDA(s->ev_count.reserve(n_warps));
+        ACG_CUDA(s->cands.reserve(s->n_chunks * acg::kern::kExport * 4ull));
+        ACG_CUDA(s->cand_n.reserve(s->n_chunks));
         a.events = s->events.p;
+        a.cands = s->cands.p;
+        a.cand_n = s->cand_n.p;
         a.ev_count = s->ev_count.p;
         a.ev_cap = s->ev_cap;
         a.ev_total = s->scalars64.p + 4;
         ACG_CUDA(launch_sparse_u(s->U_run, a, s->grid, s->tpb_run, smem_sparse(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
-        ACG_CUDA(launch_fixup(kCount, a, s->n_chunks, smem_sparse(dd), st));
+        ACG_CUDA(launch_fixup(s->U_run, a, smem_sparse(dd), st));
         ++s->launches;
     } else {
         ACG_CUDA(launch_exact_pass(d.mode, kCount, stats, s->U_run, a, s->grid, s->tpb, smem_bytes(dd), st));
@@ -454,8 +473,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     ACG_CUDA(cub::DeviceScan::InclusiveSum(s->cub_tmp.p, tmp, in_it, s->chunk_offs.p + 1,
                                            static_cast<int>(s->n_chunks), st));
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[3], st));
-    // K3: ordered records (sparse mode: also the per-state visits)
-    if (want_list || (want_counts && mode == ACG_MODE_SPARSE)) {
+    // K3: ordered records
+    if (want_list) {
         const int rc = enqueue_write(s, st);
         if (rc) return rc;
     }

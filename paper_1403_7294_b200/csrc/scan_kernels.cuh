@@ -41,6 +41,10 @@
 
 #include <cstdint>
 
+// Dynamic shared memory, named at global scope so inline PTX can address it
+// as a symbol (ptxas folds the base into the LDS immediate/uniform operand).
+extern __shared__ __align__(16) std::uint8_t acg_hot_smem[];
+
 namespace acg {
 namespace kern {
 
@@ -78,10 +82,12 @@ struct ScanArgs {
     unsigned long long rec_cap;
     std::uint32_t id_bits;
     unsigned long long* follows_total;      // COUNT with stats (optional)
-    // sparse-mode event log: per chunk `ev_cap` 16-byte events (see K1s)
+    // sparse-mode event log: per K1s warp `ev_cap` 16-byte events (see K1s)
     std::uint32_t* events;
-    std::uint32_t* ev_count;                // per chunk (may exceed ev_cap: overflow)
+    std::uint32_t* ev_count;                // per K1s warp (may exceed ev_cap: overflow)
     std::uint32_t ev_cap;
+    std::uint32_t* cands;                   // per chunk kExport exported candidates (uint4)
+    std::uint32_t* cand_n;                  // per chunk: exported count, 0xFFFFFFFF = re-walk
     unsigned long long* ev_total;           // sum of events (mode heuristic)
 };
 
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const long long p = pos0[u] + off;
-            w[u] = (act[u] && p >= 0 && p + 16 <= a.n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
+            w[u] = (act[u] && p >= 0 && p < a.n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
         }
     };
     load(0);
@@ -272,7 +278,8 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
                 for (int k = 0; k < 16; ++k) {
                     const long long p = pos0[u] + off + k;
                     const bool inside = p >= 0 && p < a.n;
-                    const int c = inside ? column_of<MODE>(a.text[p], smap, a) : -1;
+                    const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
+                    const int c = inside ? column_of<MODE>((word >> (8 * (k & 3))) & 0xFFu, smap, a) : -1;
                     if (STATS && owned_blk && inside)
                         fol[u] += c < 0 ? (MODE == 0 ? __ldg(a.follows_esc + st[u])
                                                      : __ldg(a.follows + st[u] * K + (K - 1)))
@@ -301,166 +308,279 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
 }
 
 // ===================================================================== K1s ==
-// Truncated-automaton fast pass (dna4 alphabet). Per step and stream: one
-// shared u16 load and an OR into the sub-block flag accumulator. Text is read
-// in 16*RB-byte refills per stream (RB 16-byte vector loads of one span,
-// prefetched one refill ahead), so every DRAM sector is consumed whole.
-// Every flagged 4-step sub-block logs one 8-byte event:
-//   w0 = walk offset of the sub-block << 15 | A_H state at its start
-//   w1 = the block's 16 packed 2-bit symbols (0xFFFFFFFF: escapes/edges)
-template <int U, int RB, int TPB>  // RB = 16-byte blocks per refill (64-byte refills at RB=4)
+// Truncated-automaton fast pass (dna4 alphabet). Per step and stream:
+//   c2 = PRMT(byte k of (word & 0x06060606))      column * 2
+//   a  = (v * 8 + c2) & 0x3FFFF                    next row address (drops the flag bit)
+//   v  = LDS.U16 [a + table]                       (table base folded into the LDS)
+//   acc |= v                                       flag accumulator
+// Interior threads (all U chunk windows inside the buffer) read text with
+// unchecked 16*RB-byte refills per stream, double-buffered one refill ahead
+// (256-bit loads when 32-byte aligned), validated with a 6-op SIMD test per
+// word (exactly A,C,G,T pass). A block with any non-ACGT byte or past a text
+// edge is walked per byte from the same registers. Every 4 steps the
+// sub-block's flag bit and start state are folded into registers.
+//
+// Event log. After each 16-step block the warp ballots its flagged streams and
+// writes their events to consecutive slots of a per-warp buffer (coalesced):
+//   w0 = walk offset of the block | flag bits << 17 | stream slot (lane*U+u) << 21
+//   w1 = A_H state at sub-blocks 0,1 (u16 each), w2 = sub-blocks 2,3
+//   w3 = the block's 16 packed 2-bit columns (0xFFFFFFFF: per-byte block, re-read text)
+__device__ __forceinline__ std::uint32_t lds_hot(std::uint32_t off) {
+    std::uint16_t v;
+    asm volatile("{ .reg .u32 t; mov.u32 t, acg_hot_smem; add.u32 t, t, %1; ld.shared.u16 %0, [t]; }"
+                 : "=h"(v)
+                 : "r"(off));
+    return v;
+}
+
+// 0 iff all 4 bytes of w are in {A,C,G,T}
+__device__ __forceinline__ std::uint32_t acgt_bad(std::uint32_t w) {
+    const std::uint32_t t = ((w >> 2) & ~(w >> 1)) & 0x01010101u;  // byte is T-like ((b & 6) == 4)
+    const std::uint32_t z = (w ^ 0x41414141u) & 0xF9F9F9F9u;
+    return z ^ (t * 0x11u);
+}
+
+// 16 columns packed 2 bits each (symbol k at bits 2k), for the event record
+__device__ __forceinline__ std::uint32_t pack_cols(const uint4& w) {
+    const std::uint32_t m0 = ((w.x >> 1) & 0x03030303u) * 0x01041040u, m1 = ((w.y >> 1) & 0x03030303u) * 0x01041040u;
+    const std::uint32_t m2 = ((w.z >> 1) & 0x03030303u) * 0x01041040u, m3 = ((w.w >> 1) & 0x03030303u) * 0x01041040u;
+    return __byte_perm(__byte_perm(m0, m1, 0x0073u), __byte_perm(m2, m3, 0x7300u), 0x7610u);
+}
+
+__device__ __forceinline__ uint4 ldg_text(const std::uint8_t* p) {
+#ifdef ACG_ABLATE_TEXT
+    const std::uint32_t h = static_cast<std::uint32_t>(reinterpret_cast<std::uintptr_t>(p)) * 2654435761u;
+    const std::uint32_t m = 0x41414141u | ((h & 0x06060606u));
+    return make_uint4(m, m ^ 0x02020202u, m ^ 0x04040404u, m ^ 0x06060606u);
+#endif
+    uint4 v;
+    asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// 32 bytes (two blocks) with one 256-bit load (sm_100: LDG.E.ENL2.256); p 32-byte aligned
+__device__ __forceinline__ void ldg_text32(const std::uint8_t* p, uint4& lo, uint4& hi) {
+#ifdef ACG_ABLATE_TEXT
+    lo = ldg_text(p);
+    hi = ldg_text(p + 16);
+    return;
+#endif
+    asm volatile("ld.global.nc.L2::128B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+}
+
+// 16 bytes at p (any byte of [p, p+16) inside [0, n)); bytes past n are masked by the caller
+__device__ __forceinline__ uint4 ldg_block_checked(const std::uint8_t* text, long long p, long long n) {
+    return (p >= 0 && p < n) ? ldg_text(text + p) : make_uint4(0, 0, 0, 0);
+}
+
+// One 16-step block of U streams from registers.
+template <int U>
+__device__ __forceinline__ void k1s_block(const uint4 (&wb)[U], std::uint32_t (&st)[U], std::uint32_t (&fl)[U],
+                                          std::uint32_t (&s01)[U], std::uint32_t (&s23)[U]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        std::uint32_t acc[U], w6[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const std::uint32_t word = j == 0 ? wb[u].x : j == 1 ? wb[u].y : j == 2 ? wb[u].z : wb[u].w;
+            w6[u] = word & 0x06060606u;
+            if (j == 0) s01[u] = st[u];
+            else if (j == 1) s01[u] |= st[u] << 16;
+            else if (j == 2) s23[u] = st[u];
+            else s23[u] |= st[u] << 16;
+            acc[u] = 0;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            std::uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = lds_hot((st[u] * 8u + __byte_perm(w6[u], 0u, 0x4440u + kk)) & 0x3FFFFu);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                acc[u] |= v[u];
+                st[u] = v[u];  // flag bit stripped by the next address mask
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const std::uint32_t bit = (acc[u] >> (15 - j)) & (1u << j);
+            fl[u] = j ? (fl[u] | bit) : bit;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        st[u] &= 0x7FFFu;
+        s01[u] &= 0x7FFF7FFFu;
+        s23[u] &= 0x7FFF7FFFu;
+    }
+}
+
+// One 16-step block of one stream, per byte from registers: bytes outside
+// [0, n) and non-ACGT bytes are escapes (every state goes to the root).
+__device__ __forceinline__ void k1s_block_slow(const uint4 wv, long long pb, long long n, std::uint32_t& st,
+                                               std::uint32_t& fl, std::uint32_t& s01, std::uint32_t& s23) {
+    fl = 0;
+    s01 = 0;
+    s23 = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if ((k & 3) == 0) {
+            const int j = k >> 2;
+            if (j < 2) s01 |= st << (16 * j);
+            else s23 |= st << (16 * (j - 2));
+        }
+        const std::uint32_t word = k < 4 ? wv.x : k < 8 ? wv.y : k < 12 ? wv.z : wv.w;
+        const std::uint32_t bb = (word >> (8 * (k & 3))) & 0xFFu;
+        const long long p = pb + k;
+        if (p < 0 || p >= n || !(bb == 'A' || bb == 'C' || bb == 'G' || bb == 'T')) {
+            st = 0;
+            continue;
+        }
+        const std::uint32_t v = lds_hot(st * 8u + (bb & 6u));
+        if (v & 0x8000u) fl |= 1u << (k >> 2);
+        st = v & 0x7FFFu;
+    }
+}
+
+template <int U, int RB, int TPB>  // RB = 16-byte blocks per refill
 __global__ void __launch_bounds__(TPB, 1) sparse_scan_kernel(const ScanArgs a) {
-    extern __shared__ __align__(16) std::uint8_t smem[];
-    const std::uint32_t tab = smem_u32(smem);
     const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (static_cast<long long>(blockIdx.x) * blockDim.x * U >= a.n_chunks) return;
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
-        uint4* dst = reinterpret_cast<uint4*>(smem);
+        uint4* dst = reinterpret_cast<uint4*>(acg_hot_smem);
         for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     __syncthreads();
-    const long long c0 = tid * U;  // streams walk chunks c0 .. c0+U-1
-    if (c0 >= a.n_chunks) return;
-    const int n_act = static_cast<int>(min(static_cast<long long>(U), a.n_chunks - c0));
+    const int lane = threadIdx.x & 31;
+    const long long wid = tid >> 5;
+    if (wid * 32 * U >= a.n_chunks) return;  // whole warp idle (idle lanes of a live warp stay for the ballots)
+    const long long c0 = tid * U;             // streams walk chunks c0 .. c0+U-1
+    const int n_act = static_cast<int>(max(0ll, min(static_cast<long long>(U), a.n_chunks - c0)));
     const long long p0 = a.emit_from + c0 * a.chunk - a.halo;  // stream u starts at p0 + u*chunk
-    const std::uint32_t cap = a.ev_cap;
-    uint2* evbase = reinterpret_cast<uint2*>(a.events) + static_cast<unsigned long long>(c0) * cap;
-
-    std::uint32_t st[U], nev[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        st[u] = 0;
-        nev[u] = 0;
-    }
     const long long steps = a.halo + a.chunk;
+    const std::uint32_t wcap = a.ev_cap;
+    uint4* evw = reinterpret_cast<uint4*>(a.events) + static_cast<unsigned long long>(wid) * wcap;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    std::uint32_t wn = 0;  // warp-uniform event count
 
-    uint4 w[U][RB];
-    auto load = [&](long long off) {
+    std::uint32_t st[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) st[u] = 0;
+
+    // interior: every block of every stream lies inside [0, n) -> unchecked loads
+    const bool interior = n_act == U && p0 >= 0 && p0 + (U - 1) * a.chunk + steps <= a.n;
+    const std::uint8_t* ptr = a.text + p0;
+    const long long cs = a.chunk;
+    const std::uint32_t R = 16u * RB;
+#ifdef ACG_NO_LDG256
+    const bool al32 = false;
+#else
+    const bool al32 = ((reinterpret_cast<std::uintptr_t>(ptr) | static_cast<std::uintptr_t>(cs)) & 31u) == 0;
+#endif
+    uint4 wa[U][RB], wb[U][RB];
+    auto load = [&](uint4 (&buf)[U][RB], std::uint32_t off0) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            if (interior && al32) {
 #pragma unroll
-            for (int b = 0; b < RB; ++b) {
-                const long long p = p0 + u * a.chunk + off + 16 * b;
-                if (u < n_act && p >= 0 && p + 16 <= a.n && off + 16 * b < steps) {
-                    asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                                 : "=r"(w[u][b].x), "=r"(w[u][b].y), "=r"(w[u][b].z), "=r"(w[u][b].w)
-                                 : "l"(a.text + p));
-                } else {
-                    w[u][b] = make_uint4(0, 0, 0, 0);
+                for (int b = 0; b + 1 < RB; b += 2) ldg_text32(ptr + u * cs + off0 + 16 * b, buf[u][b], buf[u][b + 1]);
+                if (RB & 1) buf[u][RB - 1] = ldg_text(ptr + u * cs + off0 + 16 * (RB - 1));
+            } else if (interior) {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) buf[u][b] = ldg_text(ptr + u * cs + off0 + 16 * b);
+            } else {
+#pragma unroll
+                for (int b = 0; b < RB; ++b) {
+                    const long long o = u * cs + off0 + 16 * b;
+                    buf[u][b] = (u < n_act && off0 + 16 * b < steps) ? ldg_block_checked(a.text, p0 + o, a.n)
+                                                                    : make_uint4(0, 0, 0, 0);
                 }
             }
         }
     };
-    load(0);
-    for (long long off64 = 0; off64 < steps; off64 += 16 * RB) {
-        std::uint32_t pk[U][RB];
-        std::uint32_t fastm = (1u << RB) - 1;  // per block: every active stream in range and valid
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-            for (int b = 0; b < RB; ++b) {
-                const long long p = p0 + u * a.chunk + off64 + 16 * b;
-                std::uint32_t bad = 0;
-                pk[u][b] = dna4_pack(w[u][b], bad);
-                if (u < n_act && !(p >= 0 && p + 16 <= a.n && bad == 0)) fastm &= ~(1u << b);
-            }
-        }
-        if (off64 + 16 * RB < steps) load(off64 + 16 * RB);
-        const int nblk = static_cast<int>(min(static_cast<long long>(RB), (steps - off64) >> 4));
+    auto process = [&](const uint4 (&buf)[U][RB], std::uint32_t off0) {
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
-            if (b >= nblk) break;
-            const long long off = off64 + 16 * b;
-            std::uint32_t pkb[U];
-            const std::uint32_t offw = static_cast<std::uint32_t>(off);
-            if ((fastm >> b) & 1u) {
+            const std::uint32_t off = off0 + 16u * b;
+            if (off >= steps) break;
+            std::uint32_t bad = 0;
+#ifndef ACG_ABLATE_VALIDATE
 #pragma unroll
-                for (int u = 0; u < U; ++u) pkb[u] = pk[u][b];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    std::uint32_t acc[U], ss[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        ss[u] = st[u];
-                        acc[u] = 0;
-                    }
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const int k = 4 * j + kk;
-                        std::uint32_t v[U];
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const std::uint32_t c2 = k ? (pkb[u] >> (2 * k - 1)) & 6u : (pkb[u] << 1) & 6u;
-                            v[u] = lds_u16(tab + (st[u] << 3) + c2);
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            acc[u] |= v[u];
-                            st[u] = v[u] & 0x7FFFu;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        if (acc[u] & 0x8000u) {
-                            if (nev[u] < cap)
-                                evbase[static_cast<unsigned long long>(u) * cap + nev[u]] =
-                                    make_uint2(((offw + 4u * j) << 15) | ss[u], pkb[u]);
-                            ++nev[u];
-                        }
-                    }
-                }
-            } else {
-                // block with escapes or text edges: per byte; escapes reset to the
-                // root (exact in both automata: the root is hot and has no outputs)
+            for (int u = 0; u < U; ++u)
+                bad |= acgt_bad(buf[u][b].x) | acgt_bad(buf[u][b].y) | acgt_bad(buf[u][b].z) | acgt_bad(buf[u][b].w);
+#endif
+            if (!interior) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
+                    const long long p = p0 + u * cs + off;
+                    if (u < n_act && !(p >= 0 && p + 16 <= a.n)) bad = 1;
+                }
+            }
+            std::uint32_t fl[U], s01[U], s23[U];
+            const bool fast = bad == 0;
+            if (fast) {
+                uint4 wv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) wv[u] = buf[u][b];
+                k1s_block<U>(wv, st, fl, s01, s23);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    fl[u] = 0;
                     if (u >= n_act) continue;
-                    const long long pb = p0 + u * a.chunk + off;
-                    std::uint32_t ss = st[u], acc = 0;
-#pragma unroll 1
-                    for (int k = 0; k < 16; ++k) {
-                        if ((k & 3) == 0) {
-                            ss = st[u];
-                            acc = 0;
-                        }
-                        const long long p = pb + k;
-                        const std::uint32_t bb = (p >= 0 && p < a.n) ? a.text[p] : 0u;
-                        if (bb == 'A' || bb == 'C' || bb == 'G' || bb == 'T') {
-                            const std::uint32_t v = lds_u16(tab + (st[u] << 3) + (((bb >> 1) & 3u) << 1));
-                            acc |= v;
-                            st[u] = v & 0x7FFFu;
-                        } else {
-                            st[u] = 0;
-                        }
-                        if ((k & 3) == 3 && (acc & 0x8000u)) {
-                            if (nev[u] < cap)
-                                evbase[static_cast<unsigned long long>(u) * cap + nev[u]] =
-                                    make_uint2(((offw + static_cast<std::uint32_t>(k - 3)) << 15) | ss, 0xFFFFFFFFu);
-                            ++nev[u];
-                        }
+                    k1s_block_slow(buf[u][b], p0 + u * cs + off, a.n, st[u], fl[u], s01[u], s23[u]);
+                }
+            }
+            // warp-coalesced event log (converged here)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (u >= n_act) fl[u] = 0;
+#ifdef ACG_ABLATE_EVENTS
+                wn ^= fl[u] ^ s01[u] ^ s23[u];
+                continue;
+#endif
+                const unsigned m = __ballot_sync(0xffffffffu, fl[u] != 0);
+                if (m) {
+                    if (fl[u]) {
+                        const std::uint32_t idx = min(wn + static_cast<std::uint32_t>(__popc(m & lt_mask)), wcap - 1);
+                        evw[idx] = make_uint4(off | (fl[u] << 17) | (static_cast<std::uint32_t>(lane * U + u) << 21),
+                                              s01[u], s23[u], fast ? pack_cols(buf[u][b]) : 0xFFFFFFFFu);
                     }
+                    wn += static_cast<std::uint32_t>(__popc(m));
                 }
             }
         }
+    };
+    load(wa, 0);
+    for (std::uint32_t off0 = 0; off0 < steps; off0 += 2 * R) {
+        if (off0 + R < steps) load(wb, off0 + R);
+        process(wa, off0);
+        if (off0 + R >= steps) break;
+        if (off0 + 2 * R < steps) load(wa, off0 + 2 * R);
+        process(wb, off0 + R);
     }
-    unsigned long long tot = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        if (u >= n_act) continue;
-        a.ev_count[c0 + u] = nev[u];
-        tot += nev[u];
+#ifdef ACG_ABLATE_EVENTS
+    if (wn == 0x12345678u) a.ev_count[wid] = st[0];
+    wn = 0;
+#endif
+    if (lane == 0) {
+        a.ev_count[wid] = wn;
+        if (a.ev_total && wn) atomicAdd(a.ev_total, static_cast<unsigned long long>(wn));
     }
-    if (a.ev_total && tot) atomicAdd(a.ev_total, tot);
 }
 
 // ===================================================================== K1f ==
-// Event replay, one warp per chunk, lanes over the chunk's flagged
-// sub-blocks. Every flagged step is walked INDEPENDENTLY: re-walk A_H over
-// the 4-step sub-block from its recorded start state (reproducing the fast
-// pass's states exactly), and from every flagged transition (s, c) walk the
-// full DFA until the state is hot again, collecting candidate outputs
-// (offset, state).
+// Event replay, one warp per K1s warp buffer (32*U chunks), lanes over its
+// events (coalesced). Every flagged step is walked INDEPENDENTLY: re-walk A_H
+// over each flagged 4-step sub-block from its recorded start state
+// (reproducing the fast pass's states exactly), and from every flagged
+// transition (s, c) walk the full DFA until the state is hot again,
+// collecting candidate outputs (chunk slot, offset, state).
 //
 // Exactness without ordering: a flagged transition taken from a PROXY state
 // (inside a true cold excursion) starts a walk whose state is, at every
@@ -470,181 +590,256 @@ __global__ void __launch_bounds__(TPB, 1) sparse_scan_kernel(const ScanArgs a) {
 // least as deep). Every true excursion starts with an exact flagged
 // transition. Hence out(deepest candidate at each offset) is exactly the true
 // output set: per chunk, keep for each offset the deepest candidate.
-// Candidates are rare in sparse mode; a lane holding more than kCand falls
-// back to an exact walk of the chunk.
-constexpr int kCand = 4;
+//
+// The warp then writes every chunk's record count, adds per-state visits of
+// the kept candidates, and exports them (offset order, with their record
+// prefix inside the chunk) for the emit pass. Candidates are rare in sparse
+// mode; a lane holding more than kCand of them makes the warp fall back to an
+// exact replay of its chunks.
+constexpr int kCand = 8;
+constexpr int kExport = 8;  // exported candidates per chunk (more: emit re-walks the chunk)
 
 struct Cands {
-    std::uint32_t off[kCand];
+    std::uint32_t key[kCand];  // slot << 24 | walk offset
     std::uint32_t st[kCand];
     int n;  // may exceed kCand (overflow)
 };
 
-__device__ __forceinline__ void walk_event(const uint2 e, long long pos0, long long steps, std::uint32_t tab,
-                                           Cands& cd, const ScanArgs& a) {
-    const long long sb = e.x >> 15;
-    const std::uint32_t pk = e.y;
+__device__ __forceinline__ int text_col(const ScanArgs& a, long long p) {
+    const std::uint32_t b = (p >= 0 && p < a.n) ? a.text[p] : 0u;
+    return column_of<0>(b, nullptr, a);
+}
+
+__device__ __forceinline__ void walk_event(const uint4 e, long long chunk_base, std::uint32_t tab, Cands& cd,
+                                           const ScanArgs& a) {
+    const long long boff = e.x & 0x1FFFFu;
+    std::uint32_t fl = (e.x >> 17) & 0xFu;
+    const std::uint32_t slot = e.x >> 21;
+    const std::uint32_t pk = e.w;
     const bool pk_ok = pk != 0xFFFFFFFFu;
+    const long long pos0 = a.emit_from + (chunk_base + slot) * a.chunk - a.halo;
+    const long long steps = a.halo + a.chunk;
     const std::uint32_t H = a.H;
     auto col_at = [&](long long o) -> int {
-        if (pk_ok && (o >> 4) == (sb >> 4)) return static_cast<int>((pk >> (2 * (o & 15))) & 3u);
-        const long long p = pos0 + o;
-        const std::uint32_t b = (p >= 0 && p < a.n) ? a.text[p] : 0u;
-        return column_of<0>(b, nullptr, a);
+        if (pk_ok && (o >> 4) == (boff >> 4)) return static_cast<int>((pk >> (2 * (o & 15))) & 3u);
+        return text_col(a, pos0 + o);
     };
-    std::uint32_t s = e.x & 0x7FFFu;
+    while (fl) {
+        const int j = __ffs(fl) - 1;
+        fl &= fl - 1;
+        std::uint32_t s = ((j < 2 ? e.y : e.z) >> (16 * (j & 1))) & 0x7FFFu;
+        const long long sb = boff + 4 * j;
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-        const long long i = sb + kk;
-        const int col = col_at(i);
-        if (col < 0) {
-            s = 0;
-            continue;
-        }
-        const std::uint32_t v = lds_u16(tab + (s << 3) + (static_cast<std::uint32_t>(col) << 1));
-        if (v & 0x8000u) {
-            // independent walk of the full DFA from (s, col) at offset i
-            std::uint32_t x = __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
-            long long k = i;
-            for (;;) {
-                if (k >= a.halo && has_out(x, a)) {
-                    if (cd.n < kCand) {
-                        cd.off[cd.n] = static_cast<std::uint32_t>(k);
-                        cd.st[cd.n] = x;
-                    }
-                    ++cd.n;
-                }
-                if (x < H || k + 1 >= steps) break;
-                ++k;
-                const int cc = col_at(k);
-                x = cc < 0 ? 0u : __ldg(a.next + x * 4u + static_cast<std::uint32_t>(cc));
+        for (int kk = 0; kk < 4; ++kk) {
+            const long long i = sb + kk;
+            const int col = col_at(i);
+            if (col < 0) {
+                s = 0;
+                continue;
             }
+            const std::uint32_t v = lds_u16(tab + (s << 3) + (static_cast<std::uint32_t>(col) << 1));
+            if (v & 0x8000u) {
+                std::uint32_t x = __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
+                long long k = i;
+                for (;;) {
+                    if (k >= a.halo && has_out(x, a)) {
+                        if (cd.n < kCand) {
+                            cd.key[cd.n] = (slot << 24) | static_cast<std::uint32_t>(k);
+                            cd.st[cd.n] = x;
+                        }
+                        ++cd.n;
+                    }
+                    if (x < H || k + 1 >= steps) break;
+                    ++k;
+                    const int cc = col_at(k);
+                    x = cc < 0 ? 0u : __ldg(a.next + x * 4u + static_cast<std::uint32_t>(cc));
+                }
+            }
+            s = v & 0x7FFFu;
         }
-        s = v & 0x7FFFu;
     }
 }
 
-// Exact walk of a whole chunk window by one lane (event-log or candidate overflow).
+// Exact sequential replay of one chunk window by one lane: walk A_H from shared
+// memory, replaying each flagged transition's excursion exactly (no event log).
 template <int PASS>
-__device__ __noinline__ void exact_chunk_walk(long long c, const ScanArgs& a) {
+__device__ __noinline__ void exact_chunk_walk(long long c, std::uint32_t tab, const ScanArgs& a) {
     const long long pos0 = a.emit_from + c * a.chunk - a.halo;
     const long long steps = a.halo + a.chunk;
     unsigned long long cnt = 0, wr = PASS == kWrite ? a.chunk_offs[c] : 0ull;
     std::uint32_t s = 0;
     for (long long o = 0; o < steps; ++o) {
-        const long long p = pos0 + o;
-        const int col = column_of<0>((p >= 0 && p < a.n) ? a.text[p] : 0u, nullptr, a);
-        s = col < 0 ? 0u : __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
-        if (o >= a.halo && has_out(s, a)) emit<PASS>(s, p, cnt, wr, a);
+        const int col = text_col(a, pos0 + o);
+        if (col < 0) {
+            s = 0;
+            continue;
+        }
+        const std::uint32_t v = lds_u16(tab + (s << 3) + (static_cast<std::uint32_t>(col) << 1));
+        if (!(v & 0x8000u)) {
+            s = v & 0x7FFFu;
+            continue;
+        }
+        std::uint32_t x = __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
+        for (;;) {
+            if (o >= a.halo && has_out(x, a)) emit<PASS>(x, pos0 + o, cnt, wr, a);
+            if (x < a.H || o + 1 >= steps) break;
+            ++o;
+            const int cc = text_col(a, pos0 + o);
+            x = cc < 0 ? 0u : __ldg(a.next + x * 4u + static_cast<std::uint32_t>(cc));
+        }
+        s = x < a.H ? x : 0u;
     }
     if (PASS == kCount) a.chunk_counts[c] = cnt;
 }
 
-// Per-offset deepest-candidate selection and output (count or ordered write).
-template <int PASS>
-__device__ __noinline__ void resolve_candidates(long long c, Cands cd, int lane, const ScanArgs& a) {
-    const long long pos0 = a.emit_from + c * a.chunk - a.halo;
+__device__ __noinline__ void resolve_warp(Cands cd, long long chunk_base, int n_slots, int lane, const ScanArgs& a);
+
+template <int U>
+__device__ void fixup_warp(long long wid, std::uint32_t tab, int lane, const ScanArgs& a) {
+    const long long chunk_base = wid * 32 * U;
+    const int n_slots = static_cast<int>(min(static_cast<long long>(32 * U), a.n_chunks - chunk_base));
+    const std::uint32_t ne = a.ev_count[wid];
+    const uint4* ev = reinterpret_cast<const uint4*>(a.events) + static_cast<unsigned long long>(wid) * a.ev_cap;
+    Cands cd;
+    cd.n = 0;
+    if (ne <= a.ev_cap)
+        for (std::uint32_t j = lane; j < ne; j += 32) walk_event(ev[j], chunk_base, tab, cd, a);
+    const bool overflow = __any_sync(0xffffffffu, cd.n > kCand) || ne > a.ev_cap;
+    if (overflow) {  // exact replay of every chunk of this buffer, one lane per chunk (rare)
+        for (int sl = lane; sl < n_slots; sl += 32) {
+            a.cand_n[chunk_base + sl] = 0xFFFFFFFFu;  // emit pass re-walks
+            exact_chunk_walk<kCount>(chunk_base + sl, tab, a);
+        }
+        return;
+    }
+    if (!__any_sync(0xffffffffu, cd.n > 0)) {
+        for (int sl = lane; sl < n_slots; sl += 32) {
+            a.chunk_counts[chunk_base + sl] = 0;
+            a.cand_n[chunk_base + sl] = 0;
+        }
+        return;
+    }
+    resolve_warp(cd, chunk_base, n_slots, lane, a);
+}
+
+// Dedup, counts, visits and export of one warp buffer's candidates (rare path).
+__device__ __noinline__ void resolve_warp(Cands cd, long long chunk_base, int n_slots, int lane, const ScanArgs& a) {
+    // keep, per (slot, offset), the deepest candidate (ties: lowest (lane, index))
     bool keep[kCand];
-    std::uint32_t dep[kCand];
+    std::uint32_t dep[kCand], nout[kCand];
 #pragma unroll
     for (int q = 0; q < kCand; ++q) {
         keep[q] = q < cd.n;
         dep[q] = q < cd.n ? __ldg(a.depth + cd.st[q]) : 0u;
+        nout[q] = q < cd.n ? __ldg(a.out_off + cd.st[q] + 1) - __ldg(a.out_off + cd.st[q]) : 0u;
     }
     for (int src = 0; src < 32; ++src) {
         const int nsrc = __shfl_sync(0xffffffffu, cd.n, src);
         for (int r = 0; r < nsrc; ++r) {
-            std::uint32_t o_r = 0, s_r = 0;
+            std::uint32_t k_r = 0, s_r = 0;
 #pragma unroll
             for (int q = 0; q < kCand; ++q)
                 if (q == r) {
-                    o_r = cd.off[q];
+                    k_r = cd.key[q];
                     s_r = cd.st[q];
                 }
-            o_r = __shfl_sync(0xffffffffu, o_r, src);
+            k_r = __shfl_sync(0xffffffffu, k_r, src);
             s_r = __shfl_sync(0xffffffffu, s_r, src);
             const std::uint32_t d_r = __ldg(a.depth + s_r);
 #pragma unroll
             for (int q = 0; q < kCand; ++q) {
-                if (!keep[q] || o_r != cd.off[q]) continue;
+                if (!keep[q] || k_r != cd.key[q]) continue;
                 const bool me = src == lane && r == q;
                 const bool earlier = src < lane || (src == lane && r < q);
                 if (!me && (d_r > dep[q] || (d_r == dep[q] && earlier))) keep[q] = false;
             }
         }
     }
-    unsigned long long mine = 0;
-#pragma unroll
-    for (int q = 0; q < kCand; ++q)
-        if (keep[q]) mine += __ldg(a.out_off + cd.st[q] + 1) - __ldg(a.out_off + cd.st[q]);
-    if (PASS == kCount) {
-        unsigned long long sum = mine;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0) a.chunk_counts[c] = sum;
-        return;
-    }
-    const unsigned long long wr0 = a.chunk_offs[c];
+    // per kept candidate: rank and record prefix among kept candidates of its chunk
+    std::uint32_t rank[kCand];
+    unsigned long long pre[kCand];
 #pragma unroll
     for (int q = 0; q < kCand; ++q) {
-        // slot = outputs of kept candidates at smaller offsets (kept offsets are distinct)
-        unsigned long long before = 0;
+        rank[q] = 0;
+        pre[q] = 0;
+    }
+    for (int src = 0; src < 32; ++src) {
+        const int nsrc = __shfl_sync(0xffffffffu, cd.n, src);
+        for (int r = 0; r < nsrc; ++r) {
+            std::uint32_t k_r = 0, n_r = 0;
+            int kp_r = 0;
+#pragma unroll
+            for (int q = 0; q < kCand; ++q)
+                if (q == r) {
+                    k_r = cd.key[q];
+                    n_r = nout[q];
+                    kp_r = keep[q];
+                }
+            k_r = __shfl_sync(0xffffffffu, k_r, src);
+            n_r = __shfl_sync(0xffffffffu, n_r, src);
+            kp_r = __shfl_sync(0xffffffffu, kp_r, src);
+#pragma unroll
+            for (int q = 0; q < kCand; ++q) {
+                if (!keep[q] || !kp_r) continue;
+                if ((k_r >> 24) == (cd.key[q] >> 24) && k_r < cd.key[q]) {
+                    ++rank[q];
+                    pre[q] += n_r;
+                }
+            }
+        }
+    }
+    // export + visits
+#pragma unroll
+    for (int q = 0; q < kCand; ++q) {
+        if (!keep[q]) continue;
+        const long long c = chunk_base + (cd.key[q] >> 24);
+        if (rank[q] < kExport)
+            reinterpret_cast<uint4*>(a.cands)[c * kExport + rank[q]] =
+                make_uint4(cd.key[q] & 0xFFFFFFu, cd.st[q], static_cast<std::uint32_t>(pre[q]),
+                           static_cast<std::uint32_t>(pre[q] >> 32));
+        if (a.visits) atomicAdd(a.visits + out_rank(cd.st[q], a), 1ull);
+    }
+    // per-chunk totals (lane per slot)
+    for (int sl0 = 0; sl0 < n_slots; sl0 += 32) {
+        const int sl = sl0 + lane;
+        unsigned long long tot = 0;
+        std::uint32_t nk = 0;
         for (int src = 0; src < 32; ++src) {
             const int nsrc = __shfl_sync(0xffffffffu, cd.n, src);
             for (int r = 0; r < nsrc; ++r) {
-                std::uint32_t o_r = 0, s_r = 0;
-                int k_r = 0;
+                std::uint32_t k_r = 0, n_r = 0;
+                int kp_r = 0;
 #pragma unroll
-                for (int z = 0; z < kCand; ++z)
-                    if (z == r) {
-                        o_r = cd.off[z];
-                        s_r = cd.st[z];
-                        k_r = keep[z];
+                for (int q = 0; q < kCand; ++q)
+                    if (q == r) {
+                        k_r = cd.key[q];
+                        n_r = nout[q];
+                        kp_r = keep[q];
                     }
-                o_r = __shfl_sync(0xffffffffu, o_r, src);
-                s_r = __shfl_sync(0xffffffffu, s_r, src);
                 k_r = __shfl_sync(0xffffffffu, k_r, src);
-                if (k_r && keep[q] && o_r < cd.off[q])
-                    before += __ldg(a.out_off + s_r + 1) - __ldg(a.out_off + s_r);
+                n_r = __shfl_sync(0xffffffffu, n_r, src);
+                kp_r = __shfl_sync(0xffffffffu, kp_r, src);
+                if (kp_r && static_cast<int>(k_r >> 24) == sl) {
+                    tot += n_r;
+                    ++nk;
+                }
             }
         }
-        if (keep[q]) {
-            unsigned long long w2 = wr0 + before, dummy = 0;
-            emit<PASS>(cd.st[q], pos0 + cd.off[q], dummy, w2, a);
+        if (sl < n_slots) {
+            a.chunk_counts[chunk_base + sl] = tot;
+            a.cand_n[chunk_base + sl] = nk <= static_cast<std::uint32_t>(kExport) ? nk : 0xFFFFFFFFu;
         }
     }
-}
-
-template <int PASS>
-__device__ __forceinline__ void fixup_chunk(long long c, std::uint32_t tab, int lane, const ScanArgs& a) {
-    const long long pos0 = a.emit_from + c * a.chunk - a.halo;
-    const long long steps = a.halo + a.chunk;
-    const std::uint32_t ne = a.ev_count[c];
-    const uint2* ev = reinterpret_cast<const uint2*>(a.events) + static_cast<unsigned long long>(c) * a.ev_cap;
-    Cands cd;
-    cd.n = 0;
-    if (ne <= a.ev_cap)
-        for (std::uint32_t j = lane; j < ne; j += 32) walk_event(ev[j], pos0, steps, tab, cd, a);
-    const bool overflow = __any_sync(0xffffffffu, cd.n > kCand) || ne > a.ev_cap;
-    if (overflow) {
-        if (lane == 0) exact_chunk_walk<PASS>(c, a);
-        return;
-    }
-    if (!__any_sync(0xffffffffu, cd.n > 0)) {
-        if (PASS == kCount && lane == 0) a.chunk_counts[c] = 0;
-        return;
-    }
-    resolve_candidates<PASS>(c, cd, lane, a);
 }
 
 // Persistent: one CTA per SM stages the truncated table once; warps stride
-// over the chunks (COUNT: all; WRITE: the compacted chunks with matches).
-template <int PASS>
+// over the K1s warp buffers.
+template <int U>
 __global__ void __launch_bounds__(1024, 1) fixup_kernel(const ScanArgs a) {
     extern __shared__ __align__(16) std::uint8_t smem[];
     const std::uint32_t tab = smem_u32(smem);
     const int lane = threadIdx.x & 31;
-    const long long n_work = PASS == kWrite ? static_cast<long long>(*a.active_count) : a.n_chunks;
+    const long long n_work = (a.n_chunks + 32 * U - 1) / (32 * U);
     const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
     const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if ((static_cast<long long>(blockIdx.x) * blockDim.x >> 5) >= n_work) return;
@@ -654,8 +849,40 @@ __global__ void __launch_bounds__(1024, 1) fixup_kernel(const ScanArgs a) {
         for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     __syncthreads();
-    for (long long w = w0; w < n_work; w += warps)
-        fixup_chunk<PASS>(PASS == kWrite ? static_cast<long long>(a.active_list[w]) : w, tab, lane, a);
+    for (long long w = w0; w < n_work; w += warps) fixup_warp<U>(w, tab, lane, a);
+}
+
+// Sparse-mode emit: one thread per chunk with matches writes the exported
+// candidates' records at the chunk's slot range; a chunk whose export
+// overflowed is replayed exactly (records only; its visits were counted).
+__global__ void __launch_bounds__(256) sparse_emit_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    const std::uint32_t tab = smem_u32(smem);
+    const long long n_work = static_cast<long long>(*a.active_count);
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    bool need_tab = false;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n_work; t += stride)
+        need_tab |= a.cand_n[a.active_list[t]] == 0xFFFFFFFFu;
+    if (__syncthreads_or(need_tab)) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        __syncthreads();
+    }
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n_work; t += stride) {
+        const long long c = a.active_list[t];
+        const std::uint32_t nk = a.cand_n[c];
+        if (nk == 0xFFFFFFFFu) {
+            exact_chunk_walk<kWrite>(c, tab, a);
+            continue;
+        }
+        const long long pos0 = a.emit_from + c * a.chunk - a.halo;
+        for (std::uint32_t i = 0; i < nk; ++i) {
+            const uint4 cd = reinterpret_cast<const uint4*>(a.cands)[c * kExport + i];
+            unsigned long long wr = a.chunk_offs[c] + (static_cast<unsigned long long>(cd.w) << 32 | cd.z), dummy = 0;
+            emit<kWrite>(cd.y, pos0 + cd.x, dummy, wr, a);
+        }
+    }
 }
 
 // Compacts the ids of chunks with at least one match (order is irrelevant:

@@ -60,6 +60,19 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         _run([NVCC, *ARCH, "-shared", "-o", lib, auto_o, dev_o, "-Xcompiler", "-pthread"])
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment builds (kernel ablations) into lib/variants/<name>/libacg.so."""
+    out = os.path.join(LIB, "variants", name)
+    os.makedirs(out, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+    dev_o = os.path.join(out, "acg_device.o")
+    _run([NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", "-o", dev_o,
+          os.path.join(CSRC, "acg_device.cu")] + inc + [f"-D{d}" for d in defines])
+    lib = os.path.join(out, "libacg.so")
+    _run([NVCC, *ARCH, "-shared", "-o", lib, os.path.join(LIB, "obj", "automaton.o"), dev_o, "-Xcompiler", "-pthread"])
+    return lib
+
+
 def build_oracle() -> None:
     """Test infrastructure: the C restatement and (when /root/reference is
     present) the reference compiled into oracle/_ref/."""
