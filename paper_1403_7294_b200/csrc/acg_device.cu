@@ -131,11 +131,15 @@ struct acg_scanner {
     std::uint32_t U_run = 4;  // interleave of the last run
     std::uint32_t tpb_run = acg::kern::kTPB;
     unsigned long long chunk_override = 0;
+    // last run's arguments (a sparse run whose task list overflowed is re-run at sync)
+    const std::uint8_t* run_text = nullptr;
+    std::uint64_t run_n = 0, run_emit = 0, run_base = 0;
+    unsigned long long min_task_cap = 0;
     // mode: requested (ACG_MODE_*), used by the last run, and the event rate seen
     int mode_req = 0;
     int mode_run = 0;
     double last_event_rate = -1.0;
-    DevBuf<std::uint32_t> events, ev_count, cands, cand_n;
+    DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
     cudaEvent_t ev[6] = {};
@@ -259,27 +263,41 @@ cudaError_t launch_sparse(const ScanArgs& args, unsigned grid, unsigned tpb, std
     return cudaGetLastError();
 }
 
-constexpr unsigned kFixupTPB = 1024;  // 32 warps, one K1s warp buffer per warp at a time
-
+// Sparse-mode fix-up: F1 re-walk (tasks), F2 excursion walks, F3 resolve.
+unsigned fixup_rewalk_grid(unsigned long long bufs, int sms) {
+    return static_cast<unsigned>(std::max<unsigned long long>(1, std::min<unsigned long long>((bufs + 31) / 32, sms)));
+}
 template <int U>
-cudaError_t launch_fixup_u(const ScanArgs& args, std::size_t smem, cudaStream_t st) {
-    auto k = acg::kern::fixup_kernel<U>;
-    if (cudaError_t e = prepare_smem(k, smem)) return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+cudaError_t launch_fixup_u(const ScanArgs& args, std::size_t smem, int sms, cudaStream_t st) {
+    using namespace acg::kern;
     const unsigned long long bufs = (args.n_chunks + 32ull * U - 1) / (32ull * U);
-    const unsigned g = static_cast<unsigned>(
-        std::max<unsigned long long>(1, std::min<unsigned long long>((bufs + 31) / 32, sms)));
-    k<<<g, kFixupTPB, smem, st>>>(args);
-    return cudaGetLastError();
+    const unsigned g1 = fixup_rewalk_grid(bufs, sms);
+    {
+        auto k = fixup_rewalk_kernel<U>;
+        if (cudaError_t e = prepare_smem(k, smem)) return e;
+        k<<<g1, 1024, smem, st>>>(args);
+        if (cudaError_t e = cudaGetLastError()) return e;
+    }
+    {
+        const unsigned g2 = std::max(1u, std::min<unsigned>(g1 * 32u * 2u / 8u, static_cast<unsigned>(sms) * 8u));
+        fixup_walk_kernel<U><<<g2, 256, 0, st>>>(args, g1 * 32u);
+        if (cudaError_t e = cudaGetLastError()) return e;
+    }
+    {
+        auto k = fixup_resolve_kernel<U>;
+        if (cudaError_t e = prepare_smem(k, smem)) return e;
+        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(1, std::min<unsigned long long>((bufs + 15) / 16, sms)));
+        k<<<g, 512, smem, st>>>(args);
+        if (cudaError_t e = cudaGetLastError()) return e;
+    }
+    return cudaSuccess;
 }
 
-cudaError_t launch_fixup(std::uint32_t U, const ScanArgs& args, std::size_t smem, cudaStream_t st) {
+cudaError_t launch_fixup(std::uint32_t U, const ScanArgs& args, std::size_t smem, int sms, cudaStream_t st) {
     switch (U) {
-        case 1: return launch_fixup_u<1>(args, smem, st);
-        case 2: return launch_fixup_u<2>(args, smem, st);
-        default: return launch_fixup_u<4>(args, smem, st);
+        case 1: return launch_fixup_u<1>(args, smem, sms, st);
+        case 2: return launch_fixup_u<2>(args, smem, sms, st);
+        default: return launch_fixup_u<4>(args, smem, sms, st);
     }
 }
 
@@ -367,6 +385,10 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     s->launches = 0;
     s->synced = false;
     s->last = st;
+    s->run_text = d_text;
+    s->run_n = n;
+    s->run_emit = emit_from;
+    s->run_base = base;
     const std::uint64_t owned = n - emit_from;
     // mode: sparse (truncated automaton + fix-up) when the automaton allows it
     // and excursions were rare on the previous run; exact otherwise
@@ -451,6 +473,26 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         ACG_CUDA(s->ev_count.reserve(n_warps));
         ACG_CUDA(s->cands.reserve(s->n_chunks * acg::kern::kExport * 4ull));
         ACG_CUDA(s->cand_n.reserve(s->n_chunks));
+        ACG_CUDA(s->cand_list.reserve(n_warps * acg::kern::kCandList * 2ull));
+        ACG_CUDA(s->cand_cnt.reserve(n_warps));
+        ACG_CUDA(cudaMemsetAsync(s->cand_cnt.p, 0, n_warps * sizeof(std::uint32_t), st));
+        a.cand_list = s->cand_list.p;
+        a.cand_cnt = s->cand_cnt.p;
+        // excursion tasks: one region per fix-up warp; sized from the previous run's event
+        // rate with headroom (1 per 16 walked bytes at first); overflow re-runs at sync
+        const unsigned long long walked = s->n_chunks * walk;
+        const double rate = s->last_event_rate > 0 ? s->last_event_rate : 1.0 / 16;
+        const unsigned long long regions = fixup_rewalk_grid(n_warps, dd.num_sms) * 32ull;
+        unsigned long long rcap = static_cast<unsigned long long>(walked * std::min(1.0, rate * 3.0) / regions) + 1024;
+        rcap = std::max(rcap, s->min_task_cap);
+        rcap = std::min<unsigned long long>(rcap, 0x7FFFFFFFull);
+        ACG_CUDA(s->tasks.reserve(regions * rcap * 4ull));
+        ACG_CUDA(s->task_cnt.reserve(regions));
+        a.tasks = s->tasks.p;
+        a.task_cnt = s->task_cnt.p;
+        a.task_max = s->scalars32.p + 1;
+        a.task_cap = static_cast<std::uint32_t>(rcap);
+        ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 1, 0, sizeof(std::uint32_t), st));
         a.events = s->events.p;
         a.cands = s->cands.p;
         a.cand_n = s->cand_n.p;
@@ -460,8 +502,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         ACG_CUDA(launch_sparse_u(s->U_run, a, s->grid, s->tpb_run, smem_sparse(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
-        ACG_CUDA(launch_fixup(s->U_run, a, smem_sparse(dd), st));
-        ++s->launches;
+        ACG_CUDA(launch_fixup(s->U_run, a, smem_sparse(dd), dd.num_sms, st));
+        s->launches += 3;
     } else {
         ACG_CUDA(launch_exact_pass(d.mode, kCount, stats, s->U_run, a, s->grid, s->tpb, smem_bytes(dd), st));
         ++s->launches;
@@ -502,7 +544,20 @@ int scanner_sync(acg_scanner* s) {
                              cudaMemcpyDeviceToHost, st));
     ACG_CUDA(cudaMemcpyAsync(s->pinned + 5, s->scalars64.p + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              st));
+    ACG_CUDA(cudaMemcpyAsync(s->pinned + 6, s->scalars32.p, 2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
     ACG_CUDA(cudaStreamSynchronize(st));
+    if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
+        const std::uint32_t ntask = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[1];
+        if (ntask > s->args.task_cap) {  // a task region overflowed: grow and run again
+            s->min_task_cap = ntask + ntask / 4 + 1024;
+            const int req = s->mode_req;
+            s->mode_req = ACG_MODE_SPARSE;
+            const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
+            s->mode_req = req;
+            if (rc) return rc;
+            return scanner_sync(s);
+        }
+    }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
     if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
         const double walked = static_cast<double>(s->n_chunks) * static_cast<double>(s->chunk + s->dd->dfa->halo);

@@ -87,6 +87,12 @@ struct ScanArgs {
     std::uint32_t* ev_count;                // per K1s warp (may exceed ev_cap: overflow)
     std::uint32_t ev_cap;
     std::uint32_t* cands;                   // per chunk kExport exported candidates (uint4)
+    std::uint32_t* cand_list;               // per K1s warp buffer: kCandList (key, state) pairs
+    std::uint32_t* cand_cnt;                // per K1s warp buffer: candidates appended (zeroed per run)
+    std::uint32_t* tasks;                   // excursion tasks (uint4): one region of task_cap per fix-up warp
+    std::uint32_t* task_cnt;                // per region: tasks appended
+    std::uint32_t* task_max;                // max over regions (overflow check at sync)
+    std::uint32_t task_cap;
     std::uint32_t* cand_n;                  // per chunk: exported count, 0xFFFFFFFF = re-walk
     unsigned long long* ev_total;           // sum of events (mode heuristic)
 };
@@ -323,8 +329,9 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
 // Event log. After each 16-step block the warp ballots its flagged streams and
 // writes their events to consecutive slots of a per-warp buffer (coalesced):
 //   w0 = walk offset of the block | flag bits << 17 | stream slot (lane*U+u) << 21
+//        | w2 valid << 28 | w3 valid << 29
 //   w1 = A_H state at sub-blocks 0,1 (u16 each), w2 = sub-blocks 2,3
-//   w3 = the block's 16 packed 2-bit columns (0xFFFFFFFF: per-byte block, re-read text)
+//   w3 = this block's 16 packed 2-bit columns (valid if w0 bit 28)
 __device__ __forceinline__ std::uint32_t lds_hot(std::uint32_t off) {
     std::uint16_t v;
     asm volatile("{ .reg .u32 t; mov.u32 t, acg_hot_smem; add.u32 t, t, %1; ld.shared.u16 %0, [t]; }"
@@ -354,7 +361,7 @@ __device__ __forceinline__ uint4 ldg_text(const std::uint8_t* p) {
     return make_uint4(m, m ^ 0x02020202u, m ^ 0x04040404u, m ^ 0x06060606u);
 #endif
     uint4 v;
-    asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
     return v;
@@ -367,7 +374,7 @@ __device__ __forceinline__ void ldg_text32(const std::uint8_t* p, uint4& lo, uin
     hi = ldg_text(p + 16);
     return;
 #endif
-    asm volatile("ld.global.nc.L2::128B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.L2::128B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
                  : "l"(p));
 }
@@ -548,8 +555,9 @@ __global__ void __launch_bounds__(TPB, 1) sparse_scan_kernel(const ScanArgs a) {
                 if (m) {
                     if (fl[u]) {
                         const std::uint32_t idx = min(wn + static_cast<std::uint32_t>(__popc(m & lt_mask)), wcap - 1);
-                        evw[idx] = make_uint4(off | (fl[u] << 17) | (static_cast<std::uint32_t>(lane * U + u) << 21),
-                                              s01[u], s23[u], fast ? pack_cols(buf[u][b]) : 0xFFFFFFFFu);
+                        evw[idx] = make_uint4(off | (fl[u] << 17) | (static_cast<std::uint32_t>(lane * U + u) << 21) |
+                                                  (fast ? 1u << 28 : 0u),
+                                              s01[u], s23[u], fast ? pack_cols(buf[u][b]) : 0u);
                     }
                     wn += static_cast<std::uint32_t>(__popc(m));
                 }
@@ -596,7 +604,8 @@ __global__ void __launch_bounds__(TPB, 1) sparse_scan_kernel(const ScanArgs a) {
 // prefix inside the chunk) for the emit pass. Candidates are rare in sparse
 // mode; a lane holding more than kCand of them makes the warp fall back to an
 // exact replay of its chunks.
-constexpr int kCand = 8;
+constexpr int kCand = 8;      // candidates per lane in the resolver (32*kCand per buffer)
+constexpr int kCandList = 256;  // per-buffer candidate list in global memory
 constexpr int kExport = 8;  // exported candidates per chunk (more: emit re-walks the chunk)
 
 struct Cands {
@@ -610,51 +619,60 @@ __device__ __forceinline__ int text_col(const ScanArgs& a, long long p) {
     return column_of<0>(b, nullptr, a);
 }
 
+// Full-DFA walk from (s, col) at walk offset i until the state is hot again;
+// collects candidate outputs. Columns past the logged block come from the text.
+__device__ __forceinline__ void excursion(std::uint32_t s, std::uint32_t col, long long i, long long boff,
+                                          std::uint32_t win, bool wok, long long pos0, long long steps,
+                                          std::uint32_t slot, Cands& cd, const ScanArgs& a) {
+    std::uint32_t x = __ldg(a.next + s * 4u + col);
+    for (;;) {
+        if (i >= a.halo && has_out(x, a)) {
+            if (cd.n < kCand) {
+                cd.key[cd.n] = (slot << 24) | static_cast<std::uint32_t>(i);
+                cd.st[cd.n] = x;
+            }
+            ++cd.n;
+        }
+        if (x < a.H || i + 1 >= steps) return;
+        ++i;
+        const long long d = i - boff;
+        const int cc = (wok && d < 16) ? static_cast<int>((win >> (2 * d)) & 3u) : text_col(a, pos0 + i);
+        x = cc < 0 ? 0u : __ldg(a.next + x * 4u + static_cast<std::uint32_t>(cc));
+    }
+}
+
 __device__ __forceinline__ void walk_event(const uint4 e, long long chunk_base, std::uint32_t tab, Cands& cd,
                                            const ScanArgs& a) {
     const long long boff = e.x & 0x1FFFFu;
-    std::uint32_t fl = (e.x >> 17) & 0xFu;
-    const std::uint32_t slot = e.x >> 21;
-    const std::uint32_t pk = e.w;
-    const bool pk_ok = pk != 0xFFFFFFFFu;
+    const std::uint32_t fl = (e.x >> 17) & 0xFu;
+    const std::uint32_t slot = (e.x >> 21) & 0x7Fu;
+    const bool wok = (e.x >> 28) & 1u;
     const long long pos0 = a.emit_from + (chunk_base + slot) * a.chunk - a.halo;
     const long long steps = a.halo + a.chunk;
-    const std::uint32_t H = a.H;
-    auto col_at = [&](long long o) -> int {
-        if (pk_ok && (o >> 4) == (boff >> 4)) return static_cast<int>((pk >> (2 * (o & 15))) & 3u);
-        return text_col(a, pos0 + o);
-    };
-    while (fl) {
-        const int j = __ffs(fl) - 1;
-        fl &= fl - 1;
-        std::uint32_t s = ((j < 2 ? e.y : e.z) >> (16 * (j & 1))) & 0x7FFFu;
-        const long long sb = boff + 4 * j;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            const long long i = sb + kk;
-            const int col = col_at(i);
+    // re-walk A_H from the first flagged sub-block to the end of the last one
+    const int j0 = __ffs(fl) - 1, j1 = 31 - __clz(fl);
+    std::uint32_t s = e.y;
+    if (wok) {
+        for (int d = 4 * j0; d < 4 * j1 + 4; ++d) {
+            const std::uint32_t col = (e.z >> (2 * d)) & 3u;
+            const std::uint32_t v = lds_u16(tab + (s << 3) + (col << 1));
+#ifndef ACG_ABLATE_FIX_EXC
+            if (v & 0x8000u) excursion(s, col, boff + d, boff, e.z, true, pos0, steps, slot, cd, a);
+#else
+            if (v == 0x12345u) cd.n = 99;
+#endif
+            s = v & 0x7FFFu;
+        }
+    } else {  // block with escapes / text edges: columns from the text
+        for (int d = 4 * j0; d < 4 * j1 + 4; ++d) {
+            const int col = text_col(a, pos0 + boff + d);
             if (col < 0) {
                 s = 0;
                 continue;
             }
             const std::uint32_t v = lds_u16(tab + (s << 3) + (static_cast<std::uint32_t>(col) << 1));
-            if (v & 0x8000u) {
-                std::uint32_t x = __ldg(a.next + s * 4u + static_cast<std::uint32_t>(col));
-                long long k = i;
-                for (;;) {
-                    if (k >= a.halo && has_out(x, a)) {
-                        if (cd.n < kCand) {
-                            cd.key[cd.n] = (slot << 24) | static_cast<std::uint32_t>(k);
-                            cd.st[cd.n] = x;
-                        }
-                        ++cd.n;
-                    }
-                    if (x < H || k + 1 >= steps) break;
-                    ++k;
-                    const int cc = col_at(k);
-                    x = cc < 0 ? 0u : __ldg(a.next + x * 4u + static_cast<std::uint32_t>(cc));
-                }
-            }
+            if (v & 0x8000u)
+                excursion(s, static_cast<std::uint32_t>(col), boff + d, boff, 0u, false, pos0, steps, slot, cd, a);
             s = v & 0x7FFFu;
         }
     }
@@ -694,32 +712,219 @@ __device__ __noinline__ void exact_chunk_walk(long long c, std::uint32_t tab, co
 
 __device__ __noinline__ void resolve_warp(Cands cd, long long chunk_base, int n_slots, int lane, const ScanArgs& a);
 
+// F1: re-walk the flagged sub-blocks of one warp buffer (lanes over events,
+// coalesced reads), appending one excursion task per flagged step:
+//   w0 = chunk index, w1 = walk offset | A_H state before the step << 17,
+//   w2 = column | block columns valid << 2, w3 = the block's packed columns.
 template <int U>
-__device__ void fixup_warp(long long wid, std::uint32_t tab, int lane, const ScanArgs& a) {
+__device__ void fixup_rewalk_warp(long long wid, std::uint32_t tab, int lane, uint4* region, std::uint32_t& nreg,
+                                  const ScanArgs& a) {
+    const long long chunk_base = wid * 32 * U;
+    const std::uint32_t ne = a.ev_count[wid];
+    if (ne > a.ev_cap) {  // cannot happen (one slot per block and stream); defensive
+        if (lane == 0) a.cand_cnt[wid] = 0xFFFFFFFFu;
+        return;
+    }
+    const uint4* ev = reinterpret_cast<const uint4*>(a.events) + static_cast<unsigned long long>(wid) * a.ev_cap;
+    const unsigned lt = (1u << lane) - 1u;
+    for (std::uint32_t base = 0; base < ne; base += 32) {
+        const std::uint32_t j = base + lane;
+        const bool have = j < ne;
+        const uint4 e = have ? ev[j] : make_uint4(0, 0, 0, 0);
+        const long long boff = e.x & 0x1FFFFu;
+        std::uint32_t fl = have ? (e.x >> 17) & 0xFu : 0u;
+        const std::uint32_t slot = (e.x >> 21) & 0x7Fu;
+        const bool wok = (e.x >> 28) & 1u;
+        const long long chunk = chunk_base + slot;
+        const long long pos0 = a.emit_from + chunk * a.chunk - a.halo;
+        // one round per flagged sub-block of the busiest lane (usually one)
+        while (__any_sync(0xffffffffu, fl != 0)) {
+            const bool act = fl != 0;
+            const int jj = act ? __ffs(fl) - 1 : 0;
+            fl &= fl - 1;
+            std::uint32_t s = ((jj < 2 ? e.y : e.z) >> (16 * (jj & 1))) & 0x7FFFu;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int d = 4 * jj + kk;
+                bool task = false;
+                std::uint32_t col = 0;
+                const std::uint32_t sprev = s;
+                if (act) {
+                    int c;
+                    if (wok) c = static_cast<int>((e.w >> (2 * d)) & 3u);
+                    else c = text_col(a, pos0 + boff + d);
+                    if (c < 0) {
+                        s = 0;
+                    } else {
+                        col = static_cast<std::uint32_t>(c);
+                        const std::uint32_t v = lds_u16(tab + (s << 3) + (col << 1));
+                        task = (v & 0x8000u) != 0;
+                        s = v & 0x7FFFu;
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, task);
+                if (m) {
+                    if (task) {
+                        const std::uint32_t q = nreg + __popc(m & lt);
+                        if (q < a.task_cap)
+                            region[q] = make_uint4(static_cast<std::uint32_t>(chunk),
+                                                   static_cast<std::uint32_t>(boff + d) | (sprev << 17),
+                                                   col | (wok ? 4u : 0u), e.w);
+                    }
+                    nreg += static_cast<std::uint32_t>(__popc(m));
+                }
+            }
+        }
+    }
+}
+
+template <int U>
+__global__ void __launch_bounds__(1024, 1) fixup_rewalk_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    const std::uint32_t tab = smem_u32(smem);
+    const int lane = threadIdx.x & 31;
+    const long long n_work = (a.n_chunks + 32 * U - 1) / (32 * U);
+    const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if ((static_cast<long long>(blockIdx.x) * blockDim.x >> 5) >= n_work) return;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    // each fix-up warp appends its tasks to its own region (task_cap tasks) with a register counter
+    uint4* region = reinterpret_cast<uint4*>(a.tasks) + static_cast<unsigned long long>(w0) * a.task_cap;
+    std::uint32_t nreg = 0;
+    for (long long w = w0; w < n_work; w += warps) fixup_rewalk_warp<U>(w, tab, lane, region, nreg, a);
+    if (lane == 0) {
+        a.task_cnt[w0] = nreg;
+        atomicMax(a.task_max, nreg);
+    }
+}
+
+// F2: one thread per excursion task: walk the full DFA (L2) from the exact or
+// proxy state until the state is hot again; candidates go to the task's
+// buffer list.
+constexpr int kWalkILP = 4;
+
+template <int U>
+__device__ __forceinline__ void record_cand(long long chunk, long long i, std::uint32_t x, const ScanArgs& a) {
+    const long long wid = chunk / (32 * U);
+    const std::uint32_t slot = static_cast<std::uint32_t>(chunk - wid * 32 * U);
+    const std::uint32_t q = atomicAdd(a.cand_cnt + wid, 1u);
+    if (q < kCandList)
+        reinterpret_cast<uint2*>(a.cand_list)[static_cast<unsigned long long>(wid) * kCandList + q] =
+            make_uint2((slot << 24) | static_cast<std::uint32_t>(i), x);
+}
+
+// F2: two warps per task region; every lane walks kWalkILP tasks at once
+// (independent dependent-lookup chains interleaved).
+template <int U>
+__global__ void __launch_bounds__(256) fixup_walk_kernel(const ScanArgs a, std::uint32_t n_regions) {
+    const long long steps = a.halo + a.chunk;
+    const std::uint32_t H = a.H;
+    const std::uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const std::uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (std::uint32_t rw = gw; rw < 2 * n_regions; rw += nw) {
+        const std::uint32_t r = rw >> 1, half = rw & 1;
+        const std::uint32_t nt = min(a.task_cnt[r], a.task_cap);
+        const uint4* tks = reinterpret_cast<const uint4*>(a.tasks) + static_cast<unsigned long long>(r) * a.task_cap;
+        // lanes of this warp take tasks half*32 + lane + 64*q (q = 0, 1, ...), kWalkILP at a time
+        for (std::uint32_t t0 = half * 32 + lane; t0 < nt; t0 += 64 * kWalkILP) {
+            std::uint32_t x[kWalkILP], pk[kWalkILP];
+            long long i[kWalkILP], boff[kWalkILP], chunk[kWalkILP];
+            bool live[kWalkILP], wok[kWalkILP];
+#pragma unroll
+            for (int c = 0; c < kWalkILP; ++c) {
+                const std::uint32_t t = t0 + 64u * c;
+                live[c] = t < nt;
+                const uint4 tk = live[c] ? tks[t] : make_uint4(0, 0, 0, 0);
+                chunk[c] = tk.x;
+                i[c] = tk.y & 0x1FFFFu;
+                boff[c] = i[c] & ~15ll;
+                wok[c] = (tk.z >> 2) & 1u;
+                pk[c] = tk.w;
+                x[c] = live[c] ? __ldg(a.next + (tk.y >> 17) * 4u + (tk.z & 3u)) : 0u;
+            }
+            for (;;) {
+                bool any = false;
+#pragma unroll
+                for (int c = 0; c < kWalkILP; ++c) {
+                    if (!live[c]) continue;
+                    if (i[c] >= a.halo && has_out(x[c], a)) record_cand<U>(chunk[c], i[c], x[c], a);
+                    if (x[c] < H || i[c] + 1 >= steps) {
+                        live[c] = false;
+                        continue;
+                    }
+                    any = true;
+                    ++i[c];
+                    const long long d = i[c] - boff[c];
+                    const long long pos0 = a.emit_from + chunk[c] * a.chunk - a.halo;
+                    const int cc = (wok[c] && d < 16) ? static_cast<int>((pk[c] >> (2 * d)) & 3u) : text_col(a, pos0 + i[c]);
+                    x[c] = cc < 0 ? 0u : __ldg(a.next + x[c] * 4u + static_cast<std::uint32_t>(cc));
+                }
+                if (!any) break;
+            }
+        }
+    }
+}
+
+// F3: per warp buffer: counts (and, when candidates exist, dedup + export).
+template <int U>
+__device__ void fixup_resolve_warp(long long wid, std::uint32_t tab, int lane, const ScanArgs& a) {
     const long long chunk_base = wid * 32 * U;
     const int n_slots = static_cast<int>(min(static_cast<long long>(32 * U), a.n_chunks - chunk_base));
-    const std::uint32_t ne = a.ev_count[wid];
-    const uint4* ev = reinterpret_cast<const uint4*>(a.events) + static_cast<unsigned long long>(wid) * a.ev_cap;
-    Cands cd;
-    cd.n = 0;
-    if (ne <= a.ev_cap)
-        for (std::uint32_t j = lane; j < ne; j += 32) walk_event(ev[j], chunk_base, tab, cd, a);
-    const bool overflow = __any_sync(0xffffffffu, cd.n > kCand) || ne > a.ev_cap;
-    if (overflow) {  // exact replay of every chunk of this buffer, one lane per chunk (rare)
+    const std::uint32_t nc = a.cand_cnt[wid];
+    if (nc > 32u * kCand) {  // exact replay of every chunk of this buffer, one lane per chunk (practically never)
         for (int sl = lane; sl < n_slots; sl += 32) {
             a.cand_n[chunk_base + sl] = 0xFFFFFFFFu;  // emit pass re-walks
             exact_chunk_walk<kCount>(chunk_base + sl, tab, a);
         }
         return;
     }
-    if (!__any_sync(0xffffffffu, cd.n > 0)) {
+    if (nc == 0) {
         for (int sl = lane; sl < n_slots; sl += 32) {
             a.chunk_counts[chunk_base + sl] = 0;
             a.cand_n[chunk_base + sl] = 0;
         }
         return;
     }
+    Cands cd;
+    cd.n = 0;
+    const uint2* cl = reinterpret_cast<const uint2*>(a.cand_list) + static_cast<unsigned long long>(wid) * kCandList;
+#pragma unroll
+    for (int q = 0; q < kCand; ++q) {
+        const std::uint32_t idx = static_cast<std::uint32_t>(lane) + 32u * q;
+        if (idx < nc) {
+            const uint2 v = cl[idx];
+            cd.key[q] = v.x;
+            cd.st[q] = v.y;
+            cd.n = q + 1;
+        }
+    }
     resolve_warp(cd, chunk_base, n_slots, lane, a);
+}
+
+template <int U>
+__global__ void __launch_bounds__(512, 1) fixup_resolve_kernel(const ScanArgs a) {
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    const std::uint32_t tab = smem_u32(smem);
+    const int lane = threadIdx.x & 31;
+    const long long n_work = (a.n_chunks + 32 * U - 1) / (32 * U);
+    const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if ((static_cast<long long>(blockIdx.x) * blockDim.x >> 5) >= n_work) return;
+    // the table is only needed by the exact fallback
+    bool need = false;
+    for (long long w = w0; w < n_work; w += warps) need |= a.cand_cnt[w] > 32u * kCand;
+    if (__syncthreads_or(need)) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        __syncthreads();
+    }
+    for (long long w = w0; w < n_work; w += warps) fixup_resolve_warp<U>(w, tab, lane, a);
 }
 
 // Dedup, counts, visits and export of one warp buffer's candidates (rare path).
@@ -830,26 +1035,6 @@ __device__ __noinline__ void resolve_warp(Cands cd, long long chunk_base, int n_
             a.cand_n[chunk_base + sl] = nk <= static_cast<std::uint32_t>(kExport) ? nk : 0xFFFFFFFFu;
         }
     }
-}
-
-// Persistent: one CTA per SM stages the truncated table once; warps stride
-// over the K1s warp buffers.
-template <int U>
-__global__ void __launch_bounds__(1024, 1) fixup_kernel(const ScanArgs a) {
-    extern __shared__ __align__(16) std::uint8_t smem[];
-    const std::uint32_t tab = smem_u32(smem);
-    const int lane = threadIdx.x & 31;
-    const long long n_work = (a.n_chunks + 32 * U - 1) / (32 * U);
-    const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-    const long long w0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if ((static_cast<long long>(blockIdx.x) * blockDim.x >> 5) >= n_work) return;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
-        uint4* dst = reinterpret_cast<uint4*>(smem);
-        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    __syncthreads();
-    for (long long w = w0; w < n_work; w += warps) fixup_warp<U>(w, tab, lane, a);
 }
 
 // Sparse-mode emit: one thread per chunk with matches writes the exported
