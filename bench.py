@@ -38,6 +38,21 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
+def golden_check(w, m: int, dsum: int, dxor: int, counts) -> str:
+    """Compare the timed run's output with the reference's own statistics for
+    this workload (tests/golden/configs_full.json, from oracle/make_goldens.py)."""
+    import hashlib
+    p = os.path.join(ROOT, "tests", "golden", "configs_full.json")
+    try:
+        with open(p) as f:
+            case = next(c for c in json.load(f)["cases"] if c["name"] == w.name and c["n"] == w.n)
+    except (OSError, StopIteration, ValueError):
+        return "no golden for this workload"
+    sha = hashlib.sha256(np.asarray(counts, dtype="<u8").tobytes()).hexdigest()
+    ok = (m, dsum, dxor, sha) == (case["m"], case["dsum"], case["dxor"], case["counts_sha256"])
+    return "bit-exact vs reference (count, digest, per-pattern counts)" if ok else "MISMATCH vs reference golden"
+
+
 def peaks() -> tuple[float, str]:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -210,6 +225,7 @@ def main() -> None:
     import torch
     import torch.distributed as dist
     from paper_1403_7294_b200 import acmatch as am
+    from paper_1403_7294_b200 import shards
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -219,20 +235,19 @@ def main() -> None:
     # weak scaling: rank r owns [r*n, (r+1)*n) of a world*n byte text; the
     # dictionary is the workload's (its substrings come from the first n bytes)
     n = w.n
-    shard_lo = rank * n
     a = am.Automaton.from_arrays(concat, offs)
     halo_guess = ((int((offs[1:] - offs[:-1]).max()) + 15) // 16) * 16
-    start = max(0, shard_lo - halo_guess)
+    sh = shards.weak_shard(n, world, rank, halo_guess)
+    start, emit_from = sh.start, sh.emit_from
     from dataclasses import replace
     wt = replace(w, n=world * n)
-    h_text = torch.empty(shard_lo + n - start, dtype=torch.uint8, pin_memory=True)
-    synth.text(wt, start, shard_lo + n, out=h_text.numpy())
+    h_text = torch.empty(sh.window, dtype=torch.uint8, pin_memory=True)
+    synth.text(wt, sh.start, sh.hi, out=h_text.numpy())
     if args.profile_layout:
         a.optimize_layout(h_text.numpy()[: 1 << 20])
     lay = a.layout()
     assert lay["halo"] == halo_guess
     d_text = h_text.cuda()
-    emit_from = shard_lo - start
 
     flags = am.SCAN_LIST | am.SCAN_COUNTS | am.SCAN_PROFILE
     sc = am.Scanner(a, local, flags)
@@ -247,7 +262,7 @@ def main() -> None:
         if world > 1:
             sc.copy_pattern_counts(counts_all.data_ptr(), stream.cuda_stream)
             with torch.cuda.stream(stream):
-                dist.all_reduce(counts_all)
+                shards.reduce_counts(counts_all)
 
     for _ in range(args.warmup):
         step()
@@ -353,6 +368,8 @@ def main() -> None:
         "check": {"digest_sum": dsum, "digest_xor": dxor, "unsorted_pairs": unsorted,
                   "count_sum": int(counts_local.sum())},
     }
+    if world == 1:
+        line["check"]["golden"] = golden_check(w, int(m_total), dsum, dxor, counts_local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(w, concat, offs, args.cpu_sample_mib << 20, os.cpu_count(), 1, 0)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

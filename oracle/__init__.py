@@ -61,6 +61,8 @@ _REF_SYMS = {
     "ref_scan": (u64, [vp, vp, u64, C.POINTER(u64), vp, vp, u64]),
     "ref_scan_window_stats": (C.c_int, [vp, vp, u64, u64, u64, vp, C.POINTER(u64), C.POINTER(u64),
                                         C.POINTER(u64), C.POINTER(u64)]),
+    "ref_window_digest": (C.c_int, [vp, vp, u64, u64, u64, vp, C.POINTER(u64), C.POINTER(u64),
+                                    C.POINTER(u64), C.POINTER(u64)]),
     "ref_run_partitioned": (C.c_int, [vp, vp, u32, vp, u64, u32, vp, vp, u64, C.POINTER(u64),
                                       C.POINTER(C.c_double), C.POINTER(u32)]),
     "ref_partitioned_prepare": (vp, [vp, vp, u32, u32]),
@@ -293,6 +295,16 @@ class RefAutomaton:
         m, s, x, f = u64(acc["m"]), u64(acc["dsum"]), u64(acc["dxor"]), u64(acc["follows"])
         rc = ref().ref_scan_window_stats(self._h, _ptr(t), t.size, start, emit_from, _ptr(counts), C.byref(m),
                                          C.byref(s), C.byref(x), C.byref(f))
+        acc.update(m=m.value, dsum=s.value, dxor=x.value, follows=f.value)
+        return rc
+
+    def window_digest(self, window, emit_from: int, abs_base: int, counts: np.ndarray, acc: dict) -> int:
+        """Reference scan of `window` (from the root) keeping ends >= emit_from;
+        digest keys use absolute ends abs_base + end."""
+        t = _u8(window)
+        m, s, x, f = u64(acc["m"]), u64(acc["dsum"]), u64(acc["dxor"]), u64(acc["follows"])
+        rc = ref().ref_window_digest(self._h, _ptr(t), t.size, emit_from, abs_base, _ptr(counts), C.byref(m),
+                                     C.byref(s), C.byref(x), C.byref(f))
         acc.update(m=m.value, dsum=s.value, dxor=x.value, follows=f.value)
         return rc
 

@@ -109,36 +109,44 @@ std::uint64_t ref_scan(void* h, const std::uint8_t* text, std::uint64_t n, std::
 }
 
 // Windowed reference scan for golden statistics: the reference scan of
-// text[start, n) (from the root), keeping records with absolute end >=
-// emit_from. Accumulates per-pattern counts, the record count, the
-// order-independent digest (key = end*2^20 + id) and the failure follows of
-// the steps at positions >= emit_from. Also verifies (end, id) strict order.
-// Returns 0, or 5 if the window output was not strictly increasing.
-int ref_scan_window_stats(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t start,
-                          std::uint64_t emit_from, std::uint64_t* counts, std::uint64_t* m,
-                          std::uint64_t* dsum, std::uint64_t* dxor, std::uint64_t* follows) {
+// text[0, n) (from the root), keeping records with end >= emit_from. The
+// window starts at absolute offset abs_base of the whole text; digest keys use
+// absolute ends (key = (abs_base + end)*2^20 + id). Accumulates per-pattern
+// counts, the record count, the order-independent digest and the failure
+// follows of the steps at positions >= emit_from. Also verifies (end, id)
+// strict order. Returns 0, or 5 if the output was not strictly increasing.
+int ref_window_digest(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t emit_from,
+                      std::uint64_t abs_base, std::uint64_t* counts, std::uint64_t* m, std::uint64_t* dsum,
+                      std::uint64_t* dxor, std::uint64_t* follows) {
     const Automaton& a = *static_cast<Automaton*>(h);
     const char* base = reinterpret_cast<const char*>(text);
     acmatch::ScanStats all, pre;
-    const auto recs = acmatch::scan(a, std::string_view(base + start, n - start), all);
-    if (emit_from > start) (void)acmatch::scan(a, std::string_view(base + start, emit_from - start), pre);
+    const auto recs = acmatch::scan(a, std::string_view(base, n), all);
+    if (emit_from > 0) (void)acmatch::scan(a, std::string_view(base, emit_from), pre);
     *follows += all.failure_follows - pre.failure_follows;
     int rc = 0;
     bool first = true;
     MatchRecord prev{};
     for (const MatchRecord& r : recs) {
-        const std::uint64_t end = r.end + start;
-        if (end < emit_from) continue;
-        if (!first && !acmatch::match_before(prev, MatchRecord{r.pattern_id, end})) rc = 5;
-        prev = MatchRecord{r.pattern_id, end};
+        if (r.end < emit_from) continue;
+        if (!first && !acmatch::match_before(prev, r)) rc = 5;
+        prev = r;
         first = false;
         counts[r.pattern_id]++;
-        const std::uint64_t k = mix64((end << 20) + r.pattern_id);
+        const std::uint64_t k = mix64(((abs_base + r.end) << 20) + r.pattern_id);
         *dsum += k;
         *dxor ^= k;
         ++*m;
     }
     return rc;
+}
+
+// ref_window_digest over text[start, n) of a whole-text buffer.
+int ref_scan_window_stats(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t start,
+                          std::uint64_t emit_from, std::uint64_t* counts, std::uint64_t* m,
+                          std::uint64_t* dsum, std::uint64_t* dxor, std::uint64_t* follows) {
+    return ref_window_digest(h, text + start, n - start, emit_from > start ? emit_from - start : 0, start, counts, m,
+                             dsum, dxor, follows);
 }
 
 // acmatch::run_partitioned (include/acmatch/partition.hpp:108-170), as is.

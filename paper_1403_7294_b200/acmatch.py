@@ -175,6 +175,11 @@ class Automaton:
                 "alphabet": "dna4" if mode.value == 0 else "generic"}
 
 
+def version() -> str:
+    """Library version string (acg_version)."""
+    return _lib.acg().acg_version().decode()
+
+
 def build(patterns: Sequence[Pattern]) -> Automaton:
     """aho_corasick.hpp:130-233. Raises EmptyDictionaryError, EmptyPatternError,
     or Error when ids are not dense in load order (:135-136)."""
