@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -27,6 +28,21 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+// CUDA driver initialisation (cuInit, ~0.6 s on a B200 node) happens when the
+// library is loaded rather than inside the caller's first scan, so a drop-in
+// user's first acmatch::scan costs only context creation and kernel loading.
+// No context is created here (the device is not known yet). ACG_EAGER_INIT=0
+// turns it off (e.g. for a process that forks CUDA-using children).
+struct EagerDriverInit {
+    EagerDriverInit() {
+        const char* e = std::getenv("ACG_EAGER_INIT");
+        if (e && e[0] == '0') return;
+        int count = 0;
+        (void)cudaGetDeviceCount(&count);
+        (void)cudaGetLastError();
+    }
+} g_eager_driver_init;
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -92,6 +108,10 @@ struct acg_automaton {
     std::vector<std::uint64_t> profile;  // per NFA state visit counts on a sample (optional)
     mutable std::mutex mu;
     mutable std::map<int, std::shared_ptr<DeviceDfa>> dev;
+    // host DFA (dense table, hot tables, CSR outputs), compiled by acg_build for
+    // the sm_100 shared-memory budget; recompiled only if a layout knob changes
+    mutable std::shared_ptr<acg::Dfa> dfa;
+    mutable std::size_t dfa_budget = 0;
 };
 
 struct acg_result {
@@ -154,6 +174,21 @@ std::size_t hot_budget(int smem_optin) {
     return b > 0 ? static_cast<std::size_t>(b) : 0;
 }
 
+constexpr int kSm100SmemOptin = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOptin on B200 (227 KiB)
+
+// The automaton's host DFA for a device's shared-memory budget (a->mu held).
+std::shared_ptr<acg::Dfa> host_dfa_locked(const acg_automaton* a, int smem_optin) {
+    std::size_t budget = hot_budget(smem_optin);
+    if (a->hot_limit) budget = std::min<std::size_t>(budget, (a->hot_limit + 1ull) * 2ull * 256ull);
+    if (!a->dfa || a->dfa_budget != budget) {
+        auto dfa = std::make_shared<acg::Dfa>();
+        acg::compile_dfa(a->nfa, budget, a->profile.empty() ? nullptr : &a->profile, *dfa, a->hot_limit);
+        a->dfa = std::move(dfa);
+        a->dfa_budget = budget;
+    }
+    return a->dfa;
+}
+
 int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa>* out) {
     std::lock_guard<std::mutex> lock(a->mu);
     auto it = a->dev.find(device);
@@ -172,12 +207,8 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
     dd->device = device;
     ACG_CUDA(cudaDeviceGetAttribute(&dd->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     ACG_CUDA(cudaDeviceGetAttribute(&dd->num_sms, cudaDevAttrMultiProcessorCount, device));
-    auto dfa = std::make_shared<acg::Dfa>();
-    std::size_t budget = hot_budget(dd->smem_optin);
-    if (a->hot_limit) budget = std::min<std::size_t>(budget, (a->hot_limit + 1ull) * 2ull * 256ull);
-    acg::compile_dfa(a->nfa, budget, a->profile.empty() ? nullptr : &a->profile, *dfa, a->hot_limit);
-    dd->dfa = dfa;
-    const acg::Dfa& d = *dfa;
+    dd->dfa = host_dfa_locked(a, dd->smem_optin);
+    const acg::Dfa& d = *dd->dfa;
     ACG_CUDA(upload(dd->next, d.next.data(), d.next.size()));
     ACG_CUDA(upload(dd->out_off, d.out_off.data(), d.out_off.size()));
     ACG_CUDA(upload(dd->out_ids, d.out_ids.data(), d.out_ids.size()));
@@ -687,6 +718,8 @@ int acg_build(const std::uint8_t* concat, const std::uint64_t* offsets, std::uin
         }
         if (rc == acg::kErrEmptyDictionary) return fail(rc, "dictionary is empty");
         if (rc != acg::kOk) return fail(rc, "invalid dictionary");
+        std::lock_guard<std::mutex> lock(a->mu);
+        host_dfa_locked(a.get(), kSm100SmemOptin);
     } catch (const std::bad_alloc&) {
         return fail(ACG_ERR_OUT_OF_MEMORY, "host allocation failed while building the automaton");
     }
@@ -741,7 +774,9 @@ int acg_optimize_layout(acg_automaton* a, const std::uint8_t* sample, std::uint6
         s = nfa.next_state(s, sample[i]);
         ++visits[s];
     }
+    std::lock_guard<std::mutex> lock(a->mu);
     a->profile = std::move(visits);
+    a->dfa.reset();
     return ACG_OK;
 }
 
@@ -750,14 +785,20 @@ int acg_set_hot_limit(acg_automaton* a, std::uint32_t max_hot_rows) {
     std::lock_guard<std::mutex> lock(a->mu);
     if (!a->dev.empty()) return fail(ACG_ERR_INVALID, "layout is fixed once the automaton has been scanned");
     a->hot_limit = max_hot_rows;
+    a->dfa.reset();
     return ACG_OK;
 }
 
 int acg_automaton_layout(const acg_automaton* a, std::uint32_t* n_states, std::uint32_t* hot_rows,
                          std::uint32_t* columns, std::uint32_t* halo, int* alphabet_mode) {
-    std::shared_ptr<DeviceDfa> dd;
-    if (const int rc = get_device_dfa(a, current_device(), &dd)) return rc;
-    const acg::Dfa& d = *dd->dfa;
+    if (!a) return fail(ACG_ERR_INVALID, "null automaton");
+    std::shared_ptr<const acg::Dfa> dfa;
+    {
+        std::lock_guard<std::mutex> lock(a->mu);
+        if (a->dev.empty()) dfa = host_dfa_locked(a, kSm100SmemOptin);
+        else dfa = a->dev.begin()->second->dfa;
+    }
+    const acg::Dfa& d = *dfa;
     if (n_states) *n_states = d.S;
     if (hot_rows) *hot_rows = d.H;
     if (columns) *columns = d.K;

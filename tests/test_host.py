@@ -117,7 +117,6 @@ def test_host_build_matches_oracle_on_config_dictionaries(cfg):
             (o.failure(s), o.depth(s), o.outputs(s), o.transitions(s))
 
 
-@pytest.mark.gpu  # the DFA layout is sized to the device's shared memory
 def test_layout_reports_dfa_geometry():
     w = synth.CONFIGS[1].scaled(1 << 20, patterns=2000)
     concat, offs = synth.patterns(w)
