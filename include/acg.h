@@ -127,13 +127,17 @@ int acg_scanner_digest(acg_scanner* s, uint64_t* dsum, uint64_t* dxor, uint64_t*
 int acg_scanner_kernel_ms(acg_scanner* s, float* ms5);
 /* Scan mode. SPARSE walks the truncated hot automaton from shared memory and
  * replays the rare cold excursions exactly; EXACT walks the full DFA in
- * lockstep (hot rows in shared memory, cold rows from L2). AUTO picks SPARSE
- * when the automaton allows it and the previous run's excursion rate was low.
- * Both are bit-exact; ACG_SCAN_STATS always runs EXACT. */
-enum { ACG_MODE_AUTO = 0, ACG_MODE_SPARSE = 1, ACG_MODE_EXACT = 2 };
+ * lockstep (hot rows in shared memory, cold rows from L2); FILTER streams the
+ * text through a sampled q-gram Bloom prefilter and walks only the 64-byte
+ * blocks where a match can end (DNA dictionaries whose shortest pattern has
+ * >= 13 bytes and a selective filter). AUTO picks FILTER, else SPARSE, else
+ * EXACT from the automaton and the previous run's candidate / excursion
+ * rates. All are bit-exact; ACG_SCAN_STATS always runs EXACT. */
+enum { ACG_MODE_AUTO = 0, ACG_MODE_SPARSE = 1, ACG_MODE_EXACT = 2, ACG_MODE_FILTER = 3 };
 int acg_scanner_set_mode(acg_scanner* s, int mode);
-/* Mode of the last run (ACG_MODE_SPARSE / ACG_MODE_EXACT) and, when sparse,
- * its event rate (events per walked byte; -1 before the first sparse sync). */
+/* Mode of the last run (ACG_MODE_SPARSE / _EXACT / _FILTER) and its event
+ * rate: sparse, excursion events per walked byte; filter, passing samples per
+ * text byte (-1 before the first sync of that mode). */
 int acg_scanner_last_mode(acg_scanner* s, double* event_rate);
 /* Copies the P per-pattern counts (u64) into a caller device buffer, enqueued
  * on `stream` (NULL = the stream of the last run) — e.g. for an NCCL all-reduce. */

@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib
 
 SCAN_LIST, SCAN_COUNTS, SCAN_STATS, SCAN_PROFILE = 1, 2, 4, 8
-MODE_AUTO, MODE_SPARSE, MODE_EXACT = 0, 1, 2
+MODE_AUTO, MODE_SPARSE, MODE_EXACT, MODE_FILTER = 0, 1, 2, 3
 
 
 # ---- errors (include/acmatch/errors.hpp:9-48) ------------------------------
@@ -343,7 +343,7 @@ class Scanner:
     def last_mode(self) -> tuple[str, float]:
         rate = C.c_double()
         m = _lib.acg().acg_scanner_last_mode(self._h, C.byref(rate))
-        return {MODE_SPARSE: "sparse", MODE_EXACT: "exact"}.get(m, "none"), rate.value
+        return {MODE_SPARSE: "sparse", MODE_EXACT: "exact", MODE_FILTER: "filter"}.get(m, "none"), rate.value
 
     def copy_pattern_counts(self, d_dst_ptr: int, stream: int = 0) -> None:
         _check(_lib.acg().acg_scanner_copy_pattern_counts(self._h, C.c_void_p(d_dst_ptr), C.c_void_p(stream or None)))

@@ -24,6 +24,7 @@
 #include "../../include/acg.h"
 #include "automaton.hpp"
 #include "scan_kernels.cuh"
+#include "filter_kernels.cuh"
 
 namespace {
 
@@ -86,6 +87,7 @@ struct DeviceDfa {
     DevBuf<std::uint32_t> next, out_off, out_ids, depth;
     DevBuf<std::uint16_t> hot16, hotH, follows, follows_esc;
     DevBuf<std::uint8_t> symmap;
+    DevBuf<std::uint32_t> qbloom;  // filter mode: kQWords Bloom words
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
     std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
     int smem_optin = 0;
@@ -159,6 +161,8 @@ struct acg_scanner {
     int mode_req = 0;
     int mode_run = 0;
     double last_event_rate = -1.0;
+    double last_filter_rate = -1.0;  // filter mode: passing samples per text byte
+    DevBuf<std::uint32_t> dirty, block_count;  // filter mode
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
@@ -227,6 +231,7 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
         std::copy(d.hotH.begin(), d.hotH.end(), hh.begin());
         ACG_CUDA(upload(dd->hotH, hh.data(), hh.size()));
     }
+    if (d.filter_ok) ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size()));
     a->dev[device] = dd;
     *out = dd;
     return ACG_OK;
@@ -344,6 +349,10 @@ cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid
 std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
+// Filter mode: batch depth of KQ and the hot rows the block walks stage (48 KiB).
+constexpr int kQBatch = 4;
+std::uint32_t qwalk_hot_rows(const acg::Dfa& d) { return std::min<std::uint32_t>(d.H, 6144u); }
+
 // Enqueue K3 (compaction + ordered write) for the current geometry.
 int enqueue_write(acg_scanner* s, cudaStream_t st) {
     using namespace acg::kern;
@@ -362,7 +371,15 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     wa.records = want_list ? s->records.p : nullptr;
     wa.rec_cap = want_list ? s->records.n : 0;
     wa.visits = nullptr;  // both modes count visits in their count pass
-    if (s->mode_run == ACG_MODE_SPARSE) {
+    if (s->mode_run == ACG_MODE_FILTER) {
+        auto k = acg::kern::qverify_write_kernel;
+        const std::size_t smem = static_cast<std::size_t>(wa.hot_rows) * 8;
+        ACG_CUDA(prepare_smem(k, smem));
+        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
+            1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 4ull * dd.num_sms)));
+        k<<<g, 256, smem, st>>>(wa);
+        ACG_CUDA(cudaGetLastError());
+    } else if (s->mode_run == ACG_MODE_SPARSE) {
         wa.visits = nullptr;  // counted with the candidates in the count pass
         auto k = acg::kern::sparse_emit_kernel;
         ACG_CUDA(prepare_smem(k, smem_sparse(dd)));
@@ -383,6 +400,12 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     const DeviceDfa& dd = *s->dd;
     const unsigned long long streams = static_cast<unsigned long long>(dd.num_sms) * s->tpb_run * s->U_run;
     const unsigned long long halo = dd.dfa->halo;
+    if (s->mode_run == ACG_MODE_FILTER) {  // fixed 8 KiB chunks of 128 dirty-bit blocks
+        s->chunk = static_cast<unsigned long long>(acg::kQChunkBlocks) * acg::kQBlock;
+        s->n_chunks = (owned + s->chunk - 1) / s->chunk;
+        s->grid = static_cast<unsigned>(dd.num_sms);
+        return;
+    }
     unsigned long long chunk = s->chunk_override;
     if (!chunk) {
         chunk = (owned + streams - 1) / streams;
@@ -424,7 +447,10 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     // mode: sparse (truncated automaton + fix-up) when the automaton allows it
     // and excursions were rare on the previous run; exact otherwise
     int mode = s->mode_req;
-    if (stats || !d.sparse_ok) mode = ACG_MODE_EXACT;
+    if (mode == ACG_MODE_FILTER && !d.filter_ok) mode = ACG_MODE_AUTO;
+    if (mode == ACG_MODE_AUTO && d.filter_ok && (s->last_filter_rate < 0 || s->last_filter_rate < 1.0 / 256))
+        mode = ACG_MODE_FILTER;
+    if (stats || (mode != ACG_MODE_FILTER && !d.sparse_ok)) mode = ACG_MODE_EXACT;
     if (mode == ACG_MODE_AUTO)
         mode = (s->last_event_rate < 0 || s->last_event_rate < 0.08) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
     s->mode_run = mode;
@@ -494,7 +520,39 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
 
     // K1: count pass
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
-    if (mode == ACG_MODE_SPARSE) {
+    if (mode == ACG_MODE_FILTER) {
+        const unsigned long long n_dwords = s->n_chunks * (acg::kQChunkBlocks / 32);
+        ACG_CUDA(s->dirty.reserve(n_dwords));
+        ACG_CUDA(s->block_count.reserve(s->n_chunks * acg::kQChunkBlocks));
+        ACG_CUDA(cudaMemsetAsync(s->dirty.p, 0, n_dwords * sizeof(std::uint32_t), st));
+        ACG_CUDA(cudaMemsetAsync(s->chunk_counts.p, 0, s->n_chunks * sizeof(unsigned long long), st));
+        a.qbloom = dd.qbloom.p;
+        a.q = d.q;
+        a.max_len = d.max_len;
+        a.dirty = s->dirty.p;
+        a.block_count = s->block_count.p;
+        a.hot_rows = qwalk_hot_rows(d);
+        a.ev_total = s->scalars64.p + 4;
+        {
+            auto k = qfilter_kernel<kQBatch>;
+            const std::size_t smem = acg::kQWords * sizeof(std::uint32_t);
+            ACG_CUDA(prepare_smem(k, smem));
+            k<<<dd.num_sms, 512, smem, st>>>(a);
+            ACG_CUDA(cudaGetLastError());
+            ++s->launches;
+        }
+        if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+        {
+            auto k = qverify_count_kernel;
+            const std::size_t smem = static_cast<std::size_t>(a.hot_rows) * 8;
+            ACG_CUDA(prepare_smem(k, smem));
+            const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
+                1, std::min<unsigned long long>((n_dwords + 255) / 256, 4ull * dd.num_sms)));
+            k<<<g, 256, smem, st>>>(a, static_cast<long long>(n_dwords));
+            ACG_CUDA(cudaGetLastError());
+            ++s->launches;
+        }
+    } else if (mode == ACG_MODE_SPARSE) {
         // per K1s warp: one 16-byte event per flagged (block, stream) -> no overflow
         const unsigned long long walk = s->chunk + d.halo;
         const unsigned long long per_warp = 32ull * s->U_run;
@@ -590,6 +648,8 @@ int scanner_sync(acg_scanner* s) {
         }
     }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
+    if (s->mode_run == ACG_MODE_FILTER && s->run_n)
+        s->last_filter_rate = static_cast<double>(s->pinned[5]) / static_cast<double>(s->run_n);
     if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
         const double walked = static_cast<double>(s->n_chunks) * static_cast<double>(s->chunk + s->dd->dfa->halo);
         s->last_event_rate = static_cast<double>(s->pinned[5]) / walked;
@@ -939,14 +999,14 @@ int acg_scanner_kernel_ms(acg_scanner* s, float* ms5) {
 
 int acg_scanner_set_mode(acg_scanner* s, int mode) {
     if (!s) return fail(ACG_ERR_INVALID, "null scanner");
-    if (mode < ACG_MODE_AUTO || mode > ACG_MODE_EXACT) return fail(ACG_ERR_INVALID, "unknown mode");
+    if (mode < ACG_MODE_AUTO || mode > ACG_MODE_FILTER) return fail(ACG_ERR_INVALID, "unknown mode");
     s->mode_req = mode;
     return ACG_OK;
 }
 
 int acg_scanner_last_mode(acg_scanner* s, double* event_rate) {
     if (!s) return -1;
-    if (event_rate) *event_rate = s->last_event_rate;
+    if (event_rate) *event_rate = s->mode_run == ACG_MODE_FILTER ? s->last_filter_rate : s->last_event_rate;
     return s->mode_run;
 }
 

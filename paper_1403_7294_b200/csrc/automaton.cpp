@@ -1,5 +1,6 @@
 // Host automaton build (reference algorithm) and dense-DFA compilation.
 #include "automaton.hpp"
+#include "qfilter.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -213,8 +214,50 @@ int build_nfa(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32
     for (std::uint32_t j = nfa.edge_off[0]; j < nfa.edge_off[1]; ++j) nfa.root_row[nfa.edge_byte[j]] = nfa.edge_to[j];
     nfa.n_patterns = count;
     nfa.max_len = max_len;
+    nfa.min_len = ~0u;
+    for (std::uint32_t i = 0; i < count; ++i)
+        nfa.min_len = std::min<std::uint32_t>(nfa.min_len, static_cast<std::uint32_t>(offs[i + 1] - offs[i]));
+    nfa.pat_bytes.assign(concat, concat + offs[count]);
+    nfa.pat_off.assign(offs, offs + count + 1);
+    for (auto& o : nfa.pat_off) o -= offs[0];
     return kOk;
 }
+
+namespace {
+
+// The q-gram prefilter (qfilter.hpp): every pattern's q-grams at offsets
+// 0..kQSample-1 into the three Bloom stages.
+void compile_qfilter(const Nfa& nfa, Dfa& d) {
+    d.filter_ok = false;
+    d.qbloom.clear();
+    if (d.mode != kAlphaDna4 || nfa.min_len < kQMinQ + kQSample - 1) return;
+    const std::uint32_t q = std::min(kQMaxQ, nfa.min_len - (kQSample - 1));
+    d.q = q;
+    d.qbloom.assign(kQWords, 0u);
+    auto set = [&](std::uint32_t word_off, std::uint32_t h) { d.qbloom[word_off + (h >> 5)] |= 1u << (h & 31); };
+    for (std::uint32_t p = 0; p < nfa.n_patterns; ++p) {
+        const std::uint8_t* b = nfa.pat_bytes.data() + nfa.pat_off[p];
+        for (std::uint32_t o = 0; o < kQSample; ++o) {
+            std::uint32_t c = 0;
+            for (std::uint32_t k = 0; k < q; ++k) c |= ((static_cast<std::uint32_t>(b[o + k]) >> 1) & 3u) << (2 * k);
+            set(0, qhash0(c));
+            set(kQOff1, qhash1(c));
+            set(kQOff2, qhash2(c));
+        }
+    }
+    auto fill = [&](std::uint32_t lo, std::uint32_t hi) {
+        std::uint64_t ones = 0;
+        for (std::uint32_t i = lo; i < hi; ++i) ones += static_cast<std::uint64_t>(__builtin_popcount(d.qbloom[i]));
+        return static_cast<double>(ones) / (32.0 * (hi - lo));
+    };
+    d.filter_fp = fill(0, kQOff1) * fill(kQOff1, kQOff2) * fill(kQOff2, kQWords);
+    // worth it when a random sample passes rarely (dirty blocks are walked ~2x)
+    d.filter_ok = d.filter_fp <= 1e-3;
+    if (!d.filter_ok) d.qbloom.clear();
+}
+
+}  // namespace
+
 
 void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& d,
                  std::uint32_t hot_limit) {
@@ -360,6 +403,8 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
     d.id_bits = 1;
     while ((1ull << d.id_bits) < nfa.n_patterns) ++d.id_bits;
     d.halo = (nfa.max_len + 15u) & ~15u;
+    d.max_len = nfa.max_len;
+    compile_qfilter(nfa, d);
 }
 
 }  // namespace acg

@@ -32,6 +32,9 @@ struct Nfa {
     StateId root_row[256];               // :115-117
     std::uint32_t n_patterns = 0;
     std::uint32_t max_len = 0;
+    std::uint32_t min_len = 0;
+    std::vector<std::uint8_t> pat_bytes;  // the dictionary as given (q-gram prefilter build)
+    std::vector<std::uint64_t> pat_off;   // n_patterns + 1
 
     std::uint32_t state_count() const { return static_cast<std::uint32_t>(fail.size()); }
     bool goto_transition(StateId s, std::uint8_t b, StateId* out) const;
@@ -83,6 +86,13 @@ struct Dfa {
     std::vector<std::uint16_t> follows_esc;  // per state, for bytes outside the pattern alphabet (dna4 mode)
     std::uint32_t id_bits = 1;           // bits for a pattern id in a packed record
     std::uint32_t halo = 0;              // round_up(max_len, 16): warm-up bytes before each chunk
+    std::uint32_t max_len = 0;
+    // Sampled q-gram prefilter (filter mode; qfilter.hpp): dna4 dictionaries
+    // whose shortest pattern has at least kQMinQ + kQSample - 1 bytes.
+    bool filter_ok = false;
+    std::uint32_t q = 0;
+    std::vector<std::uint32_t> qbloom;   // kQWords words: the three Bloom stages
+    double filter_fp = 1.0;              // fraction of random q-grams passing all stages
 };
 
 // Fold the NFA into the dense DFA image. `hot_budget_bytes` bounds the u16 hot

@@ -95,6 +95,13 @@ struct ScanArgs {
     std::uint32_t task_cap;
     std::uint32_t* cand_n;                  // per chunk: exported count, 0xFFFFFFFF = re-walk
     unsigned long long* ev_total;           // sum of events (mode heuristic)
+    // filter mode (filter_kernels.cuh)
+    const std::uint32_t* qbloom;            // kQWords Bloom words
+    std::uint32_t q;                        // q-gram length
+    std::uint32_t max_len;                  // longest pattern
+    std::uint32_t* dirty;                   // 1 bit per 64-byte block of [emit_from, n), n_chunks*4 words
+    std::uint32_t* block_count;             // per dirty block: matches ending in it (count pass)
+    std::uint32_t hot_rows;                 // rows of hot16 staged in shared memory by the block walks
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {
