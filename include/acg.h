@@ -144,6 +144,10 @@ int acg_scanner_last_mode(acg_scanner* s, double* event_rate);
 int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream);
 /* Geometry of the last run: chunks, chunk bytes, and launches issued. */
 int acg_scanner_last_geometry(acg_scanner* s, uint64_t* n_chunks, uint64_t* chunk_bytes, uint32_t* launches);
+/* Filter-mode eligibility (diagnostics): returns 1 when the sampled q-gram
+ * prefilter applies, with its q-gram length and the fraction of random
+ * q-grams that pass all Bloom stages; 0 otherwise. */
+int acg_automaton_filter_info(const acg_automaton* a, uint32_t* q, double* pass_rate);
 /* Device layout of the automaton (diagnostics): states, hot rows in smem, columns. */
 int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* hot_rows, uint32_t* columns,
                          uint32_t* halo, int* alphabet_mode);

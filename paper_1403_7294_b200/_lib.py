@@ -61,6 +61,7 @@ ACG_SYMBOLS = {
     "acg_scanner_set_mode": (C.c_int, [vp, C.c_int]),
     "acg_scanner_last_mode": (C.c_int, [vp, C.POINTER(C.c_double)]),
     "acg_automaton_layout": (C.c_int, [vp, u32p, u32p, u32p, u32p, C.POINTER(C.c_int)]),
+    "acg_automaton_filter_info": (C.c_int, [vp, u32p, C.POINTER(C.c_double)]),
     "acg_scanner_set_geometry": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint64]),
 }
 

@@ -167,6 +167,12 @@ class Automaton:
         """Diagnostics: cap the shared-memory-resident rows (exercises cold paths)."""
         _check(_lib.acg().acg_set_hot_limit(self._h, max_hot_rows))
 
+    def filter_info(self) -> dict:
+        """Filter-mode eligibility: q-gram length and Bloom pass rate."""
+        q, fp = C.c_uint32(), C.c_double()
+        ok = _lib.acg().acg_automaton_filter_info(self._h, C.byref(q), C.byref(fp))
+        return {"eligible": bool(ok), "q": q.value, "pass_rate": fp.value}
+
     def layout(self) -> dict:
         v = [C.c_uint32() for _ in range(4)]
         mode = C.c_int()

@@ -88,6 +88,8 @@ struct DeviceDfa {
     DevBuf<std::uint16_t> hot16, hotH, follows, follows_esc;
     DevBuf<std::uint8_t> symmap;
     DevBuf<std::uint32_t> qbloom;  // filter mode: kQWords Bloom words
+    DevBuf<std::uint32_t> qtab, qb_off, qb_ent, pat_off;  // filter mode: exact q-gram table, patterns
+    DevBuf<std::uint8_t> pat_bytes;
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
     std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
     int smem_optin = 0;
@@ -162,7 +164,11 @@ struct acg_scanner {
     int mode_run = 0;
     double last_event_rate = -1.0;
     double last_filter_rate = -1.0;  // filter mode: passing samples per text byte
-    DevBuf<std::uint32_t> dirty, block_count;  // filter mode
+    // filter mode: KQ survivors (count in scalars32[3]), V0 record scratch
+    // (count in scalars64[5]), per-chunk fill counters, heavy chunks (count in scalars32[2])
+    DevBuf<unsigned long long> qcands, qscratch;
+    DevBuf<std::uint32_t> qfill, qheavy;
+    bool regrow = false;  // enqueue_write after a record-buffer regrowth
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
@@ -231,7 +237,14 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
         std::copy(d.hotH.begin(), d.hotH.end(), hh.begin());
         ACG_CUDA(upload(dd->hotH, hh.data(), hh.size()));
     }
-    if (d.filter_ok) ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size()));
+    if (d.filter_ok) {
+        ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size()));
+        ACG_CUDA(upload(dd->qtab, d.qtab.data(), d.qtab.size()));
+        ACG_CUDA(upload(dd->qb_off, d.qb_off.data(), d.qb_off.size()));
+        ACG_CUDA(upload(dd->qb_ent, d.qb_ent.data(), d.qb_ent.size()));
+        ACG_CUDA(upload(dd->pat_off, d.pat_off32.data(), d.pat_off32.size()));
+        ACG_CUDA(upload(dd->pat_bytes, a->nfa.pat_bytes.data(), a->nfa.pat_bytes.size()));
+    }
     a->dev[device] = dd;
     *out = dd;
     return ACG_OK;
@@ -349,9 +362,15 @@ cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid
 std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
-// Filter mode: batch depth of KQ and the hot rows the block walks stage (48 KiB).
-constexpr int kQBatch = 4;
-std::uint32_t qwalk_hot_rows(const acg::Dfa& d) { return std::min<std::uint32_t>(d.H, 6144u); }
+// Filter mode: batch depth and block size of KQ.
+#ifndef ACG_QBATCH
+#define ACG_QBATCH 2
+#endif
+#ifndef ACG_QTHREADS
+#define ACG_QTHREADS 512
+#endif
+constexpr int kQBatch = ACG_QBATCH;
+constexpr int kQThreads = ACG_QTHREADS;
 
 // Enqueue K3 (compaction + ordered write) for the current geometry.
 int enqueue_write(acg_scanner* s, cudaStream_t st) {
@@ -372,12 +391,24 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     wa.rec_cap = want_list ? s->records.n : 0;
     wa.visits = nullptr;  // both modes count visits in their count pass
     if (s->mode_run == ACG_MODE_FILTER) {
-        auto k = acg::kern::qverify_write_kernel;
-        const std::size_t smem = static_cast<std::size_t>(wa.hot_rows) * 8;
-        ACG_CUDA(prepare_smem(k, smem));
-        const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
-            1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 4ull * dd.num_sms)));
-        k<<<g, 256, smem, st>>>(wa);
+        // records into their chunk's slots: from the scratch list, or (record
+        // buffer regrown) by confirming the survivors again
+        ACG_CUDA(cudaMemsetAsync(s->qfill.p, 0, s->n_chunks * sizeof(std::uint32_t), st));
+        if (s->regrow) {
+            acg::kern::qconfirm_kernel<kWrite><<<8 * dd.num_sms, 256, 0, st>>>(wa);
+        } else {
+            acg::kern::qscatter_kernel<<<4 * dd.num_sms, 256, 0, st>>>(wa);
+        }
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+        ACG_CUDA(s->qheavy.reserve(s->n_chunks));
+        ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 2, 0, sizeof(std::uint32_t), st));
+        acg::kern::qsort_chunks_kernel<<<4 * dd.num_sms, 256, 0, st>>>(wa, s->qheavy.p, s->scalars32.p + 2);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+        auto k = acg::kern::qheavy_kernel;
+        ACG_CUDA(prepare_smem(k, dd.hotH_bytes));
+        k<<<dd.num_sms, 256, dd.hotH_bytes, st>>>(wa, s->qheavy.p, s->scalars32.p + 2);
         ACG_CUDA(cudaGetLastError());
     } else if (s->mode_run == ACG_MODE_SPARSE) {
         wa.visits = nullptr;  // counted with the candidates in the count pass
@@ -447,8 +478,9 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     // mode: sparse (truncated automaton + fix-up) when the automaton allows it
     // and excursions were rare on the previous run; exact otherwise
     int mode = s->mode_req;
-    if (mode == ACG_MODE_FILTER && !d.filter_ok) mode = ACG_MODE_AUTO;
-    if (mode == ACG_MODE_AUTO && d.filter_ok && (s->last_filter_rate < 0 || s->last_filter_rate < 1.0 / 256))
+    const bool filter_ok = d.filter_ok && d.sparse_ok;  // heavy chunks replay with A_H
+    if (mode == ACG_MODE_FILTER && !filter_ok) mode = ACG_MODE_AUTO;
+    if (mode == ACG_MODE_AUTO && filter_ok && (s->last_filter_rate < 0 || s->last_filter_rate < 1.0 / 256))
         mode = ACG_MODE_FILTER;
     if (stats || (mode != ACG_MODE_FILTER && !d.sparse_ok)) mode = ACG_MODE_EXACT;
     if (mode == ACG_MODE_AUTO)
@@ -506,7 +538,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     a.H = d.H;
     a.Hn = d.Hn;
     a.Cn = d.Cn;
-    a.smem_table_bytes = mode == ACG_MODE_SPARSE ? dd.hotH_bytes : dd.hot_bytes;
+    a.smem_table_bytes = (mode == ACG_MODE_SPARSE || (mode == ACG_MODE_FILTER && d.sparse_ok)) ? dd.hotH_bytes : dd.hot_bytes;
     a.hotH = dd.hotH.p;
     a.chunk_counts = s->chunk_counts.p;
     a.active_list = s->active_list.p;
@@ -521,37 +553,48 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     // K1: count pass
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
     if (mode == ACG_MODE_FILTER) {
-        const unsigned long long n_dwords = s->n_chunks * (acg::kQChunkBlocks / 32);
-        ACG_CUDA(s->dirty.reserve(n_dwords));
-        ACG_CUDA(s->block_count.reserve(s->n_chunks * acg::kQChunkBlocks));
-        ACG_CUDA(cudaMemsetAsync(s->dirty.p, 0, n_dwords * sizeof(std::uint32_t), st));
         ACG_CUDA(cudaMemsetAsync(s->chunk_counts.p, 0, s->n_chunks * sizeof(unsigned long long), st));
+        ACG_CUDA(s->qfill.reserve(s->n_chunks));
         a.qbloom = dd.qbloom.p;
+        a.qtab = dd.qtab.p;
+        a.qtab_bits = d.qtab_bits;
+        a.qb_off = dd.qb_off.p;
+        a.qb_ent = dd.qb_ent.p;
+        a.pat_bytes = dd.pat_bytes.p;
+        a.pat_off = dd.pat_off.p;
         a.q = d.q;
         a.max_len = d.max_len;
-        a.dirty = s->dirty.p;
-        a.block_count = s->block_count.p;
-        a.hot_rows = qwalk_hot_rows(d);
-        a.ev_total = s->scalars64.p + 4;
+        a.pcounts = want_counts ? s->counts.p : nullptr;
+        a.qfill = s->qfill.p;
+        if (want_list) {
+            ACG_CUDA(s->qscratch.reserve(s->records.n));
+            a.qscratch = s->qscratch.p;
+            a.qscratch_n = s->scalars64.p + 5;
+            ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 5, 0, sizeof(unsigned long long), st));
+        }
+        // survivors: sized from the previous run's rate (x4 headroom), at least one per 4 KiB;
+        // a full list is detected at sync and the scan re-run with a larger one
+        const double rate = s->last_filter_rate > 0 ? s->last_filter_rate : 1.0 / 4096;
+        unsigned long long cap = std::max<unsigned long long>(
+            1ull << 16, static_cast<unsigned long long>(4.0 * rate * static_cast<double>(n)) + n / 4096);
+        cap = std::min<unsigned long long>(0xFFFFFFFFull, std::max(cap, s->min_task_cap));
+        ACG_CUDA(s->qcands.reserve(cap));
+        a.qcands = s->qcands.p;
+        a.qcand_cap = static_cast<std::uint32_t>(std::min<unsigned long long>(cap, s->qcands.n));
+        a.qcand_n = s->scalars32.p + 3;
+        ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 3, 0, sizeof(std::uint32_t), st));
         {
-            auto k = qfilter_kernel<kQBatch>;
+            auto k = qfilter_kernel<kQBatch, kQThreads>;
             const std::size_t smem = acg::kQWords * sizeof(std::uint32_t);
             ACG_CUDA(prepare_smem(k, smem));
-            k<<<dd.num_sms, 512, smem, st>>>(a);
+            k<<<dd.num_sms, kQThreads, smem, st>>>(a);
             ACG_CUDA(cudaGetLastError());
             ++s->launches;
         }
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
-        {
-            auto k = qverify_count_kernel;
-            const std::size_t smem = static_cast<std::size_t>(a.hot_rows) * 8;
-            ACG_CUDA(prepare_smem(k, smem));
-            const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
-                1, std::min<unsigned long long>((n_dwords + 255) / 256, 4ull * dd.num_sms)));
-            k<<<g, 256, smem, st>>>(a, static_cast<long long>(n_dwords));
-            ACG_CUDA(cudaGetLastError());
-            ++s->launches;
-        }
+        qconfirm_kernel<kCount><<<8 * dd.num_sms, 256, 0, st>>>(a);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
     } else if (mode == ACG_MODE_SPARSE) {
         // per K1s warp: one 16-byte event per flagged (block, stream) -> no overflow
         const unsigned long long walk = s->chunk + d.halo;
@@ -611,7 +654,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     }
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[4], st));
     // K4: per-pattern counts
-    if (want_counts && n_out_states) {
+    if (want_counts && n_out_states && mode != ACG_MODE_FILTER) {
         const unsigned tb = 256;
         const unsigned g = std::min<unsigned>((n_out_states + tb - 1) / tb, 8 * dd.num_sms);
         pattern_counts_kernel<<<g, tb, 0, st>>>(s->visits.p, dd.out_off.p, dd.out_ids.p, d.Hn, d.H, d.Cn, d.S,
@@ -633,7 +676,7 @@ int scanner_sync(acg_scanner* s) {
                              cudaMemcpyDeviceToHost, st));
     ACG_CUDA(cudaMemcpyAsync(s->pinned + 5, s->scalars64.p + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              st));
-    ACG_CUDA(cudaMemcpyAsync(s->pinned + 6, s->scalars32.p, 2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    ACG_CUDA(cudaMemcpyAsync(s->pinned + 6, s->scalars32.p, 4 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
     ACG_CUDA(cudaStreamSynchronize(st));
     if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
         const std::uint32_t ntask = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[1];
@@ -647,9 +690,22 @@ int scanner_sync(acg_scanner* s) {
             return scanner_sync(s);
         }
     }
+    if (s->mode_run == ACG_MODE_FILTER && s->n_chunks) {
+        const std::uint32_t ncand = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[3];
+        if (ncand > s->args.qcand_cap) {  // the survivor list overflowed: grow and run again
+            s->min_task_cap = static_cast<unsigned long long>(ncand) + ncand / 4 + 4096;
+            const int req = s->mode_req;
+            s->mode_req = ACG_MODE_FILTER;
+            const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
+            s->mode_req = req;
+            if (rc) return rc;
+            return scanner_sync(s);
+        }
+    }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
     if (s->mode_run == ACG_MODE_FILTER && s->run_n)
-        s->last_filter_rate = static_cast<double>(s->pinned[5]) / static_cast<double>(s->run_n);
+        s->last_filter_rate = static_cast<double>(reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[3]) /
+                              static_cast<double>(s->run_n);
     if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
         const double walked = static_cast<double>(s->n_chunks) * static_cast<double>(s->chunk + s->dd->dfa->halo);
         s->last_event_rate = static_cast<double>(s->pinned[5]) / walked;
@@ -657,7 +713,9 @@ int scanner_sync(acg_scanner* s) {
     if ((s->flags & ACG_SCAN_LIST) && s->m_total > s->records.n) {
         // record buffer overflowed: grow and re-emit (chunk counts and offsets are final)
         ACG_CUDA(s->records.reserve(s->m_total + s->m_total / 4));
+        s->regrow = true;
         const int rc = enqueue_write(s, st);
+        s->regrow = false;
         if (rc) return rc;
         ACG_CUDA(cudaStreamSynchronize(st));
     }
@@ -847,6 +905,19 @@ int acg_set_hot_limit(acg_automaton* a, std::uint32_t max_hot_rows) {
     a->hot_limit = max_hot_rows;
     a->dfa.reset();
     return ACG_OK;
+}
+
+int acg_automaton_filter_info(const acg_automaton* a, std::uint32_t* q, double* pass_rate) {
+    if (!a) return 0;
+    std::shared_ptr<const acg::Dfa> dfa;
+    {
+        std::lock_guard<std::mutex> lock(a->mu);
+        if (a->dev.empty()) dfa = host_dfa_locked(a, kSm100SmemOptin);
+        else dfa = a->dev.begin()->second->dfa;
+    }
+    if (q) *q = dfa->q;
+    if (pass_rate) *pass_rate = dfa->filter_fp;
+    return dfa->filter_ok ? 1 : 0;
 }
 
 int acg_automaton_layout(const acg_automaton* a, std::uint32_t* n_states, std::uint32_t* hot_rows,

@@ -226,34 +226,75 @@ int build_nfa(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32
 namespace {
 
 // The q-gram prefilter (qfilter.hpp): every pattern's q-grams at offsets
-// 0..kQSample-1 into the three Bloom stages.
+// 0..kQSample-1 into the blocked Bloom filter and the exact (code -> (pattern,
+// offset) list) hash table.
 void compile_qfilter(const Nfa& nfa, Dfa& d) {
     d.filter_ok = false;
     d.qbloom.clear();
+    d.qtab.clear();
+    d.qb_off.clear();
+    d.qb_ent.clear();
     if (d.mode != kAlphaDna4 || nfa.min_len < kQMinQ + kQSample - 1) return;
+    if (nfa.pat_bytes.size() >= (1ull << 32) || nfa.n_patterns >= (1u << 30)) return;
     const std::uint32_t q = std::min(kQMaxQ, nfa.min_len - (kQSample - 1));
+    const std::uint32_t qm = q >= 16 ? 0xFFFFFFFFu : (1u << (2 * q)) - 1u;
     d.q = q;
-    d.qbloom.assign(kQWords, 0u);
-    auto set = [&](std::uint32_t word_off, std::uint32_t h) { d.qbloom[word_off + (h >> 5)] |= 1u << (h & 31); };
+    // (code, pattern << 2 | offset), grouped by code
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> grams;
+    grams.reserve(static_cast<std::size_t>(nfa.n_patterns) * kQSample);
     for (std::uint32_t p = 0; p < nfa.n_patterns; ++p) {
         const std::uint8_t* b = nfa.pat_bytes.data() + nfa.pat_off[p];
         for (std::uint32_t o = 0; o < kQSample; ++o) {
             std::uint32_t c = 0;
             for (std::uint32_t k = 0; k < q; ++k) c |= ((static_cast<std::uint32_t>(b[o + k]) >> 1) & 3u) << (2 * k);
-            set(0, qhash0(c));
-            set(kQOff1, qhash1(c));
-            set(kQOff2, qhash2(c));
+            grams.emplace_back(c, (p << 2) | o);
         }
     }
-    auto fill = [&](std::uint32_t lo, std::uint32_t hi) {
-        std::uint64_t ones = 0;
-        for (std::uint32_t i = lo; i < hi; ++i) ones += static_cast<std::uint64_t>(__builtin_popcount(d.qbloom[i]));
-        return static_cast<double>(ones) / (32.0 * (hi - lo));
-    };
-    d.filter_fp = fill(0, kQOff1) * fill(kQOff1, kQOff2) * fill(kQOff2, kQWords);
-    // worth it when a random sample passes rarely (dirty blocks are walked ~2x)
-    d.filter_ok = d.filter_fp <= 1e-3;
-    if (!d.filter_ok) d.qbloom.clear();
+    std::sort(grams.begin(), grams.end());
+    d.qbloom.assign(kQWords, 0u);
+    std::uint32_t keys = 0;
+    for (std::size_t i = 0; i < grams.size(); ++i) {
+        if (i && grams[i].first == grams[i - 1].first) continue;
+        ++keys;
+        d.qbloom[qword(grams[i].first)] |= qmask(grams[i].first);
+    }
+    d.qtab_bits = 10;
+    while ((1u << d.qtab_bits) < 2u * keys) ++d.qtab_bits;
+    d.qtab.assign(2ull << d.qtab_bits, kQEmpty);
+    d.qb_off.reserve(keys + 1);
+    d.qb_ent.reserve(grams.size());
+    for (std::size_t i = 0; i < grams.size();) {
+        const std::uint32_t c = grams[i].first;
+        std::uint32_t slot = qslot(c, d.qtab_bits);
+        while (d.qtab[2 * slot + 1] != kQEmpty) slot = (slot + 1) & ((1u << d.qtab_bits) - 1);
+        d.qtab[2 * slot] = c;
+        d.qtab[2 * slot + 1] = static_cast<std::uint32_t>(d.qb_off.size());
+        d.qb_off.push_back(static_cast<std::uint32_t>(d.qb_ent.size()));
+        for (; i < grams.size() && grams[i].first == c; ++i) d.qb_ent.push_back(grams[i].second);
+    }
+    d.qb_off.push_back(static_cast<std::uint32_t>(d.qb_ent.size()));
+    d.pat_off32.assign(nfa.pat_off.begin(), nfa.pat_off.end());
+    // pass rate of random q-grams (splitmix64 sample)
+    std::uint64_t z = 0x14037294ull, pass = 0;
+    const std::uint32_t trials = 1u << 20;
+    for (std::uint32_t t = 0; t < trials; ++t) {
+        z += 0x9E3779B97F4A7C15ull;
+        std::uint64_t r = z;
+        r = (r ^ (r >> 30)) * 0xBF58476D1CE4E5B9ull;
+        r = (r ^ (r >> 27)) * 0x94D049BB133111EBull;
+        const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
+        const std::uint32_t m = qmask(c);
+        pass += (d.qbloom[qword(c)] & m) == m;
+    }
+    d.filter_fp = static_cast<double>(pass) / trials;
+    // worth it when few samples survive (each survivor costs an exact probe)
+    d.filter_ok = d.filter_fp <= 5e-3;
+    if (!d.filter_ok) {
+        d.qbloom.clear();
+        d.qtab.clear();
+        d.qb_off.clear();
+        d.qb_ent.clear();
+    }
 }
 
 }  // namespace

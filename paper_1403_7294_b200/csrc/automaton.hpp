@@ -91,8 +91,13 @@ struct Dfa {
     // whose shortest pattern has at least kQMinQ + kQSample - 1 bytes.
     bool filter_ok = false;
     std::uint32_t q = 0;
-    std::vector<std::uint32_t> qbloom;   // kQWords words: the three Bloom stages
-    double filter_fp = 1.0;              // fraction of random q-grams passing all stages
+    std::vector<std::uint32_t> qbloom;   // kQWords: blocked Bloom filter of the (pattern, offset) q-grams
+    std::uint32_t qtab_bits = 0;         // exact table: 2^qtab_bits slots of (code, bucket start | kQEmpty)
+    std::vector<std::uint32_t> qtab;     // 2 * 2^qtab_bits
+    std::vector<std::uint32_t> qb_off;   // bucket offsets (keys + 1)
+    std::vector<std::uint32_t> qb_ent;   // entries: pattern id << 2 | offset
+    std::vector<std::uint32_t> pat_off32;  // pattern byte offsets (n_patterns + 1) into Nfa::pat_bytes
+    double filter_fp = 1.0;              // fraction of random q-grams passing the Bloom filter
 };
 
 // Fold the NFA into the dense DFA image. `hot_budget_bytes` bounds the u16 hot

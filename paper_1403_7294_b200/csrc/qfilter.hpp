@@ -4,12 +4,21 @@
 // Idea. Every occurrence [i, e] of a pattern of length L >= q + kQSample - 1
 // contains, at the first sample position j >= i (samples = buffer offsets
 // that are multiples of kQSample), the q-gram text[j, j+q) = P[j-i, j-i+q)
-// with j - i in [0, kQSample). The filter stores the q-grams of every pattern
-// at offsets 0..kQSample-1 in a three-stage Bloom filter (no false
-// negatives). A sample whose q-gram passes marks the 64-byte blocks holding
-// every end it could own ([j+q-1, j+maxlen-1]) as dirty, and only dirty
-// blocks are walked with the exact automaton. Every match is therefore found,
-// and reported exactly once (by the block holding its end).
+// with offset o = j - i in [0, kQSample). So:
+//
+//   1. KQ streams the text and tests the q-gram at every sample against a
+//      blocked Bloom filter of all (pattern, o) q-grams (shared memory, one
+//      32-bit word per probe, four bits per key; no false negatives);
+//   2. V0 confirms each survivor j exactly: the q-gram's (pattern, o) list
+//      from an exact hash table, then a byte compare of the pattern against
+//      the text at i = j - o. A confirmed occurrence marks the 64-byte block
+//      holding its end e = i + L - 1 as dirty;
+//   3. only dirty blocks are walked with the real automaton (V1 counts, V2
+//      writes in order), which emits every match ending in them.
+//
+// Every match's block is dirty (steps 1-2 have no false negatives for its
+// owned sample), and every match is emitted once, by the block holding its
+// end. The automaton stays the single source of truth for what is emitted.
 //
 // Codes. Base b -> 2-bit code (b >> 1) & 3 (A0 C1 T2 G3, the dna4 column);
 // a q-gram's code has base k at bits 2k (q <= 16: one 32-bit word).
@@ -24,12 +33,9 @@ constexpr std::uint32_t kQMaxQ = 16;    // q-gram length cap (32-bit codes)
 constexpr std::uint32_t kQMinQ = 10;    // below this the filter is not selective
 constexpr std::uint32_t kQBlock = 64;   // dirty-block size (bytes)
 constexpr std::uint32_t kQChunkBlocks = 128;  // blocks per output chunk (8 KiB)
-// Bloom stages: 2^20, 2^19 and 2^18 bits = 224 KiB of shared memory in total.
-constexpr std::uint32_t kQLog0 = 20, kQLog1 = 19, kQLog2 = 18;
-constexpr std::uint32_t kQOff1 = (1u << kQLog0) / 32;               // word offset of stage 1
-constexpr std::uint32_t kQOff2 = kQOff1 + (1u << kQLog1) / 32;      // word offset of stage 2
-constexpr std::uint32_t kQWords = kQOff2 + (1u << kQLog2) / 32;     // 57344 words
+constexpr std::uint32_t kQWords = 57344;      // Bloom words (224 KiB of shared memory)
 constexpr std::uint32_t kQMul0 = 0x9E3779B1u, kQMul1 = 0x85EBCA77u, kQMul2 = 0xC2B2AE3Du;
+constexpr std::uint32_t kQEmpty = 0xFFFFFFFFu;  // exact-table slot marker
 
 #if defined(__CUDACC__)
 #define ACG_HD __host__ __device__ __forceinline__
@@ -37,10 +43,34 @@ constexpr std::uint32_t kQMul0 = 0x9E3779B1u, kQMul1 = 0x85EBCA77u, kQMul2 = 0xC
 #define ACG_HD inline
 #endif
 
-// Bit index of code c in stage k (multiplicative hashing, top bits).
-ACG_HD std::uint32_t qhash0(std::uint32_t c) { return (c * kQMul0) >> (32 - kQLog0); }
-ACG_HD std::uint32_t qhash1(std::uint32_t c) { return (c * kQMul1) >> (32 - kQLog1); }
-ACG_HD std::uint32_t qhash2(std::uint32_t c) { return (c * kQMul2) >> (32 - kQLog2); }
+ACG_HD std::uint32_t qmulhi(std::uint32_t a, std::uint32_t b) {
+#if defined(__CUDA_ARCH__)
+    return __umulhi(a, b);
+#else
+    return static_cast<std::uint32_t>((static_cast<std::uint64_t>(a) * b) >> 32);
+#endif
+}
+
+ACG_HD std::uint32_t qperm(std::uint32_t x, std::uint32_t y, std::uint32_t sel) {  // PRMT, selectors < 8
+#if defined(__CUDA_ARCH__)
+    return __byte_perm(x, y, sel);
+#else
+    const std::uint64_t v = (static_cast<std::uint64_t>(y) << 32) | x;
+    std::uint32_t r = 0;
+    for (int i = 0; i < 4; ++i) r |= static_cast<std::uint32_t>((v >> (8 * ((sel >> (4 * i)) & 7u))) & 0xFFu) << (8 * i);
+    return r;
+#endif
+}
+
+// Bloom probe of code c: the word index, and a four-bit mask with one bit in
+// each byte of the word (bit (sel_i & 7) of byte i, sel from an independent
+// hash) — one PRMT builds it.
+ACG_HD std::uint32_t qword(std::uint32_t c) { return qmulhi(c * kQMul0, kQWords); }
+ACG_HD std::uint32_t qmask(std::uint32_t c) {
+    return qperm(0x08040201u, 0x80402010u, qmulhi(c, kQMul1) & 0x7777u);
+}
+// Exact table slot of code c in a table of 2^bits slots.
+ACG_HD std::uint32_t qslot(std::uint32_t c, std::uint32_t bits) { return (c * kQMul2) >> (32 - bits); }
 
 #undef ACG_HD
 

@@ -96,12 +96,22 @@ struct ScanArgs {
     std::uint32_t* cand_n;                  // per chunk: exported count, 0xFFFFFFFF = re-walk
     unsigned long long* ev_total;           // sum of events (mode heuristic)
     // filter mode (filter_kernels.cuh)
-    const std::uint32_t* qbloom;            // kQWords Bloom words
+    const std::uint32_t* qbloom;            // kQWords blocked-Bloom words
+    const std::uint32_t* qtab;              // exact q-gram table: 2^qtab_bits (code, bucket) slots
+    std::uint32_t qtab_bits;
+    const std::uint32_t* qb_off;            // bucket offsets
+    const std::uint32_t* qb_ent;            // pattern id << 2 | offset
+    const std::uint8_t* pat_bytes;          // the dictionary
+    const std::uint32_t* pat_off;           // n_patterns + 1
+    unsigned long long* qcands;             // KQ survivors (sample offsets)
+    std::uint32_t* qcand_n;                 // survivors appended (may exceed qcand_cap)
+    std::uint32_t qcand_cap;
+    unsigned long long* pcounts;            // per-pattern counts (filter mode counts them directly)
+    unsigned long long* qscratch;           // V0 count pass: packed records, unordered (rec_cap entries)
+    unsigned long long* qscratch_n;
+    std::uint32_t* qfill;                   // per chunk: records placed so far
     std::uint32_t q;                        // q-gram length
     std::uint32_t max_len;                  // longest pattern
-    std::uint32_t* dirty;                   // 1 bit per 64-byte block of [emit_from, n), n_chunks*4 words
-    std::uint32_t* block_count;             // per dirty block: matches ending in it (count pass)
-    std::uint32_t hot_rows;                 // rows of hot16 staged in shared memory by the block walks
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {

@@ -42,7 +42,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
     if force or _stale(synth, [src]):
         _run(["g++", "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", synth, src])
 
-    headers = [os.path.join(CSRC, h) for h in ("automaton.hpp", "scan_kernels.cuh")] + [
+    headers = [os.path.join(CSRC, h) for h in ("automaton.hpp", "scan_kernels.cuh", "filter_kernels.cuh",
+                                               "qfilter.hpp")] + [
         os.path.join(ROOT, "include", "acg.h")]
     auto_src = os.path.join(CSRC, "automaton.cpp")
     auto_o = os.path.join(obj, "automaton.o")
