@@ -113,7 +113,7 @@ class Automaton:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and _lib is not None:  # (module globals may be gone at interpreter exit)
             _lib.acg().acg_automaton_destroy(h)
             self._h = C.c_void_p()
 
@@ -275,7 +275,7 @@ class Scanner:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and _lib is not None:
             _lib.acg().acg_scanner_destroy(h)
             self._h = C.c_void_p()
 

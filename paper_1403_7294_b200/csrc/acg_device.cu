@@ -167,6 +167,7 @@ struct acg_scanner {
     // filter mode: KQ survivors (count in scalars32[3]), V0 record scratch
     // (count in scalars64[5]), per-chunk fill counters, heavy chunks (count in scalars32[2])
     DevBuf<unsigned long long> qcands, qscratch;
+    DevBuf<std::uint32_t> qcand_code, qwarp_n;
     DevBuf<std::uint32_t> qfill, qheavy;
     bool regrow = false;  // enqueue_write after a record-buffer regrowth
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
@@ -362,15 +363,15 @@ cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid
 std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
-// Filter mode: batch depth and block size of KQ.
-#ifndef ACG_QBATCH
-#define ACG_QBATCH 2
+// Filter mode: KQ geometry.
+#ifndef ACG_QWARPS
+#define ACG_QWARPS 15
 #endif
-#ifndef ACG_QTHREADS
-#define ACG_QTHREADS 512
+#ifndef ACG_QSTAGES
+#define ACG_QSTAGES 3
 #endif
-constexpr int kQBatch = ACG_QBATCH;
-constexpr int kQThreads = ACG_QTHREADS;
+constexpr int kQConsumerWarps = ACG_QWARPS;  // KQ: consumer warps (+1 producer warp)
+constexpr int kQStages = ACG_QSTAGES;        // KQ: shared-memory text stages
 
 // Enqueue K3 (compaction + ordered write) for the current geometry.
 int enqueue_write(acg_scanner* s, cudaStream_t st) {
@@ -563,6 +564,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.pat_bytes = dd.pat_bytes.p;
         a.pat_off = dd.pat_off.p;
         a.q = d.q;
+        a.qsh = d.q >= 16 ? 1u : 1u << (32 - 2 * d.q);
         a.max_len = d.max_len;
         a.pcounts = want_counts ? s->counts.p : nullptr;
         a.qfill = s->qfill.p;
@@ -572,22 +574,33 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             a.qscratch_n = s->scalars64.p + 5;
             ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 5, 0, sizeof(unsigned long long), st));
         }
-        // survivors: sized from the previous run's rate (x4 headroom), at least one per 4 KiB;
-        // a full list is detected at sync and the scan re-run with a larger one
+        // survivors: one region per KQ consumer warp, sized from the previous run's
+        // rate (x4 headroom over the even share); a full region is detected at sync
+        // and the scan re-run with larger regions
+        const unsigned long long warps = static_cast<unsigned long long>(dd.num_sms) * kQConsumerWarps;
         const double rate = s->last_filter_rate > 0 ? s->last_filter_rate : 1.0 / 4096;
-        unsigned long long cap = std::max<unsigned long long>(
-            1ull << 16, static_cast<unsigned long long>(4.0 * rate * static_cast<double>(n)) + n / 4096);
-        cap = std::min<unsigned long long>(0xFFFFFFFFull, std::max(cap, s->min_task_cap));
-        ACG_CUDA(s->qcands.reserve(cap));
+        unsigned long long cap = static_cast<unsigned long long>(4.0 * rate * static_cast<double>(n) / warps) + 64;
+        cap = std::min<unsigned long long>(0x7FFFFFFFull / warps, std::max(cap, s->min_task_cap));
+        ACG_CUDA(s->qcands.reserve(cap * warps));
+        ACG_CUDA(s->qcand_code.reserve(cap * warps));
+        ACG_CUDA(s->qwarp_n.reserve(warps));
         a.qcands = s->qcands.p;
-        a.qcand_cap = static_cast<std::uint32_t>(std::min<unsigned long long>(cap, s->qcands.n));
+        a.qcand_code = s->qcand_code.p;
+        a.qwarp_n = s->qwarp_n.p;
+        a.qwarps = static_cast<std::uint32_t>(warps);
+        a.qwords = static_cast<std::uint32_t>(d.qbloom.size());
+        a.qcand_cap = static_cast<std::uint32_t>(cap);
         a.qcand_n = s->scalars32.p + 3;
+        a.qcand_max = s->scalars64.p + 6;
         ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 3, 0, sizeof(std::uint32_t), st));
+        ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 6, 0, sizeof(unsigned long long), st));
+        ACG_CUDA(cudaMemsetAsync(s->qwarp_n.p, 0, warps * sizeof(std::uint32_t), st));
         {
-            auto k = qfilter_kernel<kQBatch, kQThreads>;
-            const std::size_t smem = acg::kQWords * sizeof(std::uint32_t);
+            auto k = qfilter_kernel<kQConsumerWarps, kQStages>;
+            constexpr std::size_t slot = kQConsumerWarps * 32 * 32 + 16;
+            const std::size_t smem = static_cast<std::size_t>(a.qwords) * 4 + kQStages * slot + 16 * kQStages;
             ACG_CUDA(prepare_smem(k, smem));
-            k<<<dd.num_sms, kQThreads, smem, st>>>(a);
+            k<<<dd.num_sms, 32 * (kQConsumerWarps + 1), smem, st>>>(a);
             ACG_CUDA(cudaGetLastError());
             ++s->launches;
         }
@@ -677,6 +690,8 @@ int scanner_sync(acg_scanner* s) {
     ACG_CUDA(cudaMemcpyAsync(s->pinned + 5, s->scalars64.p + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              st));
     ACG_CUDA(cudaMemcpyAsync(s->pinned + 6, s->scalars32.p, 4 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    if (s->mode_run == ACG_MODE_FILTER)
+        ACG_CUDA(cudaMemcpyAsync(s->pinned + 4, s->scalars64.p + 6, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     ACG_CUDA(cudaStreamSynchronize(st));
     if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
         const std::uint32_t ntask = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[1];
@@ -691,9 +706,9 @@ int scanner_sync(acg_scanner* s) {
         }
     }
     if (s->mode_run == ACG_MODE_FILTER && s->n_chunks) {
-        const std::uint32_t ncand = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[3];
-        if (ncand > s->args.qcand_cap) {  // the survivor list overflowed: grow and run again
-            s->min_task_cap = static_cast<unsigned long long>(ncand) + ncand / 4 + 4096;
+        const unsigned long long worst = s->pinned[4];
+        if (worst > s->args.qcand_cap) {  // a survivor region overflowed: grow and run again
+            s->min_task_cap = worst + worst / 4 + 64;
             const int req = s->mode_req;
             s->mode_req = ACG_MODE_FILTER;
             const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);

@@ -3,6 +3,7 @@
 #include "qfilter.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -251,12 +252,18 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         }
     }
     std::sort(grams.begin(), grams.end());
-    d.qbloom.assign(kQWords, 0u);
+    std::uint32_t words = kQWords;
+    if (const char* e = std::getenv("ACG_QWORDS")) {  // experiments only (Bloom size sweeps)
+        const long v = std::strtol(e, nullptr, 10);
+        if (v >= 1024 && v <= 57344) words = static_cast<std::uint32_t>(v) & ~3u;
+    }
+    d.qbloom.assign(words, 0u);
     std::uint32_t keys = 0;
     for (std::size_t i = 0; i < grams.size(); ++i) {
         if (i && grams[i].first == grams[i - 1].first) continue;
         ++keys;
-        d.qbloom[qword(grams[i].first)] |= qmask(grams[i].first);
+        const std::uint32_t y = qtop(grams[i].first, q);
+        d.qbloom[qword(y, words)] |= qmask(y);
     }
     d.qtab_bits = 10;
     while ((1u << d.qtab_bits) < 2u * keys) ++d.qtab_bits;
@@ -283,8 +290,9 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         r = (r ^ (r >> 30)) * 0xBF58476D1CE4E5B9ull;
         r = (r ^ (r >> 27)) * 0x94D049BB133111EBull;
         const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
-        const std::uint32_t m = qmask(c);
-        pass += (d.qbloom[qword(c)] & m) == m;
+        const std::uint32_t y = qtop(c, q);
+        const std::uint32_t m = qmask(y);
+        pass += (d.qbloom[qword(y, words)] & m) == m;
     }
     d.filter_fp = static_cast<double>(pass) / trials;
     // worth it when few samples survive (each survivor costs an exact probe)

@@ -33,7 +33,7 @@ constexpr std::uint32_t kQMaxQ = 16;    // q-gram length cap (32-bit codes)
 constexpr std::uint32_t kQMinQ = 10;    // below this the filter is not selective
 constexpr std::uint32_t kQBlock = 64;   // dirty-block size (bytes)
 constexpr std::uint32_t kQChunkBlocks = 128;  // blocks per output chunk (8 KiB)
-constexpr std::uint32_t kQWords = 57344;      // Bloom words (224 KiB of shared memory)
+constexpr std::uint32_t kQWords = 45056;      // Bloom words (176 KiB of shared memory; the rest stages text)
 constexpr std::uint32_t kQMul0 = 0x9E3779B1u, kQMul1 = 0x85EBCA77u, kQMul2 = 0xC2B2AE3Du;
 constexpr std::uint32_t kQEmpty = 0xFFFFFFFFu;  // exact-table slot marker
 
@@ -62,13 +62,16 @@ ACG_HD std::uint32_t qperm(std::uint32_t x, std::uint32_t y, std::uint32_t sel) 
 #endif
 }
 
-// Bloom probe of code c: the word index, and a four-bit mask with one bit in
-// each byte of the word (bit (sel_i & 7) of byte i, sel from an independent
-// hash) — one PRMT builds it.
-ACG_HD std::uint32_t qword(std::uint32_t c) { return qmulhi(c * kQMul0, kQWords); }
-ACG_HD std::uint32_t qmask(std::uint32_t c) {
-    return qperm(0x08040201u, 0x80402010u, qmulhi(c, kQMul1) & 0x7777u);
+// Bloom probe of a q-gram given as y = code << (32 - 2q) (the code in the
+// top bits: the device gets y from an unmasked 32-bit window with one
+// multiply, which also drops the bases past the q-gram). qword: the word
+// index; qmask: four bits, one in each byte of the word (bit (sel_i & 7) of
+// byte i, sel from an independent hash) — one PRMT builds it.
+ACG_HD std::uint32_t qword(std::uint32_t y, std::uint32_t words) { return qmulhi(y * kQMul0, words); }
+ACG_HD std::uint32_t qmask(std::uint32_t y) {
+    return qperm(0x08040201u, 0x80402010u, qmulhi(y, kQMul1) & 0x7777u);
 }
+ACG_HD std::uint32_t qtop(std::uint32_t code, std::uint32_t q) { return q >= 16 ? code : code << (32 - 2 * q); }
 // Exact table slot of code c in a table of 2^bits slots.
 ACG_HD std::uint32_t qslot(std::uint32_t c, std::uint32_t bits) { return (c * kQMul2) >> (32 - bits); }
 

@@ -103,14 +103,20 @@ struct ScanArgs {
     const std::uint32_t* qb_ent;            // pattern id << 2 | offset
     const std::uint8_t* pat_bytes;          // the dictionary
     const std::uint32_t* pat_off;           // n_patterns + 1
-    unsigned long long* qcands;             // KQ survivors (sample offsets)
-    std::uint32_t* qcand_n;                 // survivors appended (may exceed qcand_cap)
-    std::uint32_t qcand_cap;
+    std::uint32_t qwords;                   // Bloom words
+    unsigned long long* qcands;             // KQ survivors (sample offsets): one region of qcand_cap per KQ warp
+    std::uint32_t* qcand_code;              // their q-gram codes (top-aligned, see qtop)
+    std::uint32_t* qwarp_n;                 // per KQ consumer warp: survivors found (may exceed qcand_cap)
+    std::uint32_t qwarps;                   // KQ consumer warps (regions)
+    std::uint32_t* qcand_n;                 // total survivors (rate heuristic)
+    unsigned long long* qcand_max;          // max over regions (overflow check at sync)
+    std::uint32_t qcand_cap;                // per-region capacity
     unsigned long long* pcounts;            // per-pattern counts (filter mode counts them directly)
     unsigned long long* qscratch;           // V0 count pass: packed records, unordered (rec_cap entries)
     unsigned long long* qscratch_n;
     std::uint32_t* qfill;                   // per chunk: records placed so far
     std::uint32_t q;                        // q-gram length
+    std::uint32_t qsh;                      // 2^(32 - 2q): window * qsh puts the q-gram code in the top bits
     std::uint32_t max_len;                  // longest pattern
 };
 
