@@ -378,10 +378,9 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     using namespace acg::kern;
     const DeviceDfa& dd = *s->dd;
     ACG_CUDA(cudaMemsetAsync(s->scalars32.p, 0, sizeof(std::uint32_t), st));
-    {
-        const unsigned tb = 256;
-        const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((s->n_chunks + tb - 1) / tb, 4096ull));
-        compact_active_kernel<<<std::max(g, 1u), tb, 0, st>>>(s->chunk_counts.p, static_cast<long long>(s->n_chunks),
+    if (s->mode_run != ACG_MODE_FILTER) {  // (filter mode sweeps the chunk offsets itself)
+        const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((s->n_chunks + 2047) / 2048, 1024ull));
+        compact_active_kernel<<<std::max(g, 1u), 256, 0, st>>>(s->chunk_counts.p, static_cast<long long>(s->n_chunks),
                                                                s->active_list.p, s->scalars32.p);
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
@@ -404,7 +403,11 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         ++s->launches;
         ACG_CUDA(s->qheavy.reserve(s->n_chunks));
         ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 2, 0, sizeof(std::uint32_t), st));
-        acg::kern::qsort_chunks_kernel<<<4 * dd.num_sms, 256, 0, st>>>(wa, s->qheavy.p, s->scalars32.p + 2);
+        {
+            const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
+                1, std::min<unsigned long long>((s->n_chunks + 255) / 256, 8ull * dd.num_sms)));
+            acg::kern::qsort_chunks_kernel<<<g, 256, 0, st>>>(wa, s->qheavy.p, s->scalars32.p + 2);
+        }
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
         auto k = acg::kern::qheavy_kernel;

@@ -265,34 +265,46 @@ __global__ void __launch_bounds__(256) qscatter_kernel(const ScanArgs a) {
 }
 
 // Orders each chunk's records: warp bitonic sort when the chunk has <= 32;
-// bigger chunks go to the heavy list (qheavy_kernel).
+// bigger chunks go to the heavy list (qheavy_kernel). Warps sweep the chunk
+// offsets directly (no compacted list: its single counter would serialise
+// thousands of same-address atomics).
+__device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, v, stride);
+            const bool up = (lane & size) == 0;     // this lane's run ascends
+            const bool low = (lane & stride) == 0;  // lower element of its pair
+            v = (low == up) ? min(v, o) : max(v, o);
+        }
+    }
+    return v;
+}
+
 __global__ void __launch_bounds__(256) qsort_chunks_kernel(const ScanArgs a, std::uint32_t* heavy,
                                                            std::uint32_t* n_heavy) {
-    const long long n_work = static_cast<long long>(*a.active_count);
     const int lane = threadIdx.x & 31;
     const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-    for (long long t = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); t < n_work;
-         t += warps) {
-        const long long c = a.active_list[t];
-        const unsigned long long lo = a.chunk_offs[c], k = a.chunk_offs[c + 1] - lo;
-        if (k <= 1) continue;
-        if (k > 32) {
-            if (lane == 0) heavy[atomicAdd(n_heavy, 1u)] = static_cast<std::uint32_t>(c);
-            continue;
+    for (long long c0 = (static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+         c0 < a.n_chunks; c0 += warps * 32) {
+        const long long c = c0 + lane;
+        const unsigned long long lo = c < a.n_chunks ? a.chunk_offs[c] : 0ull;
+        const unsigned long long k = c < a.n_chunks ? a.chunk_offs[c + 1] - lo : 0ull;
+        unsigned todo = __ballot_sync(0xFFFFFFFFu, k >= 2);
+        const unsigned big = __ballot_sync(0xFFFFFFFFu, k > 32);
+        if (big & (1u << lane)) heavy[atomicAdd(n_heavy, 1u)] = static_cast<std::uint32_t>(c);
+        todo &= ~big;
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const unsigned long long slo = __shfl_sync(0xFFFFFFFFu, lo, src);
+            const unsigned long long sk = __shfl_sync(0xFFFFFFFFu, k, src);
+            if (slo + sk > a.rec_cap) continue;  // record buffer overflowed: re-emitted after regrowth
+            unsigned long long v = lane < static_cast<int>(sk) ? a.records[slo + lane] : ~0ull;
+            v = bitonic32(v, lane);
+            if (lane < static_cast<int>(sk)) a.records[slo + lane] = v;
         }
-        if (lo + k > a.rec_cap) continue;  // record buffer overflowed: re-emitted after regrowth
-        unsigned long long v = lane < static_cast<int>(k) ? a.records[lo + lane] : ~0ull;
-#pragma unroll
-        for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, v, stride);
-                const bool up = (lane & size) == 0;     // this lane's run ascends
-                const bool low = (lane & stride) == 0;  // lower element of its pair
-                v = (low == up) ? min(v, o) : max(v, o);
-            }
-        }
-        if (lane < static_cast<int>(k)) a.records[lo + lane] = v;
     }
 }
 

@@ -1094,19 +1094,41 @@ __global__ void __launch_bounds__(256) sparse_emit_kernel(const ScanArgs a) {
 }
 
 // Compacts the ids of chunks with at least one match (order is irrelevant:
-// every chunk writes at its own prefix offset).
-__global__ void compact_active_kernel(const unsigned long long* counts, long long n, std::uint32_t* list,
-                                      std::uint32_t* n_active) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const bool on = counts[i] != 0;
-        const unsigned m = __ballot_sync(__activemask(), on);
-        if (!m) continue;
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(m) - 1;
-        std::uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(n_active, static_cast<std::uint32_t>(__popc(m)));
-        base = __shfl_sync(m | (1u << lane), base, leader);
-        if (on) list[base + __popc(m & ((1u << lane) - 1))] = static_cast<std::uint32_t>(i);
+// every chunk writes at its own prefix offset). One atomic per block tile
+// (256 threads x 8 chunks): same-address atomics serialise at L2, so
+// per-warp atomics would cost ~ns each across thousands of warps.
+__global__ void __launch_bounds__(256) compact_active_kernel(const unsigned long long* counts, long long n,
+                                                             std::uint32_t* list, std::uint32_t* n_active) {
+    __shared__ std::uint32_t warp_tot[8], base_sh;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kItems = 8;
+    for (long long t0 = static_cast<long long>(blockIdx.x) * 256 * kItems; t0 < n;
+         t0 += static_cast<long long>(gridDim.x) * 256 * kItems) {
+        unsigned bits[kItems];
+        std::uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const long long i = t0 + (static_cast<long long>(warp) * kItems + k) * 32 + lane;
+            bits[k] = __ballot_sync(0xFFFFFFFFu, i < n && counts[i] != 0);
+            mine += __popc(bits[k]);
+        }
+        if (lane == 0) warp_tot[warp] = mine;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            std::uint32_t tot = 0;
+            for (int w = 0; w < 8; ++w) tot += warp_tot[w];
+            base_sh = tot ? atomicAdd(n_active, tot) : 0u;
+        }
+        __syncthreads();
+        std::uint32_t base = base_sh;
+        for (int w = 0; w < warp; ++w) base += warp_tot[w];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const long long i = t0 + (static_cast<long long>(warp) * kItems + k) * 32 + lane;
+            if (bits[k] & (1u << lane)) list[base + __popc(bits[k] & ((1u << lane) - 1))] = static_cast<std::uint32_t>(i);
+            base += __popc(bits[k]);
+        }
+        __syncthreads();
     }
 }
 
