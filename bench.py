@@ -38,6 +38,14 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
+# per-stage labels of acg_scanner_kernel_ms by scan mode
+STAGES = {
+    "filter": ("KQ_filter", "V0_confirm", "K2_prefix", "K3_order", "K4_unused"),
+    "sparse": ("K1s_walk", "K1f_fixup", "K2_prefix", "K3_write", "K4_counts"),
+    "exact": ("K1x_walk", "none", "K2_prefix", "K3_write", "K4_counts"),
+}
+
+
 def golden_check(w, m: int, dsum: int, dxor: int, counts) -> str:
     """Compare the timed run's output with the reference's own statistics for
     this workload (tests/golden/configs_full.json, from oracle/make_goldens.py)."""
@@ -368,7 +376,7 @@ def main() -> None:
     tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"config{args.config}")
+            traffic = json.load(open(tf)).get(f"config{args.config}:{mode_name}")
         except Exception:
             traffic = None
     achieved = d_text.numel() / (k1_ms * 1e-3) / 1e9
@@ -394,11 +402,11 @@ def main() -> None:
                    "scan_mode": mode_name, "excursion_event_rate": round(ev_rate, 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": f"{'sparse_scan_kernel (K1s)' if mode_name == 'sparse' else 'exact_scan_kernel<COUNT> (K1x)'}", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                     "kernel": {"sparse": "sparse_scan_kernel (K1s)", "filter": "qfilter_kernel (KQ)"}.get(
+                         mode_name, "exact_scan_kernel<COUNT> (K1x)"),
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                      "algorithmic_bytes_per_launch": int(d_text.numel()),
-                     "stage_ms": {"K1_walk": round(float(k_ms[0]), 4), "K1f_fixup": round(float(k_ms[1]), 4),
-                                  "K2_prefix": round(float(k_ms[2]), 4), "K3_write": round(float(k_ms[3]), 4),
-                                  "K4_counts": round(float(k_ms[4]), 4)}},
+                     "stage_ms": dict(zip(STAGES.get(mode_name, STAGES["exact"]), (round(float(x), 4) for x in k_ms)))},
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h_text.numel()),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(geo["launches"]) * args.steps,
