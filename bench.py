@@ -256,7 +256,7 @@ def main() -> None:
     ap.add_argument("--threads-per-block", type=int, default=0)
     ap.add_argument("--chunk-bytes", type=int, default=0)
     ap.add_argument("--profile-layout", action="store_true", help="profile-guided hot-state order")
-    ap.add_argument("--mode", default="auto", choices=["auto", "sparse", "exact"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "sparse", "exact", "filter"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -298,7 +298,8 @@ def main() -> None:
     flags = am.SCAN_LIST | am.SCAN_COUNTS | am.SCAN_PROFILE
     sc = am.Scanner(a, local, flags)
     sc.set_geometry(args.streams_per_thread, args.threads_per_block, args.chunk_bytes)
-    sc.set_mode({"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT}[args.mode])
+    sc.set_mode({"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT,
+                 "filter": am.MODE_FILTER}[args.mode])
     stream = torch.cuda.Stream()
     P = a.pattern_count()
     counts_all = torch.zeros(P, dtype=torch.int64, device="cuda")
@@ -322,8 +323,10 @@ def main() -> None:
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             step()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         ev1.record(stream)
         torch.cuda.synchronize()
     elapsed_ms = ev0.elapsed_time(ev1)
@@ -406,6 +409,7 @@ def main() -> None:
                          mode_name, "exact_scan_kernel<COUNT> (K1x)"),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                      "algorithmic_bytes_per_launch": int(d_text.numel()),
+                     "host_enqueue_ms_per_step": round(host_ms, 4),
                      "stage_ms": dict(zip(STAGES.get(mode_name, STAGES["exact"]), (round(float(x), 4) for x in k_ms)))},
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h_text.numel()),
                 "d2h_bytes_per_step": int(d2h)},

@@ -59,27 +59,93 @@ int fail(int code, const std::string& msg) {
         }                                                                                           \
     } while (0)
 
+// Device memory comes from each device's stream-ordered pool (cudaMallocAsync
+// / cudaFreeAsync) with the release threshold lifted, so workspace growth and
+// automaton teardown never synchronise the device or return memory to the
+// driver (run_partitioned builds, scans and drops one automaton per worker on
+// every run). Buffers are allocated on the stream that first uses them;
+// destructors run only after the owner synchronised its streams and free on
+// the device's housekeeping stream (never destroyed).
+std::mutex g_hk_mu;
+std::map<int, cudaStream_t> g_hk;
+
+cudaStream_t hk_stream(int device) {
+    std::lock_guard<std::mutex> lock(g_hk_mu);
+    auto it = g_hk.find(device);
+    if (it != g_hk.end()) return it->second;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        std::uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaStream_t st = nullptr;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaGetLastError();
+    cudaSetDevice(prev);
+    g_hk[device] = st;
+    return st;
+}
+
+int current_device_or0() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return d;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     std::size_t n = 0;  // capacity in elements
+    int dev = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, hk_stream(dev));
     }
-    cudaError_t reserve(std::size_t want) {
+    // grows in stream order on `st` (the old contents are not kept)
+    cudaError_t reserve(std::size_t want, cudaStream_t st) {
         if (want <= n && p) return cudaSuccess;
-        if (p) cudaFree(p);
+        dev = current_device_or0();
+        (void)hk_stream(dev);  // the pool's release threshold is set before its first use
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         n = 0;
         const std::size_t cap = std::max<std::size_t>(want, 1);
-        cudaError_t e = cudaMalloc(&p, cap * sizeof(T));
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), st);
         if (e == cudaSuccess) n = cap;
+        else p = nullptr;
         return e;
     }
 };
+
+// Small pinned host words for scanner scalars, carved from slabs that are
+// never freed (cudaFreeHost would synchronise the device).
+std::mutex g_pin_mu;
+std::vector<unsigned long long*> g_pin_free;
+
+unsigned long long* pinned_take() {
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    if (g_pin_free.empty()) {
+        constexpr int kPieces = 512, kWords = 8;
+        unsigned long long* slab = nullptr;
+        if (cudaMallocHost(&slab, kPieces * kWords * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        for (int i = kPieces - 1; i >= 0; --i) g_pin_free.push_back(slab + i * kWords);
+    }
+    unsigned long long* p = g_pin_free.back();
+    g_pin_free.pop_back();
+    return p;
+}
+void pinned_give(unsigned long long* p) {
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    g_pin_free.push_back(p);
+}
 
 struct DeviceDfa {
     int device = 0;
@@ -97,10 +163,10 @@ struct DeviceDfa {
 };
 
 template <typename T>
-cudaError_t upload(DevBuf<T>& dst, const T* src, std::size_t n) {
-    cudaError_t e = dst.reserve(n);
+cudaError_t upload(DevBuf<T>& dst, const T* src, std::size_t n, cudaStream_t st) {
+    cudaError_t e = dst.reserve(n, st);
     if (e != cudaSuccess) return e;
-    if (n) e = cudaMemcpy(dst.p, src, n * sizeof(T), cudaMemcpyHostToDevice);
+    if (n) e = cudaMemcpyAsync(dst.p, src, n * sizeof(T), cudaMemcpyHostToDevice, st);
     return e;
 }
 
@@ -141,6 +207,7 @@ struct acg_scanner {
     DevBuf<std::uint8_t> text;
     DevBuf<std::uint8_t> cub_tmp;
     unsigned long long* pinned = nullptr;  // 8 host words
+    cudaEvent_t order_ev = nullptr;        // orders a run on a new stream after the previous one
     // geometry of the last run
     acg::kern::ScanArgs args{};
     unsigned long long n_chunks = 0;
@@ -220,32 +287,34 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
     ACG_CUDA(cudaDeviceGetAttribute(&dd->num_sms, cudaDevAttrMultiProcessorCount, device));
     dd->dfa = host_dfa_locked(a, dd->smem_optin);
     const acg::Dfa& d = *dd->dfa;
-    ACG_CUDA(upload(dd->next, d.next.data(), d.next.size()));
-    ACG_CUDA(upload(dd->out_off, d.out_off.data(), d.out_off.size()));
-    ACG_CUDA(upload(dd->out_ids, d.out_ids.data(), d.out_ids.size()));
-    ACG_CUDA(upload(dd->depth, d.depth.data(), d.depth.size()));
-    ACG_CUDA(upload(dd->follows, d.follows.data(), d.follows.size()));
-    ACG_CUDA(upload(dd->follows_esc, d.follows_esc.data(), d.follows_esc.size()));
-    ACG_CUDA(upload(dd->symmap, d.symmap, 256));
+    const cudaStream_t up = hk_stream(device);
+    ACG_CUDA(upload(dd->next, d.next.data(), d.next.size(), up));
+    ACG_CUDA(upload(dd->out_off, d.out_off.data(), d.out_off.size(), up));
+    ACG_CUDA(upload(dd->out_ids, d.out_ids.data(), d.out_ids.size(), up));
+    ACG_CUDA(upload(dd->depth, d.depth.data(), d.depth.size(), up));
+    ACG_CUDA(upload(dd->follows, d.follows.data(), d.follows.size(), up));
+    ACG_CUDA(upload(dd->follows_esc, d.follows_esc.data(), d.follows_esc.size(), up));
+    ACG_CUDA(upload(dd->symmap, d.symmap, 256, up));
     // shared-memory images padded to 16 bytes for vector staging
     dd->hot_bytes = static_cast<std::uint32_t>((d.hot16.size() * 2 + 15) & ~std::size_t(15));
     std::vector<std::uint16_t> hot(dd->hot_bytes / 2, 0xFFFF);
     std::copy(d.hot16.begin(), d.hot16.end(), hot.begin());
-    ACG_CUDA(upload(dd->hot16, hot.data(), hot.size()));
+    ACG_CUDA(upload(dd->hot16, hot.data(), hot.size(), up));
     if (d.sparse_ok) {
         dd->hotH_bytes = static_cast<std::uint32_t>((d.hotH.size() * 2 + 15) & ~std::size_t(15));
         std::vector<std::uint16_t> hh(dd->hotH_bytes / 2, 0);
         std::copy(d.hotH.begin(), d.hotH.end(), hh.begin());
-        ACG_CUDA(upload(dd->hotH, hh.data(), hh.size()));
+        ACG_CUDA(upload(dd->hotH, hh.data(), hh.size(), up));
     }
     if (d.filter_ok) {
-        ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size()));
-        ACG_CUDA(upload(dd->qtab, d.qtab.data(), d.qtab.size()));
-        ACG_CUDA(upload(dd->qb_off, d.qb_off.data(), d.qb_off.size()));
-        ACG_CUDA(upload(dd->qb_ent, d.qb_ent.data(), d.qb_ent.size()));
-        ACG_CUDA(upload(dd->pat_off, d.pat_off32.data(), d.pat_off32.size()));
-        ACG_CUDA(upload(dd->pat_bytes, a->nfa.pat_bytes.data(), a->nfa.pat_bytes.size()));
+        ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size(), up));
+        ACG_CUDA(upload(dd->qtab, d.qtab.data(), d.qtab.size(), up));
+        ACG_CUDA(upload(dd->qb_off, d.qb_off.data(), d.qb_off.size(), up));
+        ACG_CUDA(upload(dd->qb_ent, d.qb_ent.data(), d.qb_ent.size(), up));
+        ACG_CUDA(upload(dd->pat_off, d.pat_off32.data(), d.pat_off32.size(), up));
+        ACG_CUDA(upload(dd->pat_bytes, a->nfa.pat_bytes.data(), a->nfa.pat_bytes.size(), up));
     }
+    ACG_CUDA(cudaStreamSynchronize(up));  // host staging vectors die here; buffers ready for any stream
     a->dev[device] = dd;
     *out = dd;
     return ACG_OK;
@@ -364,14 +433,37 @@ std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
 // Filter mode: KQ geometry.
-#ifndef ACG_QWARPS
-#define ACG_QWARPS 15
-#endif
-#ifndef ACG_QSTAGES
-#define ACG_QSTAGES 3
-#endif
-constexpr int kQConsumerWarps = ACG_QWARPS;  // KQ: consumer warps (+1 producer warp)
-constexpr int kQStages = ACG_QSTAGES;        // KQ: shared-memory text stages
+// KQ geometry: NW warps per SM, R blocks in flight per warp. ACG_QKERNEL
+// picks another instantiation (experiments only).
+struct QKernelChoice {
+    int nw = 16, r = 2;
+};
+QKernelChoice qfilter_choice() {
+    static const QKernelChoice c = [] {
+        QKernelChoice q;
+        const char* e = std::getenv("ACG_QKERNEL");
+        if (e && std::strcmp(e, "16x3") == 0) q.r = 3;
+        else if (e && std::strcmp(e, "24x2") == 0) q.nw = 24;
+        return q;
+    }();
+    return c;
+}
+unsigned qfilter_warps() { return static_cast<unsigned>(qfilter_choice().nw); }
+template <typename Kern>
+cudaError_t launch_q(Kern k, const ScanArgs& a, unsigned threads, std::size_t smem, int sms, cudaStream_t st) {
+    cudaError_t e = prepare_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<sms, threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
+    using namespace acg::kern;
+    const QKernelChoice c = qfilter_choice();
+    const std::size_t bloom = static_cast<std::size_t>(a.qwords) * 4;
+    if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2>, a, 32 * 24, bloom, sms, st);
+    if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3>, a, 32 * 16, bloom, sms, st);
+    return launch_q(qfilter_ldg_kernel<16, 2>, a, 32 * 16, bloom, sms, st);
+}
 
 // Enqueue K3 (compaction + ordered write) for the current geometry.
 int enqueue_write(acg_scanner* s, cudaStream_t st) {
@@ -401,7 +493,7 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         }
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
-        ACG_CUDA(s->qheavy.reserve(s->n_chunks));
+        ACG_CUDA(s->qheavy.reserve(s->n_chunks, st));
         ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 2, 0, sizeof(std::uint32_t), st));
         {
             const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
@@ -459,6 +551,18 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     s->grid = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + per_block - 1) / per_block));
 }
 
+// Work on `st` after everything this scanner enqueued before (possibly on
+// another stream): its workspace is reused and may be regrown on `st`.
+cudaError_t adopt_stream(acg_scanner* s, cudaStream_t st) {
+    if (s->last && s->last != st) {
+        cudaError_t e = cudaEventRecord(s->order_ev, s->last);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, s->order_ev, 0);
+        if (e != cudaSuccess) return e;
+    }
+    s->last = st;
+    return cudaSuccess;
+}
+
 int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std::uint64_t emit_from,
                 std::uint64_t base, cudaStream_t st) {
     using namespace acg::kern;
@@ -466,6 +570,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if ((reinterpret_cast<std::uintptr_t>(d_text) & 15) || (emit_from & 15))
         return fail(ACG_ERR_INVALID, "device text and emit_from must be 16-byte aligned");
     ACG_CUDA(cudaSetDevice(s->device));
+    ACG_CUDA(adopt_stream(s, st));
     const DeviceDfa& dd = *s->dd;
     const acg::Dfa& d = *dd.dfa;
     const bool want_list = s->flags & ACG_SCAN_LIST;
@@ -497,16 +602,16 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     const bool prof = s->flags & ACG_SCAN_PROFILE;
 
     const std::uint32_t n_out_states = (d.H - d.Hn) + (d.S - d.Cn);
-    ACG_CUDA(s->chunk_counts.reserve(s->n_chunks));
-    ACG_CUDA(s->chunk_offs.reserve(s->n_chunks + 1));
-    ACG_CUDA(s->active_list.reserve(s->n_chunks));
-    ACG_CUDA(s->visits.reserve(n_out_states));
-    ACG_CUDA(s->counts.reserve(d.out_ids.empty() ? 1 : s->a->nfa.n_patterns));
-    if (!s->records.p) ACG_CUDA(s->records.reserve(1u << 20));
+    ACG_CUDA(s->chunk_counts.reserve(s->n_chunks, st));
+    ACG_CUDA(s->chunk_offs.reserve(s->n_chunks + 1, st));
+    ACG_CUDA(s->active_list.reserve(s->n_chunks, st));
+    ACG_CUDA(s->visits.reserve(n_out_states, st));
+    ACG_CUDA(s->counts.reserve(d.out_ids.empty() ? 1 : s->a->nfa.n_patterns, st));
+    if (!s->records.p) ACG_CUDA(s->records.reserve(1u << 20, st));
     std::size_t cub_bytes = 0;
     const unsigned long long* in_it = s->chunk_counts.p;
     cub::DeviceScan::InclusiveSum(nullptr, cub_bytes, in_it, s->chunk_offs.p + 1, static_cast<int>(std::max<unsigned long long>(s->n_chunks, 1)), st);
-    ACG_CUDA(s->cub_tmp.reserve(cub_bytes));
+    ACG_CUDA(s->cub_tmp.reserve(cub_bytes, st));
 
     ACG_CUDA(cudaMemsetAsync(s->scalars64.p, 0, 5 * sizeof(unsigned long long), st));
     ACG_CUDA(cudaMemsetAsync(s->chunk_offs.p, 0, sizeof(unsigned long long), st));
@@ -558,7 +663,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
     if (mode == ACG_MODE_FILTER) {
         ACG_CUDA(cudaMemsetAsync(s->chunk_counts.p, 0, s->n_chunks * sizeof(unsigned long long), st));
-        ACG_CUDA(s->qfill.reserve(s->n_chunks));
+        ACG_CUDA(s->qfill.reserve(s->n_chunks, st));
         a.qbloom = dd.qbloom.p;
         a.qtab = dd.qtab.p;
         a.qtab_bits = d.qtab_bits;
@@ -572,7 +677,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.pcounts = want_counts ? s->counts.p : nullptr;
         a.qfill = s->qfill.p;
         if (want_list) {
-            ACG_CUDA(s->qscratch.reserve(s->records.n));
+            ACG_CUDA(s->qscratch.reserve(s->records.n, st));
             a.qscratch = s->qscratch.p;
             a.qscratch_n = s->scalars64.p + 5;
             ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 5, 0, sizeof(unsigned long long), st));
@@ -580,13 +685,14 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // survivors: one region per KQ consumer warp, sized from the previous run's
         // rate (x4 headroom over the even share); a full region is detected at sync
         // and the scan re-run with larger regions
-        const unsigned long long warps = static_cast<unsigned long long>(dd.num_sms) * kQConsumerWarps;
+        const unsigned warps_per_sm = qfilter_warps();
+        const unsigned long long warps = static_cast<unsigned long long>(dd.num_sms) * warps_per_sm;
         const double rate = s->last_filter_rate > 0 ? s->last_filter_rate : 1.0 / 4096;
         unsigned long long cap = static_cast<unsigned long long>(4.0 * rate * static_cast<double>(n) / warps) + 64;
         cap = std::min<unsigned long long>(0x7FFFFFFFull / warps, std::max(cap, s->min_task_cap));
-        ACG_CUDA(s->qcands.reserve(cap * warps));
-        ACG_CUDA(s->qcand_code.reserve(cap * warps));
-        ACG_CUDA(s->qwarp_n.reserve(warps));
+        ACG_CUDA(s->qcands.reserve(cap * warps, st));
+        ACG_CUDA(s->qcand_code.reserve(cap * warps, st));
+        ACG_CUDA(s->qwarp_n.reserve(warps, st));
         a.qcands = s->qcands.p;
         a.qcand_code = s->qcand_code.p;
         a.qwarp_n = s->qwarp_n.p;
@@ -598,15 +704,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 3, 0, sizeof(std::uint32_t), st));
         ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 6, 0, sizeof(unsigned long long), st));
         ACG_CUDA(cudaMemsetAsync(s->qwarp_n.p, 0, warps * sizeof(std::uint32_t), st));
-        {
-            auto k = qfilter_kernel<kQConsumerWarps, kQStages>;
-            constexpr std::size_t slot = kQConsumerWarps * 32 * 32 + 16;
-            const std::size_t smem = static_cast<std::size_t>(a.qwords) * 4 + kQStages * slot + 16 * kQStages;
-            ACG_CUDA(prepare_smem(k, smem));
-            k<<<dd.num_sms, 32 * (kQConsumerWarps + 1), smem, st>>>(a);
-            ACG_CUDA(cudaGetLastError());
-            ++s->launches;
-        }
+        ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
+        ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
         qconfirm_kernel<kCount><<<8 * dd.num_sms, 256, 0, st>>>(a);
         ACG_CUDA(cudaGetLastError());
@@ -617,12 +716,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         const unsigned long long per_warp = 32ull * s->U_run;
         const unsigned long long n_warps = (s->n_chunks + per_warp - 1) / per_warp;
         s->ev_cap = static_cast<std::uint32_t>(per_warp * (walk / 16));
-        ACG_CUDA(s->events.reserve(n_warps * s->ev_cap * 4ull));
-        ACG_CUDA(s->ev_count.reserve(n_warps));
-        ACG_CUDA(s->cands.reserve(s->n_chunks * acg::kern::kExport * 4ull));
-        ACG_CUDA(s->cand_n.reserve(s->n_chunks));
-        ACG_CUDA(s->cand_list.reserve(n_warps * acg::kern::kCandList * 2ull));
-        ACG_CUDA(s->cand_cnt.reserve(n_warps));
+        ACG_CUDA(s->events.reserve(n_warps * s->ev_cap * 4ull, st));
+        ACG_CUDA(s->ev_count.reserve(n_warps, st));
+        ACG_CUDA(s->cands.reserve(s->n_chunks * acg::kern::kExport * 4ull, st));
+        ACG_CUDA(s->cand_n.reserve(s->n_chunks, st));
+        ACG_CUDA(s->cand_list.reserve(n_warps * acg::kern::kCandList * 2ull, st));
+        ACG_CUDA(s->cand_cnt.reserve(n_warps, st));
         ACG_CUDA(cudaMemsetAsync(s->cand_cnt.p, 0, n_warps * sizeof(std::uint32_t), st));
         a.cand_list = s->cand_list.p;
         a.cand_cnt = s->cand_cnt.p;
@@ -634,8 +733,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         unsigned long long rcap = static_cast<unsigned long long>(walked * std::min(1.0, rate * 3.0) / regions) + 1024;
         rcap = std::max(rcap, s->min_task_cap);
         rcap = std::min<unsigned long long>(rcap, 0x7FFFFFFFull);
-        ACG_CUDA(s->tasks.reserve(regions * rcap * 4ull));
-        ACG_CUDA(s->task_cnt.reserve(regions));
+        ACG_CUDA(s->tasks.reserve(regions * rcap * 4ull, st));
+        ACG_CUDA(s->task_cnt.reserve(regions, st));
         a.tasks = s->tasks.p;
         a.task_cnt = s->task_cnt.p;
         a.task_max = s->scalars32.p + 1;
@@ -730,7 +829,7 @@ int scanner_sync(acg_scanner* s) {
     }
     if ((s->flags & ACG_SCAN_LIST) && s->m_total > s->records.n) {
         // record buffer overflowed: grow and re-emit (chunk counts and offsets are final)
-        ACG_CUDA(s->records.reserve(s->m_total + s->m_total / 4));
+        ACG_CUDA(s->records.reserve(s->m_total + s->m_total / 4, st));
         s->regrow = true;
         const int rc = enqueue_write(s, st);
         s->regrow = false;
@@ -753,10 +852,13 @@ int make_scanner(const acg_automaton* a, int device, std::uint32_t flags, acg_sc
     ACG_CUDA(cudaSetDevice(device));
     ACG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     ACG_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
-    ACG_CUDA(cudaMallocHost(&s->pinned, 8 * sizeof(unsigned long long)));
-    ACG_CUDA(s->scalars32.reserve(4));
-    ACG_CUDA(s->scalars64.reserve(8));
-    ACG_CUDA(cudaMemset(s->scalars64.p, 0, 8 * sizeof(unsigned long long)));
+    s->pinned = pinned_take();
+    if (!s->pinned) return fail(ACG_ERR_OUT_OF_MEMORY, "pinned host allocation failed");
+    ACG_CUDA(cudaEventCreateWithFlags(&s->order_ev, cudaEventDisableTiming));
+    ACG_CUDA(s->scalars32.reserve(4, s->stream));
+    ACG_CUDA(s->scalars64.reserve(8, s->stream));
+    ACG_CUDA(cudaMemsetAsync(s->scalars64.p, 0, 8 * sizeof(unsigned long long), s->stream));
+    s->last = s->stream;
     if (flags & ACG_SCAN_PROFILE)
         for (auto& e : s->ev) ACG_CUDA(cudaEventCreate(&e));
     *out = s.release();
@@ -770,7 +872,8 @@ void free_scanner(acg_scanner* s) {
     if (s->last) cudaStreamSynchronize(s->last);
     if (s->stream) cudaStreamDestroy(s->stream);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
-    if (s->pinned) cudaFreeHost(s->pinned);
+    if (s->pinned) pinned_give(s->pinned);
+    if (s->order_ev) cudaEventDestroy(s->order_ev);
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
     delete s;
@@ -993,7 +1096,8 @@ int acg_scanner_run_host(acg_scanner* s, const std::uint8_t* h_text, std::uint64
     if (!s || (!h_text && n)) return fail(ACG_ERR_INVALID, "null argument");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
     ACG_CUDA(cudaSetDevice(s->device));
-    ACG_CUDA(s->text.reserve(std::max<std::uint64_t>(n, 16)));
+    ACG_CUDA(adopt_stream(s, st));
+    ACG_CUDA(s->text.reserve(std::max<std::uint64_t>(n, 16), st));
     if (n) ACG_CUDA(cudaMemcpyAsync(s->text.p, h_text, n, cudaMemcpyHostToDevice, st));
     return scanner_run(s, s->text.p, n, 0, 0, st);
 }
@@ -1014,7 +1118,10 @@ int acg_scanner_packed_records(acg_scanner* s, std::uint64_t* host, std::uint64_
     if (const int rc = scanner_sync(s)) return rc;
     if (id_bits) *id_bits = s->dd->dfa->id_bits;
     const std::uint64_t m = std::min<std::uint64_t>(cap, s->m_total);
-    if (m) ACG_CUDA(cudaMemcpy(host, s->records.p, m * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+    if (m) {
+        ACG_CUDA(cudaMemcpyAsync(host, s->records.p, m * sizeof(std::uint64_t), cudaMemcpyDeviceToHost, s->last));
+        ACG_CUDA(cudaStreamSynchronize(s->last));
+    }
     return ACG_OK;
 }
 
@@ -1037,8 +1144,9 @@ int acg_scanner_pattern_counts(acg_scanner* s, std::uint64_t* host_counts) {
     if (!s) return fail(ACG_ERR_INVALID, "null scanner");
     if (!(s->flags & ACG_SCAN_COUNTS)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_COUNTS");
     if (const int rc = scanner_sync(s)) return rc;
-    ACG_CUDA(cudaMemcpy(host_counts, s->counts.p, s->a->nfa.n_patterns * sizeof(std::uint64_t),
-                        cudaMemcpyDeviceToHost));
+    ACG_CUDA(cudaMemcpyAsync(host_counts, s->counts.p, s->a->nfa.n_patterns * sizeof(std::uint64_t),
+                             cudaMemcpyDeviceToHost, s->last));
+    ACG_CUDA(cudaStreamSynchronize(s->last));
     return ACG_OK;
 }
 
@@ -1054,7 +1162,9 @@ const std::uint64_t* acg_scanner_device_records(acg_scanner* s, std::uint32_t* i
 
 std::uint64_t acg_scanner_failure_follows(acg_scanner* s) {
     if (!s || scanner_sync(s)) return 0;
-    if (cudaMemcpy(s->pinned + 4, s->scalars64.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (cudaMemcpyAsync(s->pinned + 4, s->scalars64.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->last) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s->last) != cudaSuccess)
         return 0;
     return s->pinned[4];
 }
@@ -1062,7 +1172,7 @@ std::uint64_t acg_scanner_failure_follows(acg_scanner* s) {
 int acg_scanner_digest(acg_scanner* s, std::uint64_t* dsum, std::uint64_t* dxor, std::uint64_t* unsorted_pairs) {
     if (!s) return fail(ACG_ERR_INVALID, "null scanner");
     if (const int rc = scanner_sync(s)) return rc;
-    ACG_CUDA(cudaMemset(s->scalars64.p + 1, 0, 3 * sizeof(unsigned long long)));
+    ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 1, 0, 3 * sizeof(unsigned long long), s->last));
     if (s->m_total) {
         const unsigned g = std::min<unsigned long long>((s->m_total + 255) / 256, 4096ull);
         acg::kern::digest_kernel<<<g, 256, 0, s->last>>>(s->records.p, s->m_total, s->dd->dfa->id_bits,

@@ -1,16 +1,20 @@
 // Filter-mode kernels (sampled q-gram prefilter; the scheme and its
 // exactness argument are in qfilter.hpp).
 //
-//  * qfilter_kernel (KQ) streams the text once at HBM rate: a producer warp
-//    moves the CTA's contiguous region through a ring of shared-memory stages
-//    with TMA bulk copies (mbarrier full/empty pipeline, L2 evict-first);
-//    consumer lanes take 32 bytes each. Each 16-byte half's 2-bit codes are
-//    packed into 32 bits; the next lane's first half comes by shuffle, so the
-//    q-grams at the eight samples (offsets 0, 4, .., 28) are funnel shifts of
-//    two 64-bit values. Each q-gram costs one shared-memory probe of the
-//    blocked Bloom filter (one 32-bit word, four bits), branch-free; survivors (rare) are
-//    appended to a candidate list with one warp-aggregated atomic (a full
-//    list is detected at sync and the scan re-run with a larger one).
+//  * qfilter_ldg_kernel (KQ) streams the text once at HBM rate: every warp
+//    walks its own contiguous region in 2 KiB blocks with 128-bit streaming
+//    loads straight into registers (R blocks in flight per warp), so all of
+//    shared memory holds the Bloom filter. Each 16-byte word's 2-bit codes
+//    are packed into 32 bits; the next word's codes come by shuffle, so the
+//    q-grams at the samples (offsets 0, 4, 8, 12) are funnel shifts of two
+//    32-bit values. Each q-gram costs one shared-memory probe of the blocked
+//    Bloom filter (one 32-bit word, four bits), branch-free; survivors (rare)
+//    go to the warp's own candidate region (a full region is detected at
+//    sync and the scan re-run with larger ones).
+//    (A TMA bulk-copy ring with a producer warp was measured first: 0.356 ms
+//    per GiB against 0.260 ms for this kernel at the same Bloom size — the
+//    ring's shared memory came out of the Bloom filter and its 46 KiB in
+//    flight per SM did not cover HBM latency.)
 //    Non-ACGT bytes need no check here: no occurrence contains one, so a
 //    q-gram over them can only make a (harmless) extra candidate.
 //  * qconfirm_kernel (V0) confirms each survivor exactly — the q-gram's
@@ -41,161 +45,121 @@ __device__ __forceinline__ std::uint32_t qcodes(const uint4& w) {
     return __byte_perm(__byte_perm(m0, m1, 0x0073u), __byte_perm(m2, m3, 0x7300u), 0x7610u);
 }
 
-// ---- bulk-copy (TMA) ring primitives --------------------------------------
-__device__ __forceinline__ void mbar_init(std::uint32_t bar, std::uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(std::uint32_t bar, std::uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-// Global -> shared bulk copy (TMA engine), completion counted on `bar`; the
-// text is streamed once, so it is marked evict-first in L2.
-__device__ __forceinline__ void bulk_load(std::uint32_t dst, const void* src, std::uint32_t bytes, std::uint32_t bar,
-                                          unsigned long long policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ uint4 lds128(std::uint32_t addr) {
+// KQ. No text staging in shared memory (all of it is left to the Bloom
+// filter): every warp streams its own contiguous
+// region of 2 KiB blocks with 128-bit streaming loads straight into
+// registers, R blocks in flight per warp (R*2 KiB*NW per SM). Lane l holds
+// the 16-byte words l, 32+l, 64+l, 96+l of a block (rows of 512 bytes); the
+// word after lane 31's row r is lane 0's row r+1, after row 3 it is lane 0's
+// row 0 of the next block (whose codes are computed one step ahead). 16
+// Bloom probes per lane and block; survivors go to the warp's region through
+// a shared-memory counter (no warp scan).
+__device__ __forceinline__ uint4 ldg_stream(const std::uint8_t* p) {
     uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 
-// KQ. Warp 0 is the producer: one lane streams the CTA's contiguous region
-// of the text into a ring of NST shared-memory stages with bulk copies
-// (full/empty mbarriers). Warps 1..NC consume one 1 KiB block of each stage
-// (a stage = NC KiB, plus the next 16 bytes so the last word sees its
-// neighbour).
-template <int NC, int NST>
-__global__ void __launch_bounds__(32 * (NC + 1), 1) qfilter_kernel(const ScanArgs a) {
-    constexpr std::uint32_t kUnits = NC * 32, kStage = kUnits * 32, kSlot = kStage + 16;
-    const std::uint32_t bloom_bytes = a.qwords * 4u;
+template <int NW, int R>
+__global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs a) {
+    constexpr long long kBlk = 2048;
+    __shared__ std::uint32_t wcnt[NW];
     const std::uint32_t* tab = reinterpret_cast<const std::uint32_t*>(acg_hot_smem);
-    const std::uint32_t ring = smem_u32(acg_hot_smem) + bloom_bytes;  // 16-byte aligned (qwords % 4 == 0)
-    const std::uint32_t bars = ring + NST * kSlot;                     // full[NST], empty[NST]
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.qbloom);
         uint4* dst = reinterpret_cast<uint4*>(acg_hot_smem);
-        for (std::uint32_t i = threadIdx.x; i < bloom_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-        if (threadIdx.x == 0) {
-            for (int k = 0; k < NST; ++k) {
-                mbar_init(bars + 8 * k, 1);
-                mbar_init(bars + 8 * (NST + k), NC);
-            }
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
+        for (std::uint32_t i = threadIdx.x; i < a.qwords / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+        if (threadIdx.x < NW) wcnt[threadIdx.x] = 0;
     }
     __syncthreads();
     const long long n = a.n;
-    const long long n_stages = (n + kStage - 1) / kStage;
-    const long long per = (n_stages + gridDim.x - 1) / gridDim.x;
-    const long long st0 = static_cast<long long>(blockIdx.x) * per;
-    const long long its = max(0LL, min(st0 + per, n_stages) - st0);
+    const long long nb = (n + kBlk - 1) / kBlk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long gw = static_cast<long long>(blockIdx.x) * NW + warp;
+    const long long tw = static_cast<long long>(gridDim.x) * NW;
+    const long long per = (nb + tw - 1) / tw;
+    const long long b0 = gw * per, b1 = min(b0 + per, nb);
+    const std::uint32_t qsh = a.qsh, words = a.qwords;
+    const unsigned long long region = static_cast<unsigned long long>(gw) * a.qcand_cap;
 
-    if (warp == 0) {  // producer
-        if (lane == 0) {
-            unsigned long long policy;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-            for (long long it = 0; it < its; ++it) {
-                const std::uint32_t k = static_cast<std::uint32_t>(it % NST);
-                if (it >= NST) mbar_wait(bars + 8 * (NST + k), static_cast<std::uint32_t>((it / NST - 1) & 1));
-                const long long off = (st0 + it) * kStage;
-                const std::uint32_t bytes =
-                    static_cast<std::uint32_t>((min(static_cast<long long>(kSlot), n - off) + 15) & ~15LL);
-                mbar_expect_tx(bars + 8 * k, bytes);
-                bulk_load(ring + k * kSlot, a.text + off, bytes, bars + 8 * k, policy);
-            }
-        }
-        return;
-    }
-
-    const std::uint32_t qsh = a.qsh;
-    const std::uint32_t words = a.qwords;
-#ifdef ACG_QABL_NOPROBE  // ablation: no shared-memory probe
-    auto probe = [&](std::uint32_t y) -> std::uint32_t { return (qmask(y) & ~(y * 0x9E3779B1u)) | 1u; };
-#else
+    uint4 buf[R][4];
+    auto load = [&](uint4 (&dst)[4], long long b) {
+        const long long off = b * kBlk + 16 * lane;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            dst[r] = (b < nb && off + 512 * r < n) ? ldg_stream(a.text + off + 512 * r) : make_uint4(0, 0, 0, 0);
+    };
     auto probe = [&](std::uint32_t y) -> std::uint32_t { return qmask(y) & ~tab[qword(y, words)]; };
-#endif
     auto gram = [&](std::uint32_t lo, std::uint32_t hi, int o) -> std::uint32_t {
         return (o == 0 ? lo : __funnelshift_r(lo, hi, 8 * o)) * qsh;
     };
-    // lane l of consumer warp w reads words l and 32+l of the warp's 1 KiB
-    // block (16-byte strides: conflict-free LDS.128); word 31's neighbour is
-    // word 32 (lane 0's second word), word 63's is the next block's word 0.
-    const std::uint32_t blk = static_cast<std::uint32_t>(warp - 1) * 1024u;
-    // survivors go to this warp's own region (no atomics on the hot path)
-    const unsigned long long region = (static_cast<unsigned long long>(blockIdx.x) * NC + (warp - 1)) * a.qcand_cap;
-    std::uint32_t found = 0;  // warp-uniform
-    for (long long it = 0; it < its; ++it) {
-        const std::uint32_t k = static_cast<std::uint32_t>(it % NST);
-        mbar_wait(bars + 8 * k, static_cast<std::uint32_t>((it / NST) & 1));
-#ifdef ACG_QABL_STREAM  // ablation: stream only
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bars + 8 * (NST + k));
-        continue;
-#endif
-        const std::uint32_t at = ring + k * kSlot + blk + 16 * lane;
-        const uint4 w0 = lds128(at), w1 = lds128(at + 512);
-        const uint4 nx = lane == 31 ? lds128(at + 528) : make_uint4(0, 0, 0, 0);
-        const std::uint32_t c0 = qcodes(w0), c1 = qcodes(w1), cx = qcodes(nx);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bars + 8 * (NST + k));  // this warp is done with the slot
-        std::uint32_t n0 = __shfl_down_sync(0xFFFFFFFFu, c0, 1), n1 = __shfl_down_sync(0xFFFFFFFFu, c1, 1);
-        const std::uint32_t first1 = __shfl_sync(0xFFFFFFFFu, c1, 0);
-        if (lane == 31) {
-            n0 = first1;
-            n1 = cx;
-        }
-        std::uint32_t t[8];
+
+    if (b0 < b1) {
 #pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            t[o] = probe(gram(c0, n0, o));
-            t[4 + o] = probe(gram(c1, n1, o));
-        }
-        const std::uint32_t z = min(min(min(t[0], t[1]), min(t[2], t[3])), min(min(t[4], t[5]), min(t[6], t[7])));
-        const long long P0 = (st0 + it) * kStage + blk + 16 * lane, P1 = P0 + 512;
-        const bool hit = z == 0u && P0 < n;
-        if (!__ballot_sync(0xFFFFFFFFu, hit)) continue;
-        // survivors -> the candidate list (warp-aggregated; rare)
-        std::uint32_t pm = 0;
-        if (hit) {
+        for (int k = 0; k < R; ++k) load(buf[k], b0 + k);
+        std::uint32_t cur[4];
 #pragma unroll
-            for (int o = 0; o < 8; ++o) pm |= (t[o] == 0u ? 1u : 0u) << o;
-            if (P1 >= n) pm &= 0xFu;
-        }
-        const std::uint32_t cnt = __popc(pm);
-        std::uint32_t incl = cnt;
+        for (int r = 0; r < 4; ++r) cur[r] = qcodes(buf[0][r]);
+        load(buf[0], b0 + R);
+        for (long long bb = b0; bb < b1; bb += R) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const std::uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        std::uint32_t slot = found + incl - cnt;
-        found += __shfl_sync(0xFFFFFFFFu, incl, 31);
-        for (std::uint32_t m = pm; m; m &= m - 1, ++slot) {
-            const int o = __ffs(m) - 1;
-            if (slot < a.qcand_cap) {
-                a.qcands[region + slot] = static_cast<unsigned long long>(o < 4 ? P0 + 4 * o : P1 + 4 * (o - 4));
-                a.qcand_code[region + slot] = o < 4 ? gram(c0, n0, o) : gram(c1, n1, o - 4);
+            for (int k = 0; k < R; ++k) {
+                const long long b = bb + k;
+                if (b >= b1) break;
+                const int sl = (k + 1) % R;  // slot holding block b+1
+                std::uint32_t nxt[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) nxt[r] = qcodes(buf[sl][r]);
+                load(buf[sl], b + 1 + R);
+                // neighbour codes: lane+1's word of the same row; lane 31 gets lane 0's next row
+                std::uint32_t nb_[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const std::uint32_t s = lane == 0 ? (r < 3 ? cur[r + 1] : nxt[0]) : cur[r];
+                    nb_[r] = __shfl_sync(0xFFFFFFFFu, s, (lane + 1) & 31);
+                }
+                std::uint32_t t[16];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int o = 0; o < 4; ++o) t[4 * r + o] = probe(gram(cur[r], nb_[r], o));
+                std::uint32_t z = min(min(t[0], t[1]), t[2]);
+                z = min(min(z, t[3]), t[4]);
+                z = min(min(z, t[5]), t[6]);
+                z = min(min(z, t[7]), t[8]);
+                z = min(min(z, t[9]), t[10]);
+                z = min(min(z, t[11]), t[12]);
+                z = min(min(z, t[13]), t[14]);
+                z = min(z, t[15]);
+                const bool hit = z == 0u;
+                if (__any_sync(0xFFFFFFFFu, hit) && hit) {
+                    std::uint32_t pm = 0;
+#pragma unroll
+                    for (int o = 0; o < 16; ++o) pm |= (t[o] == 0u ? 1u : 0u) << o;
+                    std::uint32_t slot = atomicAdd(&wcnt[warp], static_cast<std::uint32_t>(__popc(pm)));
+                    const long long P = b * kBlk + 16 * lane;
+                    for (std::uint32_t m = pm; m; m &= m - 1, ++slot) {
+                        const int i = __ffs(m) - 1, r = i >> 2, o = i & 3;
+                        const long long pos = P + 512 * r + 4 * o;
+                        if (pos < n && slot < a.qcand_cap) {
+                            std::uint32_t lo = cur[0], hi = nb_[0];
+                            if (r == 1) lo = cur[1], hi = nb_[1];
+                            if (r == 2) lo = cur[2], hi = nb_[2];
+                            if (r == 3) lo = cur[3], hi = nb_[3];
+                            a.qcands[region + slot] = static_cast<unsigned long long>(pos);
+                            a.qcand_code[region + slot] = gram(lo, hi, o);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
             }
         }
     }
+    __syncwarp();
     if (lane == 0) {
-        a.qwarp_n[blockIdx.x * NC + (warp - 1)] = found;
+        const std::uint32_t found = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
+        a.qwarp_n[gw] = found;
         atomicAdd(a.qcand_n, found);
         atomicMax(a.qcand_max, static_cast<unsigned long long>(found));
     }

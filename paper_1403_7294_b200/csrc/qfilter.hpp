@@ -33,7 +33,7 @@ constexpr std::uint32_t kQMaxQ = 16;    // q-gram length cap (32-bit codes)
 constexpr std::uint32_t kQMinQ = 10;    // below this the filter is not selective
 constexpr std::uint32_t kQBlock = 64;   // dirty-block size (bytes)
 constexpr std::uint32_t kQChunkBlocks = 128;  // blocks per output chunk (8 KiB)
-constexpr std::uint32_t kQWords = 45056;      // Bloom words (176 KiB of shared memory; the rest stages text)
+constexpr std::uint32_t kQWords = 57344;      // Bloom words (224 KiB: all of the opt-in shared memory but 3 KiB)
 constexpr std::uint32_t kQMul0 = 0x9E3779B1u, kQMul1 = 0x85EBCA77u, kQMul2 = 0xC2B2AE3Du;
 constexpr std::uint32_t kQEmpty = 0xFFFFFFFFu;  // exact-table slot marker
 
