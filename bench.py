@@ -40,7 +40,7 @@ HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json
 
 # per-stage labels of acg_scanner_kernel_ms by scan mode
 STAGES = {
-    "filter": ("KQ_filter", "V0_confirm", "K2_prefix", "K3_order", "K4_unused"),
+    "filter": ("KQ_filter", "V1_confirm", "unused", "unused", "ORDER"),
     "sparse": ("K1s_walk", "K1f_fixup", "K2_prefix", "K3_write", "K4_counts"),
     "exact": ("K1x_walk", "none", "K2_prefix", "K3_write", "K4_counts"),
 }
@@ -256,12 +256,15 @@ def main() -> None:
     ap.add_argument("--threads-per-block", type=int, default=0)
     ap.add_argument("--chunk-bytes", type=int, default=0)
     ap.add_argument("--profile-layout", action="store_true", help="profile-guided hot-state order")
+    ap.add_argument("--text-mib", type=int, default=0, help="experiments: scale the workload's text (MiB)")
     ap.add_argument("--mode", default="auto", choices=["auto", "sparse", "exact", "filter"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     from paper_1403_7294_b200 import synth
     w = synth.CONFIGS[args.config]
+    if args.text_mib:
+        w = w.scaled(args.text_mib << 20)
     concat, offs = synth.patterns(w)
 
     if args.impl == "reference":

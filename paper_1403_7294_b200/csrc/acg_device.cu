@@ -119,6 +119,16 @@ struct DevBuf {
         n = 0;
         const std::size_t cap = std::max<std::size_t>(want, 1);
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), st);
+        if (e == cudaErrorMemoryAllocation) {
+            // the pool keeps freed blocks: return the unused ones to the
+            // driver (after the frees completed) and try once more
+            cudaGetLastError();
+            cudaStreamSynchronize(st);
+            cudaStreamSynchronize(hk_stream(dev));
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+            e = cudaMallocAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), st);
+        }
         if (e == cudaSuccess) n = cap;
         else p = nullptr;
         return e;
@@ -237,11 +247,20 @@ struct acg_scanner {
     DevBuf<std::uint32_t> qcand_code, qwarp_n;
     DevBuf<std::uint32_t> qfill, qheavy;
     bool regrow = false;  // enqueue_write after a record-buffer regrowth
+    // filter mode region pipeline (V1 + ORDER): per-region counts, overflow
+    // scalars; qlegacy = replay through the per-chunk pipeline (a region held
+    // more matches than ORDER sorts); min_mcap = slab capacity after an overflow
+    DevBuf<std::uint32_t> qreg_n, qscal;
+    bool qlegacy = false;
+    std::uint32_t min_mcap = 0;
+    std::uint32_t last_mcap = 0;
+    unsigned long long task_regions = 0;  // sparse mode: fix-up task regions of the last run
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
     cudaEvent_t ev[6] = {};
     float kernel_ms[5] = {};
+    std::uint32_t ev_mask = 0x3F;  // events recorded by the last profiled run
 };
 
 namespace {
@@ -433,6 +452,8 @@ std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
 // Filter mode: KQ geometry.
+constexpr unsigned long long kTaskBudget = 48ull << 30;  // sparse fix-up task memory cap (bytes)
+
 // KQ geometry: NW warps per SM, R blocks in flight per warp. ACG_QKERNEL
 // picks another instantiation (experiments only).
 struct QKernelChoice {
@@ -482,7 +503,13 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     wa.records = want_list ? s->records.p : nullptr;
     wa.rec_cap = want_list ? s->records.n : 0;
     wa.visits = nullptr;  // both modes count visits in their count pass
-    if (s->mode_run == ACG_MODE_FILTER) {
+    if (s->mode_run == ACG_MODE_FILTER && !s->qlegacy) {  // region pipeline: ORDER again (slabs are intact)
+        ScanArgs oa = wa;
+        const std::uint32_t W = static_cast<std::uint32_t>(s->n_chunks);
+        acg::kern::qorder_region_kernel<<<(W + kQOrderWarps - 1) / kQOrderWarps, 32 * kQOrderWarps, 0, st>>>(
+            oa, s->chunk_offs.p);
+        ACG_CUDA(cudaGetLastError());
+    } else if (s->mode_run == ACG_MODE_FILTER) {
         // records into their chunk's slots: from the scratch list, or (record
         // buffer regrown) by confirming the survivors again
         ACG_CUDA(cudaMemsetAsync(s->qfill.p, 0, s->n_chunks * sizeof(std::uint32_t), st));
@@ -527,6 +554,14 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     const DeviceDfa& dd = *s->dd;
     const unsigned long long streams = static_cast<unsigned long long>(dd.num_sms) * s->tpb_run * s->U_run;
     const unsigned long long halo = dd.dfa->halo;
+    if (s->mode_run == ACG_MODE_FILTER && !s->qlegacy) {  // output regions = KQ warp regions
+        const unsigned long long tw = static_cast<unsigned long long>(dd.num_sms) * qfilter_warps();
+        const unsigned long long nb = (s->run_n + 2047) / 2048;
+        s->chunk = std::max<unsigned long long>(1, (nb + tw - 1) / tw) * 2048;
+        s->n_chunks = owned ? tw : 0;
+        s->grid = static_cast<unsigned>(dd.num_sms);
+        return;
+    }
     if (s->mode_run == ACG_MODE_FILTER) {  // fixed 8 KiB chunks of 128 dirty-bit blocks
         s->chunk = static_cast<unsigned long long>(acg::kQChunkBlocks) * acg::kQBlock;
         s->n_chunks = (owned + s->chunk - 1) / s->chunk;
@@ -661,9 +696,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
 
     // K1: count pass
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[0], st));
+    s->ev_mask = 0x3F;
     if (mode == ACG_MODE_FILTER) {
-        ACG_CUDA(cudaMemsetAsync(s->chunk_counts.p, 0, s->n_chunks * sizeof(unsigned long long), st));
-        ACG_CUDA(s->qfill.reserve(s->n_chunks, st));
+        if (s->qlegacy) {
+            ACG_CUDA(cudaMemsetAsync(s->chunk_counts.p, 0, s->n_chunks * sizeof(unsigned long long), st));
+            ACG_CUDA(s->qfill.reserve(s->n_chunks, st));
+        }
         a.qbloom = dd.qbloom.p;
         a.qtab = dd.qtab.p;
         a.qtab_bits = d.qtab_bits;
@@ -676,7 +714,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.max_len = d.max_len;
         a.pcounts = want_counts ? s->counts.p : nullptr;
         a.qfill = s->qfill.p;
-        if (want_list) {
+        if (want_list && s->qlegacy) {
             ACG_CUDA(s->qscratch.reserve(s->records.n, st));
             a.qscratch = s->qscratch.p;
             a.qscratch_n = s->scalars64.p + 5;
@@ -704,6 +742,36 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 3, 0, sizeof(std::uint32_t), st));
         ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 6, 0, sizeof(unsigned long long), st));
         ACG_CUDA(cudaMemsetAsync(s->qwarp_n.p, 0, warps * sizeof(std::uint32_t), st));
+        if (!s->qlegacy) {  // region pipeline: KQ -> V1 -> ORDER
+            const std::uint32_t W = static_cast<std::uint32_t>(s->n_chunks);
+            const std::uint32_t mcap = std::max<std::uint32_t>(64, s->min_mcap);
+            s->last_mcap = mcap;
+            ACG_CUDA(s->qscratch.reserve(static_cast<std::size_t>(W) * mcap, st));
+            ACG_CUDA(s->qreg_n.reserve(2ull * W, st));
+            ACG_CUDA(s->qscal.reserve(2, st));
+            ACG_CUDA(cudaMemsetAsync(s->qscal.p, 0, 2 * sizeof(std::uint32_t), st));
+            a.qscratch = s->qscratch.p;
+            a.mcap = mcap;
+            a.qreg = static_cast<long long>(s->chunk);
+            a.reg_n = s->qreg_n.p;
+            a.reg_hi = s->qreg_n.p + W;
+            a.qscal = s->qscal.p;
+            ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
+            if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+            qconfirm_region_kernel<<<8 * dd.num_sms, 256, 0, st>>>(a);
+            ACG_CUDA(cudaGetLastError());
+            if (prof) ACG_CUDA(cudaEventRecord(s->ev[2], st));
+            ScanArgs oa = a;
+            oa.records = want_list ? s->records.p : nullptr;
+            oa.rec_cap = want_list ? s->records.n : 0;
+            qorder_region_kernel<<<(W + kQOrderWarps - 1) / kQOrderWarps, 32 * kQOrderWarps, 0, st>>>(oa, s->chunk_offs.p);
+            ACG_CUDA(cudaGetLastError());
+            if (prof) ACG_CUDA(cudaEventRecord(s->ev[5], st));
+            s->ev_mask = 0x27;  // events 0, 1, 2, 5 (stages KQ, V1, ORDER)
+            s->launches += 3;
+            s->have_run = true;
+            return ACG_OK;
+        }
         ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
@@ -730,6 +798,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         const unsigned long long walked = s->n_chunks * walk;
         const double rate = s->last_event_rate > 0 ? s->last_event_rate : 1.0 / 16;
         const unsigned long long regions = fixup_rewalk_grid(n_warps, dd.num_sms) * 32ull;
+        s->task_regions = regions;
         unsigned long long rcap = static_cast<unsigned long long>(walked * std::min(1.0, rate * 3.0) / regions) + 1024;
         rcap = std::max(rcap, s->min_task_cap);
         rcap = std::min<unsigned long long>(rcap, 0x7FFFFFFFull);
@@ -799,8 +868,35 @@ int scanner_sync(acg_scanner* s) {
         const std::uint32_t ntask = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[1];
         if (ntask > s->args.task_cap) {  // a task region overflowed: grow and run again
             s->min_task_cap = ntask + ntask / 4 + 1024;
+            // excursions this frequent make the exact walk the better mode; it
+            // also needs no task memory (which would be regions x the worst
+            // region's tasks): re-run exactly instead of growing past a budget
+            const double need = static_cast<double>(s->task_regions) * s->min_task_cap * 16.0;
+            const bool go_exact = need > static_cast<double>(kTaskBudget);
             const int req = s->mode_req;
-            s->mode_req = ACG_MODE_SPARSE;
+            s->mode_req = go_exact ? ACG_MODE_EXACT : ACG_MODE_SPARSE;
+            if (go_exact) {
+                s->min_task_cap = 0;
+                s->last_event_rate = 1.0;  // AUTO: exact from now on
+            }
+            const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
+            s->mode_req = req;
+            if (rc) return rc;
+            return scanner_sync(s);
+        }
+    }
+    if (s->mode_run == ACG_MODE_FILTER && s->n_chunks && !s->qlegacy) {
+        ACG_CUDA(cudaMemcpyAsync(s->pinned + 1, s->qscal.p, 2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+        ACG_CUDA(cudaStreamSynchronize(st));
+        const std::uint32_t* qs = reinterpret_cast<const std::uint32_t*>(s->pinned + 1);
+        const std::uint32_t slab_max = qs[0], too_big = qs[1];
+        if (s->pinned[4] <= s->args.qcand_cap && (slab_max > s->last_mcap || too_big)) {
+            // a region's slab overflowed (grow it) or held more than ORDER sorts
+            // (replay through the per-chunk pipeline from now on): run again
+            if (too_big) s->qlegacy = true;
+            else s->min_mcap = slab_max + slab_max / 4 + 32;
+            const int req = s->mode_req;
+            s->mode_req = ACG_MODE_FILTER;
             const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
             s->mode_req = req;
             if (rc) return rc;
@@ -837,7 +933,14 @@ int scanner_sync(acg_scanner* s) {
         ACG_CUDA(cudaStreamSynchronize(st));
     }
     if ((s->flags & ACG_SCAN_PROFILE) && s->n_chunks) {
-        for (int i = 0; i < 5; ++i) ACG_CUDA(cudaEventElapsedTime(&s->kernel_ms[i], s->ev[i], s->ev[i + 1]));
+        // stage i-1 = time from the previous recorded event to event i
+        int prev = 0;
+        for (int i = 1; i < 6; ++i) {
+            s->kernel_ms[i - 1] = 0.f;
+            if (!(s->ev_mask >> i & 1)) continue;
+            ACG_CUDA(cudaEventElapsedTime(&s->kernel_ms[i - 1], s->ev[prev], s->ev[i]));
+            prev = i;
+        }
     }
     s->synced = true;
     return ACG_OK;

@@ -262,8 +262,8 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
     for (std::size_t i = 0; i < grams.size(); ++i) {
         if (i && grams[i].first == grams[i - 1].first) continue;
         ++keys;
-        const std::uint32_t y = qtop(grams[i].first, q);
-        d.qbloom[qword(y, words)] |= qmask(y);
+        const std::uint32_t h = qhash(qtop(grams[i].first, q));
+        d.qbloom[qword(h, words)] |= qmask(h);
     }
     d.qtab_bits = 10;
     while ((1u << d.qtab_bits) < 2u * keys) ++d.qtab_bits;
@@ -290,9 +290,9 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         r = (r ^ (r >> 30)) * 0xBF58476D1CE4E5B9ull;
         r = (r ^ (r >> 27)) * 0x94D049BB133111EBull;
         const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
-        const std::uint32_t y = qtop(c, q);
-        const std::uint32_t m = qmask(y);
-        pass += (d.qbloom[qword(y, words)] & m) == m;
+        const std::uint32_t h = qhash(qtop(c, q));
+        const std::uint32_t m = qmask(h);
+        pass += (d.qbloom[qword(h, words)] & m) == m;
     }
     d.filter_fp = static_cast<double>(pass) / trials;
     // worth it when few samples survive (each survivor costs an exact probe)

@@ -83,24 +83,38 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
     const unsigned long long region = static_cast<unsigned long long>(gw) * a.qcand_cap;
 
     uint4 buf[R][4];
-    auto load = [&](uint4 (&dst)[4], long long b) {
-        const long long off = b * kBlk + 16 * lane;
+    // blocks are loaded in order b0, b0+1, ...: a running pointer, and bounds
+    // checks only for the text's last (partial) block
+    const long long nfull = n / kBlk;
+    const std::uint8_t* lp = a.text + b0 * kBlk + 16 * lane;
+    long long lb = b0;
+    auto load = [&](uint4 (&dst)[4]) {
+        if (lb < nfull) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-            dst[r] = (b < nb && off + 512 * r < n) ? ldg_stream(a.text + off + 512 * r) : make_uint4(0, 0, 0, 0);
+            for (int r = 0; r < 4; ++r) dst[r] = ldg_stream(lp + 512 * r);
+        } else {
+            const long long off = lb * kBlk + 16 * lane;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                dst[r] = (lb < nb && off + 512 * r < n) ? ldg_stream(lp + 512 * r) : make_uint4(0, 0, 0, 0);
+        }
+        lp += kBlk;
+        ++lb;
     };
-    auto probe = [&](std::uint32_t y) -> std::uint32_t { return qmask(y) & ~tab[qword(y, words)]; };
-    auto gram = [&](std::uint32_t lo, std::uint32_t hi, int o) -> std::uint32_t {
-        return (o == 0 ? lo : __funnelshift_r(lo, hi, 8 * o)) * qsh;
+    const std::uint32_t qmul = qsh * kQMul0;  // window -> hash in one multiply (qfilter.hpp)
+    auto probe = [&](std::uint32_t h) -> std::uint32_t { return qmask(h) & ~tab[qword(h, words)]; };
+    auto window = [&](std::uint32_t lo, std::uint32_t hi, int o) -> std::uint32_t {
+        return o == 0 ? lo : __funnelshift_r(lo, hi, 8 * o);
     };
+    auto gram = [&](std::uint32_t lo, std::uint32_t hi, int o) -> std::uint32_t { return window(lo, hi, o) * qsh; };
 
     if (b0 < b1) {
 #pragma unroll
-        for (int k = 0; k < R; ++k) load(buf[k], b0 + k);
+        for (int k = 0; k < R; ++k) load(buf[k]);
         std::uint32_t cur[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) cur[r] = qcodes(buf[0][r]);
-        load(buf[0], b0 + R);
+        load(buf[0]);
         for (long long bb = b0; bb < b1; bb += R) {
 #pragma unroll
             for (int k = 0; k < R; ++k) {
@@ -110,7 +124,7 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
                 std::uint32_t nxt[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) nxt[r] = qcodes(buf[sl][r]);
-                load(buf[sl], b + 1 + R);
+                load(buf[sl]);  // block b + 1 + R
                 // neighbour codes: lane+1's word of the same row; lane 31 gets lane 0's next row
                 std::uint32_t nb_[4];
 #pragma unroll
@@ -122,7 +136,7 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
 #pragma unroll
-                    for (int o = 0; o < 4; ++o) t[4 * r + o] = probe(gram(cur[r], nb_[r], o));
+                    for (int o = 0; o < 4; ++o) t[4 * r + o] = probe(window(cur[r], nb_[r], o) * qmul);
                 std::uint32_t z = min(min(t[0], t[1]), t[2]);
                 z = min(min(z, t[3]), t[4]);
                 z = min(min(z, t[5]), t[6]);
@@ -160,9 +174,179 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
     if (lane == 0) {
         const std::uint32_t found = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
         a.qwarp_n[gw] = found;
+        if (a.reg_n) a.reg_n[gw] = a.reg_hi[gw] = 0u;  // V1's per-region counters
         atomicAdd(a.qcand_n, found);
         atomicMax(a.qcand_max, static_cast<unsigned long long>(found));
     }
+}
+
+__device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, v, stride);
+            const bool up = (lane & size) == 0;     // this lane's run ascends
+            const bool low = (lane & stride) == 0;  // lower element of its pair
+            v = (low == up) ? min(v, o) : max(v, o);
+        }
+    }
+    return v;
+}
+
+// Exact check of pattern p (bytes [lo, lo+len) of the dictionary) against
+// text[i, i+len): 16 independent byte pairs per round, so a match costs
+// ceil(len/16) dependent memory round trips rather than len.
+__device__ __forceinline__ bool qmatch(const ScanArgs& a, long long i, std::uint32_t lo, std::uint32_t len) {
+    for (std::uint32_t k0 = 0; k0 < len; k0 += 16) {
+        std::uint32_t diff = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k0 + k < len) diff |= static_cast<std::uint32_t>(__ldg(a.text + i + k0 + k) ^ __ldg(a.pat_bytes + lo + k0 + k));
+        if (diff) return false;
+    }
+    return true;
+}
+
+// V1: confirms every survivor exactly (the q-gram's (pattern, offset)
+// bucket, then a byte compare at i = j - offset); threads stride over the
+// survivor regions' slots. A match found from region w's survivors ends in
+// w or, at most 63 bytes on, in w + 1 (reg_hi counts those); it is appended
+// to w's slab (reg_n[w], zeroed by KQ, counts them even past the capacity).
+__global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) {
+    const std::uint32_t tmask = (1u << a.qtab_bits) - 1u;
+    const long long total = static_cast<long long>(a.qwarps) * a.qcand_cap;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long w = t / a.qcand_cap;
+        if (static_cast<std::uint32_t>(t - w * a.qcand_cap) >= a.qwarp_n[w]) continue;
+        const long long j = static_cast<long long>(a.qcands[t]);
+        const std::uint32_t code = a.q >= 16 ? a.qcand_code[t] : a.qcand_code[t] >> (32 - 2 * a.q);
+        std::uint32_t slot = qslot(code, a.qtab_bits), bucket = kQEmpty;
+        for (;;) {
+            const uint2 e = *reinterpret_cast<const uint2*>(a.qtab + 2 * slot);
+            if (e.y == kQEmpty) break;
+            if (e.x == code) {
+                bucket = e.y;
+                break;
+            }
+            slot = (slot + 1) & tmask;
+        }
+        if (bucket == kQEmpty) continue;
+        const long long rend = (w + 1) * a.qreg;
+        for (std::uint32_t e = a.qb_off[bucket]; e < a.qb_off[bucket + 1]; ++e) {
+            const std::uint32_t ent = a.qb_ent[e];
+            const long long i = j - static_cast<long long>(ent & 3u);
+            const std::uint32_t p = ent >> 2;
+            const std::uint32_t lo = a.pat_off[p], len = a.pat_off[p + 1] - lo;
+            if (i < 0 || i + len > a.n) continue;
+            const long long end = i + len - 1;
+            if (end < a.emit_from) continue;
+            // pre-check two bytes outside the matched q-gram (random text passes
+            // 1 in 16), then the whole pattern
+            const std::uint32_t o = ent & 3u, k1 = o + a.q < len ? o + a.q : 0u, k2 = o ? o - 1u : len - 1u;
+            const bool pre = (__ldg(a.text + i + k1) == __ldg(a.pat_bytes + lo + k1)) &
+                             (__ldg(a.text + i + k2) == __ldg(a.pat_bytes + lo + k2));
+            if (!pre || !qmatch(a, i, lo, len)) continue;
+            const std::uint32_t k = atomicAdd(a.reg_n + w, 1u);
+            if (k < a.mcap)
+                a.qscratch[static_cast<unsigned long long>(w) * a.mcap + k] =
+                    ((a.base + static_cast<unsigned long long>(end)) << a.id_bits) | p;
+            if (end >= rend) atomicAdd(a.reg_hi + w, 1u);
+            if (a.pcounts) atomicAdd(a.pcounts + p, 1ull);
+        }
+    }
+}
+
+// ORDER: one warp per region. Its slot range starts at the sum of the
+// matches owned by earlier regions (summed directly from reg_n / reg_hi: no
+// separate scan pass); it gathers its matches (its own slab's entries ending
+// in it, the previous slab's ending past that region) and sorts them: one
+// bitonic round in registers for <= 32, a warp bitonic sort in shared memory
+// for <= kQOrderMax; a bigger region sets qscal[1] and the host replays the
+// run through the per-chunk pipeline (V0/K2/K3).
+constexpr int kQOrderMax = 1024;
+constexpr int kQOrderWarps = 4;
+
+__global__ void __launch_bounds__(32 * kQOrderWarps) qorder_region_kernel(const ScanArgs a, unsigned long long* offs) {
+    __shared__ unsigned long long buf[kQOrderWarps][kQOrderMax];
+    const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long w = static_cast<long long>(blockIdx.x) * kQOrderWarps + wl;
+    if (w >= a.qwarps) return;
+    const long long W = a.qwarps;
+    unsigned long long sum = 0;
+    for (long long v = lane; v < w; v += 32) sum += a.reg_n[v];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    const std::uint32_t hprev = w > 0 ? a.reg_hi[w - 1] : 0u;
+    const std::uint32_t nw = min(a.reg_n[w], a.mcap), np = w > 0 ? min(a.reg_n[w - 1], a.mcap) : 0u;
+    const unsigned long long off = sum - hprev;
+    const std::uint32_t own = a.reg_n[w] - a.reg_hi[w] + hprev;
+    if (lane == 0) {
+        if (a.reg_n[w] > a.mcap) atomicMax(a.qscal, a.reg_n[w]);  // slab overflow: the host re-runs
+        offs[w] = off;
+        if (w == W - 1) offs[W] = off + own;
+    }
+    if (own == 0) return;
+    if (own > static_cast<std::uint32_t>(kQOrderMax)) {
+        if (lane == 0) atomicMax(a.qscal + 1, own);
+        return;
+    }
+    const long long rlo = w * a.qreg, rhi = rlo + a.qreg;
+    const unsigned long long* sw = a.qscratch + static_cast<unsigned long long>(w) * a.mcap;
+    const unsigned long long* sp = sw - a.mcap;
+    unsigned long long* b = buf[wl];
+    const unsigned lt = (1u << lane) - 1u;
+    std::uint32_t pos = 0;
+    auto gather = [&](const unsigned long long* src, std::uint32_t cntv, bool own_slab) {
+        for (std::uint32_t base = 0; base < cntv; base += 32) {
+            const std::uint32_t idx = base + lane;
+            unsigned long long key = 0;
+            bool take = false;
+            if (idx < cntv) {
+                key = src[idx];
+                const long long end = static_cast<long long>((key >> a.id_bits) - a.base);
+                take = own_slab ? end < rhi : end >= rlo;
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
+            if (take) {
+                const std::uint32_t at = pos + __popc(m & lt);
+                if (at < static_cast<std::uint32_t>(kQOrderMax)) b[at] = key;
+            }
+            pos += __popc(m);
+        }
+    };
+    if (w > 0 && hprev) gather(sp, np, false);
+    gather(sw, nw, true);
+    __syncwarp();
+    const std::uint32_t k = min(pos, static_cast<std::uint32_t>(kQOrderMax));
+    if (k <= 32) {
+        unsigned long long v = lane < static_cast<int>(k) ? b[lane] : ~0ull;
+        v = bitonic32(v, lane);
+        if (lane < static_cast<int>(k) && off + lane < a.rec_cap) a.records[off + lane] = v;
+        return;
+    }
+    std::uint32_t p2 = 64;
+    while (p2 < k) p2 <<= 1;
+    for (std::uint32_t t = k + lane; t < p2; t += 32) b[t] = ~0ull;
+    __syncwarp();
+    for (std::uint32_t size = 2; size <= p2; size <<= 1) {
+        for (std::uint32_t stride = size >> 1; stride; stride >>= 1) {
+            for (std::uint32_t t = lane; t < p2 / 2; t += 32) {
+                const std::uint32_t i = 2 * t - (t & (stride - 1));  // lower index of the pair
+                const std::uint32_t jj = i + stride;
+                const bool up = (i & size) == 0;
+                const unsigned long long x = b[i], y = b[jj];
+                if ((x > y) == up) {
+                    b[i] = y;
+                    b[jj] = x;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    for (std::uint32_t t = lane; t < k; t += 32)
+        if (off + t < a.rec_cap) a.records[off + t] = b[t];
 }
 
 // V0: exact confirmation of the survivors (see the header comment).
@@ -232,20 +416,6 @@ __global__ void __launch_bounds__(256) qscatter_kernel(const ScanArgs a) {
 // bigger chunks go to the heavy list (qheavy_kernel). Warps sweep the chunk
 // offsets directly (no compacted list: its single counter would serialise
 // thousands of same-address atomics).
-__device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, int lane) {
-#pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, v, stride);
-            const bool up = (lane & size) == 0;     // this lane's run ascends
-            const bool low = (lane & stride) == 0;  // lower element of its pair
-            v = (low == up) ? min(v, o) : max(v, o);
-        }
-    }
-    return v;
-}
-
 __global__ void __launch_bounds__(256) qsort_chunks_kernel(const ScanArgs a, std::uint32_t* heavy,
                                                            std::uint32_t* n_heavy) {
     const int lane = threadIdx.x & 31;

@@ -63,13 +63,16 @@ ACG_HD std::uint32_t qperm(std::uint32_t x, std::uint32_t y, std::uint32_t sel) 
 }
 
 // Bloom probe of a q-gram given as y = code << (32 - 2q) (the code in the
-// top bits: the device gets y from an unmasked 32-bit window with one
-// multiply, which also drops the bases past the q-gram). qword: the word
-// index; qmask: four bits, one in each byte of the word (bit (sel_i & 7) of
-// byte i, sel from an independent hash) — one PRMT builds it.
-ACG_HD std::uint32_t qword(std::uint32_t y, std::uint32_t words) { return qmulhi(y * kQMul0, words); }
-ACG_HD std::uint32_t qmask(std::uint32_t y) {
-    return qperm(0x08040201u, 0x80402010u, qmulhi(y, kQMul1) & 0x7777u);
+// top bits). Both parts come from one multiplicative hash h = y * kQMul0 —
+// on the device h = window * (2^(32-2q) * kQMul0), one multiply from the
+// unmasked 32-bit window, since the bases past the q-gram fall off the top.
+// qword: the word index (h's high bits scaled to the table); qmask: four
+// bits, one in each byte of the word (bit (sel_i & 7) of byte i, sel from
+// the high half of h * kQMul1, independent of the word index) — one PRMT.
+ACG_HD std::uint32_t qhash(std::uint32_t y) { return y * kQMul0; }
+ACG_HD std::uint32_t qword(std::uint32_t h, std::uint32_t words) { return qmulhi(h, words); }
+ACG_HD std::uint32_t qmask(std::uint32_t h) {
+    return qperm(0x08040201u, 0x80402010u, qmulhi(h, kQMul1) & 0x7777u);
 }
 ACG_HD std::uint32_t qtop(std::uint32_t code, std::uint32_t q) { return q >= 16 ? code : code << (32 - 2 * q); }
 // Exact table slot of code c in a table of 2^bits slots.

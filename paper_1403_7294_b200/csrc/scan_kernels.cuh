@@ -118,6 +118,13 @@ struct ScanArgs {
     std::uint32_t q;                        // q-gram length
     std::uint32_t qsh;                      // 2^(32 - 2q): window * qsh puts the q-gram code in the top bits
     std::uint32_t max_len;                  // longest pattern
+    // filter mode, region pipeline (V1 + ORDER): KQ warp w's region of the
+    // buffer [w*qreg, (w+1)*qreg) owns the matches that END in it
+    long long qreg;                         // region bytes (multiple of 2048)
+    std::uint32_t* reg_n;                   // per region: matches confirmed from its survivors
+    std::uint32_t* reg_hi;                  // ... of which end in the next region
+    std::uint32_t mcap;                     // per-region slab capacity (qscratch)
+    std::uint32_t* qscal;                   // [0] max reg_n (overflow), [1] regions too big for ORDER
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {

@@ -161,3 +161,30 @@ def test_auto_picks_filter_for_cfg1():
     s.run_host(synth.text(w))
     s.sync()
     assert s.last_mode()[0] == "filter"
+
+
+def test_filter_region_sort_paths():
+    """Per-region match counts across ORDER's paths: a bitonic round in
+    registers (<= 32 per region) and the warp sort in shared memory (33..1024),
+    with matches straddling region boundaries (owned by the next region)."""
+    rng = np.random.default_rng(21)
+    words = sorted({rand_dna(rng, int(rng.integers(16, 30))).tobytes() for _ in range(40)})
+    text = rand_dna(rng, 1 << 20)
+    p = 0
+    while p < text.size - 64:
+        w = words[int(rng.integers(0, len(words)))]
+        text[p:p + len(w)] = np.frombuffer(w, np.uint8)
+        # dense (about 60 per 2 KiB region) in the first half, sparse after
+        p += int(rng.integers(len(w), 48)) if p < text.size // 2 else int(rng.integers(200, 900))
+    m = run_filter(words, text)
+    assert m > 10000
+
+
+def test_filter_region_too_dense_replays_chunk_pipeline():
+    """A homopolymer run gives every region > 1024 matches: the scanner
+    replays the run through the per-chunk pipeline, with the same result."""
+    rng = np.random.default_rng(22)
+    words = [b"A" * 16, b"A" * 24] + [rand_dna(rng, 20).tobytes() for _ in range(10)]
+    text = rand_dna(rng, 1 << 20)
+    text[100_000:300_000] = ord("A")
+    run_filter(words, text)
