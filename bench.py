@@ -352,9 +352,12 @@ def main() -> None:
     # correctness of the timed run (size-independent properties)
     dsum, dxor, unsorted = sc.digest()
     counts_local = sc.pattern_counts()
+    mode_req = {"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT, "filter": am.MODE_FILTER}[args.mode]
+    sc.__del__()  # release the timed scanner's workspace before the e2e scanner allocates its own
 
     # e2e: the public scanner API from pinned host memory, H2D + D2H inside
     sc_e2e = am.Scanner(a, local, am.SCAN_LIST | am.SCAN_COUNTS)
+    sc_e2e.set_mode(mode_req)
     h_counts = np.empty(P, dtype=np.uint64)
     for _ in range(1):
         sc_e2e.run_host_ptr(h_text.data_ptr(), h_text.numel())

@@ -164,6 +164,7 @@ struct DeviceDfa {
     DevBuf<std::uint16_t> hot16, hotH, follows, follows_esc;
     DevBuf<std::uint8_t> symmap;
     DevBuf<std::uint32_t> qbloom;  // filter mode: kQWords Bloom words
+    DevBuf<std::uint32_t> qbloom2;  // level-2 filter (large dictionaries)
     DevBuf<std::uint32_t> qtab, qb_off, qb_ent, pat_off;  // filter mode: exact q-gram table, patterns
     DevBuf<std::uint8_t> pat_bytes;
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
@@ -255,6 +256,11 @@ struct acg_scanner {
     std::uint32_t min_mcap = 0;
     std::uint32_t last_mcap = 0;
     unsigned long long task_regions = 0;  // sparse mode: fix-up task regions of the last run
+    // exact mode: records per owned byte of the last exact run (-1 = unknown);
+    // scratch_run = the last run used the single-pass slabs
+    double exact_density = -1.0;
+    bool scratch_run = false;
+    DevBuf<unsigned long long> scratch;
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
@@ -327,6 +333,7 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
     }
     if (d.filter_ok) {
         ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size(), up));
+        if (!d.qbloom2.empty()) ACG_CUDA(upload(dd->qbloom2, d.qbloom2.data(), d.qbloom2.size(), up));
         ACG_CUDA(upload(dd->qtab, d.qtab.data(), d.qtab.size(), up));
         ACG_CUDA(upload(dd->qb_off, d.qb_off.data(), d.qb_off.size(), up));
         ACG_CUDA(upload(dd->qb_ent, d.qb_ent.data(), d.qb_ent.size(), up));
@@ -385,10 +392,12 @@ cudaError_t launch_exact_pass(int alpha, int pass, bool stats, std::uint32_t U, 
         return alpha == acg::kAlphaDna4 ? launch_exact<2, 0, kCount, true>(args, grid, tpb, smem, st)
                                         : launch_exact<2, 1, kCount, true>(args, grid, tpb, smem, st);
     if (alpha == acg::kAlphaDna4)
-        return pass == kCount ? launch_exact_u<0, kCount>(U, args, grid, tpb, smem, st)
-                              : launch_exact_u<0, kWrite>(U, args, grid, tpb, smem, st);
-    return pass == kCount ? launch_exact_u<1, kCount>(U, args, grid, tpb, smem, st)
-                          : launch_exact_u<1, kWrite>(U, args, grid, tpb, smem, st);
+        return pass == kCount   ? launch_exact_u<0, kCount>(U, args, grid, tpb, smem, st)
+               : pass == kWrite ? launch_exact_u<0, kWrite>(U, args, grid, tpb, smem, st)
+                                : launch_exact_u<0, kScratch>(U, args, grid, tpb, smem, st);
+    return pass == kCount   ? launch_exact_u<1, kCount>(U, args, grid, tpb, smem, st)
+           : pass == kWrite ? launch_exact_u<1, kWrite>(U, args, grid, tpb, smem, st)
+                            : launch_exact_u<1, kScratch>(U, args, grid, tpb, smem, st);
 }
 
 constexpr unsigned sparse_tpb(unsigned U) { return U == 1 ? 1024u : 512u; }
@@ -452,7 +461,9 @@ std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
 // Filter mode: KQ geometry.
-constexpr unsigned long long kTaskBudget = 48ull << 30;  // sparse fix-up task memory cap (bytes)
+constexpr unsigned long long kTaskBudget = 48ull << 30;
+constexpr double kSparseMaxEventRate = 0.005;  // AUTO: sparse mode below this event rate
+constexpr unsigned long long kScratchBudget = 24ull << 30;  // exact-mode single-pass slabs (bytes)  // sparse fix-up task memory cap (bytes)
 
 // KQ geometry: NW warps per SM, R blocks in flight per warp. ACG_QKERNEL
 // picks another instantiation (experiments only).
@@ -481,9 +492,10 @@ cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
     using namespace acg::kern;
     const QKernelChoice c = qfilter_choice();
     const std::size_t bloom = static_cast<std::size_t>(a.qwords) * 4;
-    if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2>, a, 32 * 24, bloom, sms, st);
-    if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3>, a, 32 * 16, bloom, sms, st);
-    return launch_q(qfilter_ldg_kernel<16, 2>, a, 32 * 16, bloom, sms, st);
+    if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true>, a, 32 * 16, bloom, sms, st);
+    if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2, false>, a, 32 * 24, bloom, sms, st);
+    if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3, false>, a, 32 * 16, bloom, sms, st);
+    return launch_q(qfilter_ldg_kernel<16, 2, false>, a, 32 * 16, bloom, sms, st);
 }
 
 // Enqueue K3 (compaction + ordered write) for the current geometry.
@@ -491,7 +503,7 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     using namespace acg::kern;
     const DeviceDfa& dd = *s->dd;
     ACG_CUDA(cudaMemsetAsync(s->scalars32.p, 0, sizeof(std::uint32_t), st));
-    if (s->mode_run != ACG_MODE_FILTER) {  // (filter mode sweeps the chunk offsets itself)
+    if (s->mode_run != ACG_MODE_FILTER && !s->scratch_run) {  // (filter mode sweeps the chunk offsets itself)
         const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((s->n_chunks + 2047) / 2048, 1024ull));
         compact_active_kernel<<<std::max(g, 1u), 256, 0, st>>>(s->chunk_counts.p, static_cast<long long>(s->n_chunks),
                                                                s->active_list.p, s->scalars32.p);
@@ -541,6 +553,14 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
             1, std::min<unsigned long long>((s->n_chunks + 255) / 256, static_cast<unsigned long long>(dd.num_sms))));
         k<<<g, 256, smem_sparse(dd), st>>>(wa);
         ACG_CUDA(cudaGetLastError());
+    } else if (s->scratch_run) {
+        // slabs -> slot ranges; overflowed chunks are re-walked by the WRITE pass
+        const unsigned g = static_cast<unsigned>(
+            std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 16ull * dd.num_sms)));
+        acg::kern::scratch_copy_kernel<<<g, 256, 0, st>>>(wa, s->active_list.p, s->scalars32.p);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+        ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
     } else {
         ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
     }
@@ -612,6 +632,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     const bool want_counts = s->flags & ACG_SCAN_COUNTS;
     const bool stats = s->flags & ACG_SCAN_STATS;
     s->launches = 0;
+    s->scratch_run = false;
     s->synced = false;
     s->last = st;
     s->run_text = d_text;
@@ -628,7 +649,10 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         mode = ACG_MODE_FILTER;
     if (stats || (mode != ACG_MODE_FILTER && !d.sparse_ok)) mode = ACG_MODE_EXACT;
     if (mode == ACG_MODE_AUTO)
-        mode = (s->last_event_rate < 0 || s->last_event_rate < 0.08) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
+        // measured on the BASELINE configs: sparse wins at 8.5e-4 events per walked
+        // byte (cfg0: 3x faster than exact) and loses badly at 0.025 (cfg4) and
+        // 0.0625 (cfg2: fix-up replay dominates)
+        mode = (s->last_event_rate < 0 || s->last_event_rate < kSparseMaxEventRate) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
     s->mode_run = mode;
     s->U_run = stats ? 2u : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 1u : 4u));
     if (mode == ACG_MODE_SPARSE && s->U_run > 4) s->U_run = 4;
@@ -736,6 +760,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.qwarp_n = s->qwarp_n.p;
         a.qwarps = static_cast<std::uint32_t>(warps);
         a.qwords = static_cast<std::uint32_t>(d.qbloom.size());
+        a.qbloom2 = d.qbloom2.empty() ? nullptr : dd.qbloom2.p;
+        a.qwords2 = static_cast<std::uint32_t>(d.qbloom2.size());
         a.qcand_cap = static_cast<std::uint32_t>(cap);
         a.qcand_n = s->scalars32.p + 3;
         a.qcand_max = s->scalars64.p + 6;
@@ -821,7 +847,20 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         ACG_CUDA(launch_fixup(s->U_run, a, smem_sparse(dd), dd.num_sms, st));
         s->launches += 3;
     } else {
-        ACG_CUDA(launch_exact_pass(d.mode, kCount, stats, s->U_run, a, s->grid, s->tpb, smem_bytes(dd), st));
+        // single pass (count + per-chunk slabs) once the previous run told the
+        // record density and the slabs fit the budget; count + write otherwise
+        if (want_list && !stats && s->exact_density >= 0) {
+            const unsigned long long scap =
+                static_cast<unsigned long long>(s->exact_density * 1.25 * static_cast<double>(s->chunk)) + 32;
+            if (static_cast<double>(scap) * s->n_chunks * 8.0 <= static_cast<double>(kScratchBudget)) {
+                ACG_CUDA(s->scratch.reserve(scap * s->n_chunks, st));
+                a.scratch = s->scratch.p;
+                a.scap = scap;
+                s->scratch_run = true;
+            }
+        }
+        ACG_CUDA(launch_exact_pass(d.mode, s->scratch_run ? kScratch : kCount, stats, s->U_run, a, s->grid, s->tpb,
+                                   smem_bytes(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
     }
@@ -916,6 +955,8 @@ int scanner_sync(acg_scanner* s) {
         }
     }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
+    if (s->mode_run == ACG_MODE_EXACT && s->run_n > s->run_emit)
+        s->exact_density = static_cast<double>(s->m_total) / static_cast<double>(s->run_n - s->run_emit);
     if (s->mode_run == ACG_MODE_FILTER && s->run_n)
         s->last_filter_rate = static_cast<double>(reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[3]) /
                               static_cast<double>(s->run_n);

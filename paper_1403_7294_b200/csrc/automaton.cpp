@@ -232,6 +232,7 @@ namespace {
 void compile_qfilter(const Nfa& nfa, Dfa& d) {
     d.filter_ok = false;
     d.qbloom.clear();
+    d.qbloom2.clear();
     d.qtab.clear();
     d.qb_off.clear();
     d.qb_ent.clear();
@@ -265,8 +266,9 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         const std::uint32_t h = qhash(qtop(grams[i].first, q));
         d.qbloom[qword(h, words)] |= qmask(h);
     }
+    // load factor <= 1/4: a random (non-key) code ends its probe in ~1.4 slots
     d.qtab_bits = 10;
-    while ((1u << d.qtab_bits) < 2u * keys) ++d.qtab_bits;
+    while (d.qtab_bits < 28 && (1ull << d.qtab_bits) < 4ull * keys) ++d.qtab_bits;
     d.qtab.assign(2ull << d.qtab_bits, kQEmpty);
     d.qb_off.reserve(keys + 1);
     d.qb_ent.reserve(grams.size());
@@ -277,27 +279,55 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         d.qtab[2 * slot] = c;
         d.qtab[2 * slot + 1] = static_cast<std::uint32_t>(d.qb_off.size());
         d.qb_off.push_back(static_cast<std::uint32_t>(d.qb_ent.size()));
+        const std::size_t first = i;
         for (; i < grams.size() && grams[i].first == c; ++i) d.qb_ent.push_back(grams[i].second);
+        // a one-entry bucket is stored in the slot itself (one dependent load less)
+        if (i - first == 1 && grams[first].second < 0x7FFFFFFFu) d.qtab[2 * slot + 1] = kQSingle | grams[first].second;
     }
     d.qb_off.push_back(static_cast<std::uint32_t>(d.qb_ent.size()));
     d.pat_off32.assign(nfa.pat_off.begin(), nfa.pat_off.end());
-    // pass rate of random q-grams (splitmix64 sample)
-    std::uint64_t z = 0x14037294ull, pass = 0;
-    const std::uint32_t trials = 1u << 20;
-    for (std::uint32_t t = 0; t < trials; ++t) {
-        z += 0x9E3779B97F4A7C15ull;
-        std::uint64_t r = z;
-        r = (r ^ (r >> 30)) * 0xBF58476D1CE4E5B9ull;
-        r = (r ^ (r >> 27)) * 0x94D049BB133111EBull;
-        const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
-        const std::uint32_t h = qhash(qtop(c, q));
-        const std::uint32_t m = qmask(h);
-        pass += (d.qbloom[qword(h, words)] & m) == m;
+    // pass rates of random q-grams (splitmix64 sample), level 1 and overall
+    auto pass_rates = [&](double& fp1, double& fp) {
+        std::uint64_t z = 0x14037294ull, p1 = 0, p2 = 0;
+        const std::uint32_t trials = 1u << 20;
+        const std::uint32_t words2 = static_cast<std::uint32_t>(d.qbloom2.size());
+        for (std::uint32_t t = 0; t < trials; ++t) {
+            z += 0x9E3779B97F4A7C15ull;
+            std::uint64_t r = z;
+            r = (r ^ (r >> 30)) * 0xBF58476D1CE4E5B9ull;
+            r = (r ^ (r >> 27)) * 0x94D049BB133111EBull;
+            const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
+            const std::uint32_t h = qhash(qtop(c, q));
+            const std::uint32_t m = qmask(h);
+            if ((d.qbloom[qword(h, words)] & m) != m) continue;
+            ++p1;
+            if (!words2) {
+                ++p2;
+                continue;
+            }
+            const std::uint32_t h2 = qhash2(h), m2 = qmask(h2);
+            p2 += (d.qbloom2[qword(h2, words2)] & m2) == m2;
+        }
+        fp1 = static_cast<double>(p1) / trials;
+        fp = static_cast<double>(p2) / trials;
+    };
+    pass_rates(d.filter_fp1, d.filter_fp);
+    if (d.filter_fp > 5e-3 && d.filter_fp1 <= kQLevel1Max) {
+        // level 2: ~1.5 % of its bits set (4 bits per key)
+        std::uint64_t w2 = (static_cast<std::uint64_t>(keys) * 4 * 100 / 3 / 32 + 3) & ~3ull;
+        w2 = std::min<std::uint64_t>(std::max<std::uint64_t>(w2, 1024), 16ull << 20);
+        d.qbloom2.assign(w2, 0u);
+        for (std::size_t i = 0; i < grams.size(); ++i) {
+            if (i && grams[i].first == grams[i - 1].first) continue;
+            const std::uint32_t h2 = qhash2(qhash(qtop(grams[i].first, q)));
+            d.qbloom2[qword(h2, static_cast<std::uint32_t>(w2))] |= qmask(h2);
+        }
+        pass_rates(d.filter_fp1, d.filter_fp);
     }
-    d.filter_fp = static_cast<double>(pass) / trials;
     // worth it when few samples survive (each survivor costs an exact probe)
     d.filter_ok = d.filter_fp <= 5e-3;
     if (!d.filter_ok) {
+        d.qbloom2.clear();
         d.qbloom.clear();
         d.qtab.clear();
         d.qb_off.clear();

@@ -97,7 +97,12 @@ struct Dfa {
     std::vector<std::uint32_t> qb_off;   // bucket offsets (keys + 1)
     std::vector<std::uint32_t> qb_ent;   // entries: pattern id << 2 | offset
     std::vector<std::uint32_t> pat_off32;  // pattern byte offsets (n_patterns + 1) into Nfa::pat_bytes
-    double filter_fp = 1.0;              // fraction of random q-grams passing the Bloom filter
+    double filter_fp = 1.0;              // fraction of random q-grams passing the Bloom filter(s)
+    // Level 2 (large dictionaries): when the shared-memory filter alone passes
+    // too many q-grams, the ones it passes probe a second, L2-resident blocked
+    // Bloom filter of the same keys (empty = single level).
+    std::vector<std::uint32_t> qbloom2;
+    double filter_fp1 = 1.0;             // pass rate of level 1 alone
 };
 
 // Fold the NFA into the dense DFA image. `hot_budget_bytes` bounds the u16 hot

@@ -60,7 +60,7 @@ __device__ __forceinline__ uint4 ldg_stream(const std::uint8_t* p) {
     return v;
 }
 
-template <int NW, int R>
+template <int NW, int R, bool L2F>
 __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs a) {
     constexpr long long kBlk = 2048;
     __shared__ std::uint32_t wcnt[NW];
@@ -137,6 +137,22 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
                 for (int r = 0; r < 4; ++r)
 #pragma unroll
                     for (int o = 0; o < 4; ++o) t[4 * r + o] = probe(window(cur[r], nb_[r], o) * qmul);
+                if (L2F) {
+                    // level 2 for the samples level 1 passed: predicated L2-resident
+                    // probes, issued together (one L2 latency per block)
+                    std::uint32_t v2[16], m2[16];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+#pragma unroll
+                        for (int o = 0; o < 4; ++o) {
+                            const int i = 4 * r + o;
+                            const std::uint32_t h2 = qhash2(window(cur[r], nb_[r], o) * qmul);
+                            m2[i] = qmask(h2);
+                            v2[i] = t[i] == 0u ? __ldg(a.qbloom2 + qword(h2, a.qwords2)) : 0xFFFFFFFFu;
+                        }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) t[i] |= m2[i] & ~v2[i];
+                }
                 std::uint32_t z = min(min(t[0], t[1]), t[2]);
                 z = min(min(z, t[3]), t[4]);
                 z = min(min(z, t[5]), t[6]);
@@ -234,8 +250,10 @@ __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) 
         }
         if (bucket == kQEmpty) continue;
         const long long rend = (w + 1) * a.qreg;
-        for (std::uint32_t e = a.qb_off[bucket]; e < a.qb_off[bucket + 1]; ++e) {
-            const std::uint32_t ent = a.qb_ent[e];
+        const bool single = bucket & kQSingle;
+        const std::uint32_t e0 = single ? 0u : a.qb_off[bucket], e1 = single ? 1u : a.qb_off[bucket + 1];
+        for (std::uint32_t e = e0; e < e1; ++e) {
+            const std::uint32_t ent = single ? bucket & ~kQSingle : a.qb_ent[e];
             const long long i = j - static_cast<long long>(ent & 3u);
             const std::uint32_t p = ent >> 2;
             const std::uint32_t lo = a.pat_off[p], len = a.pat_off[p + 1] - lo;
@@ -372,8 +390,10 @@ __global__ void __launch_bounds__(256) qconfirm_kernel(const ScanArgs a) {
         }
         if (bucket == kQEmpty) continue;
         // (KQ read any bytes as codes; the pattern compare below checks the real bytes)
-        for (std::uint32_t e = a.qb_off[bucket]; e < a.qb_off[bucket + 1]; ++e) {
-            const std::uint32_t ent = a.qb_ent[e];
+        const bool single = bucket & kQSingle;
+        const std::uint32_t e0 = single ? 0u : a.qb_off[bucket], e1 = single ? 1u : a.qb_off[bucket + 1];
+        for (std::uint32_t e = e0; e < e1; ++e) {
+            const std::uint32_t ent = single ? bucket & ~kQSingle : a.qb_ent[e];
             const long long i = j - static_cast<long long>(ent & 3u);
             const std::uint32_t p = ent >> 2;
             const std::uint32_t lo = a.pat_off[p], len = a.pat_off[p + 1] - lo;

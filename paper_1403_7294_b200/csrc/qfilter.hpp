@@ -36,6 +36,7 @@ constexpr std::uint32_t kQChunkBlocks = 128;  // blocks per output chunk (8 KiB)
 constexpr std::uint32_t kQWords = 57344;      // Bloom words (224 KiB: all of the opt-in shared memory but 3 KiB)
 constexpr std::uint32_t kQMul0 = 0x9E3779B1u, kQMul1 = 0x85EBCA77u, kQMul2 = 0xC2B2AE3Du;
 constexpr std::uint32_t kQEmpty = 0xFFFFFFFFu;  // exact-table slot marker
+constexpr std::uint32_t kQSingle = 0x80000000u;  // slot payload = kQSingle | the bucket's only entry
 
 #if defined(__CUDACC__)
 #define ACG_HD __host__ __device__ __forceinline__
@@ -74,6 +75,10 @@ ACG_HD std::uint32_t qword(std::uint32_t h, std::uint32_t words) { return qmulhi
 ACG_HD std::uint32_t qmask(std::uint32_t h) {
     return qperm(0x08040201u, 0x80402010u, qmulhi(h, kQMul1) & 0x7777u);
 }
+// Level-2 filter: its own word/mask from h2 = h * kQMul3 (independent of level 1).
+constexpr std::uint32_t kQMul3 = 0x27D4EB2Fu;
+constexpr double kQLevel1Max = 0.30;  // a level-1 pass rate above this is not worth streaming
+ACG_HD std::uint32_t qhash2(std::uint32_t h) { return h * kQMul3; }
 ACG_HD std::uint32_t qtop(std::uint32_t code, std::uint32_t q) { return q >= 16 ? code : code << (32 - 2 * q); }
 // Exact table slot of code c in a table of 2^bits slots.
 ACG_HD std::uint32_t qslot(std::uint32_t c, std::uint32_t bits) { return (c * kQMul2) >> (32 - bits); }

@@ -48,7 +48,10 @@ extern __shared__ __align__(16) std::uint8_t acg_hot_smem[];
 namespace acg {
 namespace kern {
 
-enum Pass : int { kCount = 0, kWrite = 1 };
+// kScratch: one exact walk that counts AND stores each chunk's records into
+// its own scratch slab (scap per chunk; a fuller chunk keeps counting and is
+// re-walked by a WRITE pass over the overflow list).
+enum Pass : int { kCount = 0, kWrite = 1, kScratch = 2 };
 constexpr int kTPB = 512;  // threads per block of the scan kernels
 constexpr std::uint32_t kEsc16 = 0xFFFFu;
 
@@ -104,6 +107,8 @@ struct ScanArgs {
     const std::uint8_t* pat_bytes;          // the dictionary
     const std::uint32_t* pat_off;           // n_patterns + 1
     std::uint32_t qwords;                   // Bloom words
+    const std::uint32_t* qbloom2;           // level-2 Bloom filter (L2-resident; null = single level)
+    std::uint32_t qwords2;
     unsigned long long* qcands;             // KQ survivors (sample offsets): one region of qcand_cap per KQ warp
     std::uint32_t* qcand_code;              // their q-gram codes (top-aligned, see qtop)
     std::uint32_t* qwarp_n;                 // per KQ consumer warp: survivors found (may exceed qcand_cap)
@@ -125,6 +130,9 @@ struct ScanArgs {
     std::uint32_t* reg_hi;                  // ... of which end in the next region
     std::uint32_t mcap;                     // per-region slab capacity (qscratch)
     std::uint32_t* qscal;                   // [0] max reg_n (overflow), [1] regions too big for ORDER
+    // exact mode, single pass (kScratch): chunk c's slab is scratch[c*scap, (c+1)*scap)
+    unsigned long long* scratch;
+    unsigned long long scap;
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {
@@ -195,10 +203,15 @@ __device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned lo
     if (PASS == kCount) {
         cnt += hi - lo;
     } else {
+        // kWrite: wr = global record slot; kScratch: wr = slot in the chunk's slab (cnt = its fill)
         const unsigned long long endk = (a.base + static_cast<unsigned long long>(pos)) << a.id_bits;
+        const unsigned long long lim = PASS == kWrite ? a.rec_cap : a.scap;
+        unsigned long long* dst = PASS == kWrite ? a.records : a.scratch + (wr - cnt);
         for (std::uint32_t j = lo; j < hi; ++j) {
-            if (wr < a.rec_cap) a.records[wr] = endk | __ldg(a.out_ids + j);
+            const unsigned long long at = PASS == kWrite ? wr : cnt;
+            if (at < lim) dst[at] = endk | __ldg(a.out_ids + j);
             ++wr;
+            if (PASS == kScratch) ++cnt;
         }
     }
 }
@@ -243,7 +256,9 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
         st[u] = 0;
         cnt[u] = 0;
         fol[u] = 0;
-        wr[u] = (PASS == kWrite && act[u]) ? a.chunk_offs[chunk_id[u]] : 0ull;
+        wr[u] = (PASS == kWrite && act[u]) ? a.chunk_offs[chunk_id[u]]
+                : PASS == kScratch             ? static_cast<unsigned long long>(chunk_id[u]) * a.scap
+                                               : 0ull;
         pos0[u] = a.emit_from + chunk_id[u] * a.chunk - a.halo;
     }
     const std::uint32_t K = a.K, H = a.H, Hn = a.Hn;
@@ -331,7 +346,7 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
             }
         }
     }
-    if (PASS == kCount) {
+    if (PASS != kWrite) {
         unsigned long long f = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1178,6 +1193,26 @@ __global__ void digest_kernel(const unsigned long long* rec, unsigned long long 
         atomicAdd(out + 0, s);
         atomicXor(out + 1, x);
         atomicAdd(out + 2, bad);
+    }
+}
+
+// K3 of the single-pass exact mode: every chunk's slab goes to its slot range
+// (one warp per chunk, coalesced); chunks whose records overflowed their slab
+// are listed for the exact WRITE pass.
+__global__ void __launch_bounds__(256) scratch_copy_kernel(const ScanArgs a, std::uint32_t* list, std::uint32_t* n_list) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = static_cast<long long>(gridDim.x) * 8;
+    for (long long c = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
+        const unsigned long long k = a.chunk_counts[c];
+        if (k == 0) continue;
+        if (k > a.scap) {
+            if (lane == 0) list[atomicAdd(n_list, 1u)] = static_cast<std::uint32_t>(c);
+            continue;
+        }
+        const unsigned long long o = a.chunk_offs[c];
+        const unsigned long long* src = a.scratch + static_cast<unsigned long long>(c) * a.scap;
+        for (unsigned long long j = lane; j < k; j += 32)
+            if (o + j < a.rec_cap) a.records[o + j] = src[j];
     }
 }
 

@@ -188,3 +188,16 @@ def test_filter_region_too_dense_replays_chunk_pipeline():
     text = rand_dna(rng, 1 << 20)
     text[100_000:300_000] = ord("A")
     run_filter(words, text)
+
+
+def test_filter_two_level_cfg2_dictionary():
+    """cfg2's 100,000 patterns: the shared-memory filter alone passes too many
+    q-grams, so its survivors probe the L2-resident level-2 filter. Parity on
+    a scaled text with the full dictionary, planted matches included."""
+    w = synth.CONFIGS[2].scaled(8 << 20, 100_000)
+    concat, offs = synth.patterns(w)
+    a = am.Automaton.from_arrays(concat, offs)
+    info = a.filter_info()
+    assert info["eligible"] and info["q"] == 16
+    m = run_filter((concat, offs), synth.text(w))
+    assert m > 0

@@ -252,3 +252,44 @@ def test_scaled_configs_vs_oracle(k, mode):
     assert np.array_equal(s.pattern_counts(), cnt)
     dsum, dxor, unsorted = s.digest()
     assert (dsum, dxor) == oracle.digest(oi, oe) and unsorted == 0
+
+
+# ---- exact mode: single-pass slabs after the first run ------------------------
+@pytest.mark.parametrize("cfg", [0, 3])
+def test_exact_single_pass_repeat_runs(cfg):
+    """The first EXACT run counts then writes; later runs (record density known)
+    walk once into per-chunk slabs and copy them into place. Both must equal
+    the oracle, run after run."""
+    w = synth.CONFIGS[cfg].scaled(2 << 20, 300)
+    text = synth.text(w)
+    concat, offs = synth.patterns(w)
+    a = am.Automaton.from_arrays(concat, offs)
+    s = am.Scanner(a, 0, am.SCAN_LIST | am.SCAN_COUNTS)
+    s.set_mode(am.MODE_EXACT)
+    oi, oe, _, cnt = oracle.OracleAutomaton(concat, offs).scan(text, counts=True)
+    for _ in range(3):
+        s.run_host(text)
+        ids, ends = s.records()
+        assert recs(ids, ends) == recs(oi, oe)
+        assert np.array_equal(s.pattern_counts(), cnt)
+
+
+def test_exact_single_pass_slab_overflow():
+    """A sparse first text sizes small slabs; a dense second text overflows
+    them, and the overflowed chunks are re-walked by the WRITE pass."""
+    rng = np.random.default_rng(31)
+    dna = np.frombuffer(b"ACGT", np.uint8)
+    words = [b"ACGTAC", b"AAAA", b"AAAAAAAA", b"CGCGT"] + sorted({rng.choice(dna, 7).tobytes() for _ in range(20)})
+    o = oracle.OracleAutomaton.from_words(words)
+    a = am.build(am.make_patterns(words))
+    s = am.Scanner(a, 0, am.SCAN_LIST | am.SCAN_COUNTS)
+    s.set_mode(am.MODE_EXACT)
+    sparse = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, 1 << 20)]
+    dense = sparse.copy()
+    dense[200_000:600_000] = ord("A")
+    for text in (sparse, dense, sparse, dense):
+        s.run_host(text)
+        ids, ends = s.records()
+        oi, oe, _, cnt = o.scan(text, counts=True)
+        assert recs(ids, ends) == recs(oi, oe)
+        assert np.array_equal(s.pattern_counts(), cnt)
