@@ -257,6 +257,7 @@ def main() -> None:
     ap.add_argument("--chunk-bytes", type=int, default=0)
     ap.add_argument("--profile-layout", action="store_true", help="profile-guided hot-state order")
     ap.add_argument("--text-mib", type=int, default=0, help="experiments: scale the workload's text (MiB)")
+    ap.add_argument("--no-counts", action="store_true", help="experiments: match list only (no per-pattern counts)")
     ap.add_argument("--mode", default="auto", choices=["auto", "sparse", "exact", "filter"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -298,7 +299,7 @@ def main() -> None:
     assert lay["halo"] == halo_guess
     d_text = h_text.cuda()
 
-    flags = am.SCAN_LIST | am.SCAN_COUNTS | am.SCAN_PROFILE
+    flags = am.SCAN_LIST | am.SCAN_PROFILE | (0 if args.no_counts else am.SCAN_COUNTS)
     sc = am.Scanner(a, local, flags)
     sc.set_geometry(args.streams_per_thread, args.threads_per_block, args.chunk_bytes)
     sc.set_mode({"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT,
@@ -351,7 +352,7 @@ def main() -> None:
 
     # correctness of the timed run (size-independent properties)
     dsum, dxor, unsorted = sc.digest()
-    counts_local = sc.pattern_counts()
+    counts_local = sc.pattern_counts() if not args.no_counts else np.zeros(P, dtype=np.uint64)
     mode_req = {"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT, "filter": am.MODE_FILTER}[args.mode]
     sc.__del__()  # release the timed scanner's workspace before the e2e scanner allocates its own
 

@@ -167,6 +167,7 @@ struct DeviceDfa {
     DevBuf<std::uint32_t> qbloom2;  // level-2 filter (large dictionaries)
     DevBuf<std::uint32_t> qtab, qb_off, qb_ent, pat_off;  // filter mode: exact q-gram table, patterns
     DevBuf<std::uint8_t> pat_bytes;
+    DevBuf<unsigned long long> pat_code;  // filter mode: 2-bit codes of each pattern's first 64 bytes
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
     std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
     int smem_optin = 0;
@@ -245,7 +246,8 @@ struct acg_scanner {
     // filter mode: KQ survivors (count in scalars32[3]), V0 record scratch
     // (count in scalars64[5]), per-chunk fill counters, heavy chunks (count in scalars32[2])
     DevBuf<unsigned long long> qcands, qscratch;
-    DevBuf<std::uint32_t> qcand_code, qwarp_n;
+    DevBuf<unsigned long long> qcand_win;
+    DevBuf<std::uint32_t> qwarp_n;
     DevBuf<std::uint32_t> qfill, qheavy;
     bool regrow = false;  // enqueue_write after a record-buffer regrowth
     // filter mode region pipeline (V1 + ORDER): per-region counts, overflow
@@ -339,6 +341,7 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
         ACG_CUDA(upload(dd->qb_ent, d.qb_ent.data(), d.qb_ent.size(), up));
         ACG_CUDA(upload(dd->pat_off, d.pat_off32.data(), d.pat_off32.size(), up));
         ACG_CUDA(upload(dd->pat_bytes, a->nfa.pat_bytes.data(), a->nfa.pat_bytes.size(), up));
+        ACG_CUDA(upload(dd->pat_code, reinterpret_cast<const unsigned long long*>(d.pat_code.data()), d.pat_code.size(), up));
     }
     ACG_CUDA(cudaStreamSynchronize(up));  // host staging vectors die here; buffers ready for any stream
     a->dev[device] = dd;
@@ -753,10 +756,11 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         unsigned long long cap = static_cast<unsigned long long>(4.0 * rate * static_cast<double>(n) / warps) + 64;
         cap = std::min<unsigned long long>(0x7FFFFFFFull / warps, std::max(cap, s->min_task_cap));
         ACG_CUDA(s->qcands.reserve(cap * warps, st));
-        ACG_CUDA(s->qcand_code.reserve(cap * warps, st));
+        ACG_CUDA(s->qcand_win.reserve(cap * warps, st));
         ACG_CUDA(s->qwarp_n.reserve(warps, st));
         a.qcands = s->qcands.p;
-        a.qcand_code = s->qcand_code.p;
+        a.qcand_win = s->qcand_win.p;
+        a.pat_code = dd.pat_code.p;
         a.qwarp_n = s->qwarp_n.p;
         a.qwarps = static_cast<std::uint32_t>(warps);
         a.qwords = static_cast<std::uint32_t>(d.qbloom.size());

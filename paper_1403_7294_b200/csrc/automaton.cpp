@@ -286,6 +286,12 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
     }
     d.qb_off.push_back(static_cast<std::uint32_t>(d.qb_ent.size()));
     d.pat_off32.assign(nfa.pat_off.begin(), nfa.pat_off.end());
+    d.pat_code.assign(2ull * nfa.n_patterns, 0ull);
+    for (std::uint32_t p = 0; p < nfa.n_patterns; ++p) {
+        const std::uint32_t lo = nfa.pat_off[p], len = std::min<std::uint32_t>(nfa.pat_off[p + 1] - lo, 64);
+        for (std::uint32_t k = 0; k < len; ++k)
+            d.pat_code[2ull * p + k / 32] |= static_cast<std::uint64_t>((nfa.pat_bytes[lo + k] >> 1) & 3u) << (2 * (k % 32));
+    }
     // pass rates of random q-grams (splitmix64 sample), level 1 and overall
     auto pass_rates = [&](double& fp1, double& fp) {
         std::uint64_t z = 0x14037294ull, p1 = 0, p2 = 0;
@@ -327,6 +333,7 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
     // worth it when few samples survive (each survivor costs an exact probe)
     d.filter_ok = d.filter_fp <= 5e-3;
     if (!d.filter_ok) {
+        d.pat_code.clear();
         d.qbloom2.clear();
         d.qbloom.clear();
         d.qtab.clear();

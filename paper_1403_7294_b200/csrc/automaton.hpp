@@ -97,6 +97,7 @@ struct Dfa {
     std::vector<std::uint32_t> qb_off;   // bucket offsets (keys + 1)
     std::vector<std::uint32_t> qb_ent;   // entries: pattern id << 2 | offset
     std::vector<std::uint32_t> pat_off32;  // pattern byte offsets (n_patterns + 1) into Nfa::pat_bytes
+    std::vector<std::uint64_t> pat_code;   // per pattern 2 words: 2-bit codes of bytes 0..31, 32..63
     double filter_fp = 1.0;              // fraction of random q-grams passing the Bloom filter(s)
     // Level 2 (large dictionaries): when the shared-memory filter alone passes
     // too many q-grams, the ones it passes probe a second, L2-resident blocked

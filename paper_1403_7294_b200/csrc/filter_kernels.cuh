@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
                             if (r == 2) lo = cur[2], hi = nb_[2];
                             if (r == 3) lo = cur[3], hi = nb_[3];
                             a.qcands[region + slot] = static_cast<unsigned long long>(pos);
-                            a.qcand_code[region + slot] = gram(lo, hi, o);
+                            a.qcand_win[region + slot] = (static_cast<unsigned long long>(hi) << 32) | lo;
                         }
                     }
                 }
@@ -210,6 +210,30 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
     return v;
 }
 
+// The q-gram code of the sample at byte j of the survivor's 16-byte word
+// (jw = j & 15) from its 32-base code window.
+__device__ __forceinline__ std::uint32_t qwin_code(unsigned long long win, std::uint32_t jw, std::uint32_t q) {
+    const unsigned long long c = win >> (2 * jw);
+    return static_cast<std::uint32_t>(q >= 32 ? c : c & ((1ull << (2 * q)) - 1));
+}
+
+// Pre-check in code space: pattern p (2-bit codes pc0 = bases 0..31, pc1 =
+// 32..63) placed at text byte i against the survivor's 32-base window that
+// starts at byte wstart (d = i - wstart in [-3, 12]); compares every base
+// both cover. A mismatch rejects the occurrence without reading the text.
+__device__ __forceinline__ bool qwin_match(unsigned long long win, int d, std::uint32_t len, unsigned long long pc0,
+                                           unsigned long long pc1) {
+    unsigned long long al;  // pattern codes aligned to window bases
+    if (d >= 0) al = pc0 << (2 * d);
+    else al = (pc0 >> (-2 * d)) | (pc1 << (64 + 2 * d));
+    const int kmin = d > 0 ? d : 0;
+    const int kmax = min(32, d + static_cast<int>(min(len, 64u)));
+    if (kmax <= kmin) return true;
+    const unsigned long long hi = kmax >= 32 ? ~0ull : (1ull << (2 * kmax)) - 1;
+    const unsigned long long mask = hi & ~((1ull << (2 * kmin)) - 1);
+    return ((win ^ al) & mask) == 0;
+}
+
 // Exact check of pattern p (bytes [lo, lo+len) of the dictionary) against
 // text[i, i+len): 16 independent byte pairs per round, so a match costs
 // ceil(len/16) dependent memory round trips rather than len.
@@ -237,7 +261,8 @@ __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) 
         const long long w = t / a.qcand_cap;
         if (static_cast<std::uint32_t>(t - w * a.qcand_cap) >= a.qwarp_n[w]) continue;
         const long long j = static_cast<long long>(a.qcands[t]);
-        const std::uint32_t code = a.q >= 16 ? a.qcand_code[t] : a.qcand_code[t] >> (32 - 2 * a.q);
+        const unsigned long long win = a.qcand_win[t];
+        const std::uint32_t code = qwin_code(win, static_cast<std::uint32_t>(j & 15), a.q);
         std::uint32_t slot = qslot(code, a.qtab_bits), bucket = kQEmpty;
         for (;;) {
             const uint2 e = *reinterpret_cast<const uint2*>(a.qtab + 2 * slot);
@@ -260,12 +285,11 @@ __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) 
             if (i < 0 || i + len > a.n) continue;
             const long long end = i + len - 1;
             if (end < a.emit_from) continue;
-            // pre-check two bytes outside the matched q-gram (random text passes
-            // 1 in 16), then the whole pattern
-            const std::uint32_t o = ent & 3u, k1 = o + a.q < len ? o + a.q : 0u, k2 = o ? o - 1u : len - 1u;
-            const bool pre = (__ldg(a.text + i + k1) == __ldg(a.pat_bytes + lo + k1)) &
-                             (__ldg(a.text + i + k2) == __ldg(a.pat_bytes + lo + k2));
-            if (!pre || !qmatch(a, i, lo, len)) continue;
+            // pre-check in code space against the survivor's window (no text
+            // read; random text passes 4^-(bases compared beyond the q-gram)),
+            // then the whole pattern byte by byte
+            const ulonglong2 pc = *reinterpret_cast<const ulonglong2*>(a.pat_code + 2ull * p);
+            if (!qwin_match(win, static_cast<int>(i - (j & ~15LL)), len, pc.x, pc.y) || !qmatch(a, i, lo, len)) continue;
             const std::uint32_t k = atomicAdd(a.reg_n + w, 1u);
             if (k < a.mcap)
                 a.qscratch[static_cast<unsigned long long>(w) * a.mcap + k] =
@@ -377,7 +401,8 @@ __global__ void __launch_bounds__(256) qconfirm_kernel(const ScanArgs a) {
         if (static_cast<std::uint32_t>(t % a.qcand_cap) >= a.qwarp_n[t / a.qcand_cap]) continue;
         const long long j = static_cast<long long>(a.qcands[t]);
         // the survivor's q-gram code, from KQ (y holds it in the top bits)
-        const std::uint32_t code = a.q >= 16 ? a.qcand_code[t] : a.qcand_code[t] >> (32 - 2 * a.q);
+        const unsigned long long win = a.qcand_win[t];
+        const std::uint32_t code = qwin_code(win, static_cast<std::uint32_t>(j & 15), a.q);
         std::uint32_t slot = qslot(code, a.qtab_bits), bucket = kQEmpty;
         for (;;) {
             const uint2 e = *reinterpret_cast<const uint2*>(a.qtab + 2 * slot);

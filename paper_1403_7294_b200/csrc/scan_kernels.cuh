@@ -110,7 +110,8 @@ struct ScanArgs {
     const std::uint32_t* qbloom2;           // level-2 Bloom filter (L2-resident; null = single level)
     std::uint32_t qwords2;
     unsigned long long* qcands;             // KQ survivors (sample offsets): one region of qcand_cap per KQ warp
-    std::uint32_t* qcand_code;              // their q-gram codes (top-aligned, see qtop)
+    unsigned long long* qcand_win;          // their text codes: 32 bases from the survivor's 16-byte word (2 bits each)
+    const unsigned long long* pat_code;     // per pattern: 2-bit codes of its first 64 bytes (2 words)
     std::uint32_t* qwarp_n;                 // per KQ consumer warp: survivors found (may exceed qcand_cap)
     std::uint32_t qwarps;                   // KQ consumer warps (regions)
     std::uint32_t* qcand_n;                 // total survivors (rate heuristic)
