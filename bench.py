@@ -317,7 +317,7 @@ def main() -> None:
 
     for _ in range(args.warmup):
         step()
-    sc.sync()  # sizes the record buffer (first run may re-emit)
+        sc.sync()  # adaptive sizes settle (record buffer, survivor regions, slabs) before timing
     m_total = sc.match_count()
     k_ms = np.zeros(5)
     torch.cuda.synchronize()

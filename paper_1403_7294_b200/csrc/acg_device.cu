@@ -161,6 +161,7 @@ struct DeviceDfa {
     int device = 0;
     std::shared_ptr<const acg::Dfa> dfa;
     DevBuf<std::uint32_t> next, out_off, out_ids, depth;
+    DevBuf<unsigned long long> outinfo;
     DevBuf<std::uint16_t> hot16, hotH, follows, follows_esc;
     DevBuf<std::uint8_t> symmap;
     DevBuf<std::uint32_t> qbloom;  // filter mode: kQWords Bloom words
@@ -233,6 +234,7 @@ struct acg_scanner {
     std::uint32_t U = 0, tpb = acg::kern::kTPB;  // U = 0: per-mode default
     std::uint32_t U_run = 4;  // interleave of the last run
     std::uint32_t tpb_run = acg::kern::kTPB;
+    bool tpb_set = false;  // block size fixed by acg_scanner_set_geometry
     unsigned long long chunk_override = 0;
     // last run's arguments (a sparse run whose task list overflowed is re-run at sync)
     const std::uint8_t* run_text = nullptr;
@@ -261,6 +263,7 @@ struct acg_scanner {
     // exact mode: records per owned byte of the last exact run (-1 = unknown);
     // scratch_run = the last run used the single-pass slabs
     double exact_density = -1.0;
+    unsigned long long exact_max = 0, exact_chunk = 0;  // largest chunk count of the last exact run, its chunk size
     bool scratch_run = false;
     DevBuf<unsigned long long> scratch;
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
@@ -318,6 +321,7 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
     ACG_CUDA(upload(dd->next, d.next.data(), d.next.size(), up));
     ACG_CUDA(upload(dd->out_off, d.out_off.data(), d.out_off.size(), up));
     ACG_CUDA(upload(dd->out_ids, d.out_ids.data(), d.out_ids.size(), up));
+    ACG_CUDA(upload(dd->outinfo, reinterpret_cast<const unsigned long long*>(d.outinfo.data()), d.outinfo.size(), up));
     ACG_CUDA(upload(dd->depth, d.depth.data(), d.depth.size(), up));
     ACG_CUDA(upload(dd->follows, d.follows.data(), d.follows.size(), up));
     ACG_CUDA(upload(dd->follows_esc, d.follows_esc.data(), d.follows_esc.size(), up));
@@ -484,6 +488,18 @@ QKernelChoice qfilter_choice() {
     return c;
 }
 unsigned qfilter_warps() { return static_cast<unsigned>(qfilter_choice().nw); }
+// Fused KQ (a consumer warp confirms survivors while the others stream; no
+// V1 launch): region pipeline, 16x2 geometry; ACG_QFUSED=1 turns it on. Off by
+// default: measured 0.294 ms against 0.226 + 0.028 (V1) unfused on cfg1 — the
+// producers lose registers (96 at 544 threads) and the consumer issue slots.
+bool qfilter_fused(const ScanArgs& a) {
+    static const bool on = [] {
+        const char* e = std::getenv("ACG_QFUSED");
+        return e && e[0] == '1';
+    }();
+    const QKernelChoice c = qfilter_choice();
+    return on && a.reg_n && c.nw == 16 && c.r == 2;
+}
 template <typename Kern>
 cudaError_t launch_q(Kern k, const ScanArgs& a, unsigned threads, std::size_t smem, int sms, cudaStream_t st) {
     cudaError_t e = prepare_smem(k, smem);
@@ -495,10 +511,14 @@ cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
     using namespace acg::kern;
     const QKernelChoice c = qfilter_choice();
     const std::size_t bloom = static_cast<std::size_t>(a.qwords) * 4;
-    if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true>, a, 32 * 16, bloom, sms, st);
-    if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2, false>, a, 32 * 24, bloom, sms, st);
-    if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3, false>, a, 32 * 16, bloom, sms, st);
-    return launch_q(qfilter_ldg_kernel<16, 2, false>, a, 32 * 16, bloom, sms, st);
+    if (qfilter_fused(a)) {
+        if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, true>, a, 32 * 17, bloom, sms, st);
+        return launch_q(qfilter_ldg_kernel<16, 2, false, true>, a, 32 * 17, bloom, sms, st);
+    }
+    if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, false>, a, 32 * 16, bloom, sms, st);
+    if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2, false, false>, a, 32 * 24, bloom, sms, st);
+    if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3, false, false>, a, 32 * 16, bloom, sms, st);
+    return launch_q(qfilter_ldg_kernel<16, 2, false, false>, a, 32 * 16, bloom, sms, st);
 }
 
 // Enqueue K3 (compaction + ordered write) for the current geometry.
@@ -563,9 +583,9 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         acg::kern::scratch_copy_kernel<<<g, 256, 0, st>>>(wa, s->active_list.p, s->scalars32.p);
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
-        ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
+        ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb_run, smem_bytes(dd), st));
     } else {
-        ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb, smem_bytes(dd), st));
+        ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb_run, smem_bytes(dd), st));
     }
     ++s->launches;
     return ACG_OK;
@@ -657,9 +677,16 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // 0.0625 (cfg2: fix-up replay dominates)
         mode = (s->last_event_rate < 0 || s->last_event_rate < kSparseMaxEventRate) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
     s->mode_run = mode;
-    s->U_run = stats ? 2u : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 1u : 4u));
+    // default interleave: sparse 1; exact 4 on DNA, 2 on generic alphabets (cfg3
+    // at 512 MiB: U=1 5.70 ms, U=2 4.87 ms, U=4 6.77 ms — cold-row L2 waits grow with U)
+    s->U_run = stats ? 2u
+                     : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 1u : (d.mode == acg::kAlphaDna4 ? 4u : 2u)));
     if (mode == ACG_MODE_SPARSE && s->U_run > 4) s->U_run = 4;
-    s->tpb_run = mode == ACG_MODE_SPARSE ? sparse_tpb(s->U_run) : s->tpb;
+    // exact mode at interleave <= 2 runs 1024 threads per SM (twice the warps to
+    // hide cold-row L2 latency) unless the caller fixed the block size
+    s->tpb_run = mode == ACG_MODE_SPARSE                ? sparse_tpb(s->U_run)
+                 : (s->tpb_set || s->U_run > 2 || stats) ? s->tpb
+                                                        : 2 * acg::kern::kTPB;
     plan_geometry(s, owned);
     const bool prof = s->flags & ACG_SCAN_PROFILE;
 
@@ -701,6 +728,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     a.hot16 = dd.hot16.p;
     a.out_off = dd.out_off.p;
     a.out_ids = dd.out_ids.p;
+    a.outinfo = dd.outinfo.p;
     a.depth = dd.depth.p;
     a.follows = dd.follows.p;
     a.follows_esc = dd.follows_esc.p;
@@ -786,10 +814,16 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             a.reg_n = s->qreg_n.p;
             a.reg_hi = s->qreg_n.p + W;
             a.qscal = s->qscal.p;
-            ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
-            if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
-            qconfirm_region_kernel<<<8 * dd.num_sms, 256, 0, st>>>(a);
-            ACG_CUDA(cudaGetLastError());
+            if (qfilter_fused(a)) {  // V1 runs inside KQ: its region counters start at zero
+                ACG_CUDA(cudaMemsetAsync(s->qreg_n.p, 0, 2ull * W * sizeof(std::uint32_t), st));
+                ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
+                if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+            } else {
+                ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
+                if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+                qconfirm_region_kernel<<<8 * dd.num_sms, 256, 0, st>>>(a);
+                ACG_CUDA(cudaGetLastError());
+            }
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[2], st));
             ScanArgs oa = a;
             oa.records = want_list ? s->records.p : nullptr;
@@ -853,9 +887,17 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     } else {
         // single pass (count + per-chunk slabs) once the previous run told the
         // record density and the slabs fit the budget; count + write otherwise
+        a.chunk_max = s->scalars64.p + 7;
+        ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 7, 0, sizeof(unsigned long long), st));
         if (want_list && !stats && s->exact_density >= 0) {
-            const unsigned long long scap =
-                static_cast<unsigned long long>(s->exact_density * 1.25 * static_cast<double>(s->chunk)) + 32;
+            // slab = the larger of 1.25 x the mean and 1.1 x the largest chunk of the last run
+            const double mean = s->exact_density * static_cast<double>(s->chunk);
+            const double big = s->exact_chunk > 0 ? 1.1 * static_cast<double>(s->exact_max) *
+                                                        static_cast<double>(s->chunk) / static_cast<double>(s->exact_chunk)
+                                                  : 0.0;
+            unsigned long long scap = static_cast<unsigned long long>(std::max(1.25 * mean, big)) + 32;
+            if (static_cast<double>(scap) * s->n_chunks * 8.0 > static_cast<double>(kScratchBudget))
+                scap = static_cast<unsigned long long>(1.25 * mean) + 32;
             if (static_cast<double>(scap) * s->n_chunks * 8.0 <= static_cast<double>(kScratchBudget)) {
                 ACG_CUDA(s->scratch.reserve(scap * s->n_chunks, st));
                 a.scratch = s->scratch.p;
@@ -863,7 +905,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
                 s->scratch_run = true;
             }
         }
-        ACG_CUDA(launch_exact_pass(d.mode, s->scratch_run ? kScratch : kCount, stats, s->U_run, a, s->grid, s->tpb,
+        ACG_CUDA(launch_exact_pass(d.mode, s->scratch_run ? kScratch : kCount, stats, s->U_run, a, s->grid, s->tpb_run,
                                    smem_bytes(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
@@ -959,8 +1001,13 @@ int scanner_sync(acg_scanner* s) {
         }
     }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
-    if (s->mode_run == ACG_MODE_EXACT && s->run_n > s->run_emit)
+    if (s->mode_run == ACG_MODE_EXACT && s->run_n > s->run_emit) {
         s->exact_density = static_cast<double>(s->m_total) / static_cast<double>(s->run_n - s->run_emit);
+        ACG_CUDA(cudaMemcpyAsync(s->pinned + 1, s->scalars64.p + 7, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        ACG_CUDA(cudaStreamSynchronize(st));
+        s->exact_max = s->pinned[1];
+        s->exact_chunk = s->chunk;
+    }
     if (s->mode_run == ACG_MODE_FILTER && s->run_n)
         s->last_filter_rate = static_cast<double>(reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[3]) /
                               static_cast<double>(s->run_n);
@@ -1229,6 +1276,7 @@ int acg_scanner_set_geometry(acg_scanner* s, std::uint32_t streams_per_thread, s
         if (threads_per_block % 32 || threads_per_block > static_cast<std::uint32_t>(acg::kern::kTPB))
             return fail(ACG_ERR_INVALID, "threads per block must be a multiple of 32, at most 512");
         s->tpb = threads_per_block;
+        s->tpb_set = true;
     }
     s->chunk_override = chunk_bytes;
     return ACG_OK;

@@ -466,6 +466,14 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
         std::copy(nfa.out_ids.begin() + nfa.out_off[s], nfa.out_ids.begin() + nfa.out_off[s + 1],
                   d.out_ids.begin() + d.out_off[i]);
     }
+    d.outinfo.assign(S, 0ull);
+    for (std::uint32_t i = 0; i < S; ++i) {
+        const std::uint32_t lo = d.out_off[i], cnt = d.out_off[i + 1] - lo;
+        if (!cnt) continue;
+        const std::uint64_t first = d.out_ids[lo];
+        d.outinfo[i] = lo | (static_cast<std::uint64_t>(std::min<std::uint32_t>(cnt, 255)) << 32) |
+                       ((first < (1u << 24) ? first : 0ull) << 40);
+    }
     d.hot16.assign(static_cast<std::size_t>(H + 1) * K, 0xFFFF);
     for (std::size_t i = 0; i < static_cast<std::size_t>(H) * K; ++i)
         if (d.next[i] < H) d.hot16[i] = static_cast<std::uint16_t>(d.next[i]);

@@ -84,6 +84,9 @@ struct Dfa {
     std::vector<std::uint32_t> out_ids;  // ascending per state
     std::vector<std::uint16_t> follows;  // S*K failure follows taken by the reference scan on (s, column)
     std::vector<std::uint16_t> follows_esc;  // per state, for bytes outside the pattern alphabet (dna4 mode)
+    // per device state: outputs packed for one load in the scan's emission —
+    // out_off (32 bits) | count << 32 (8 bits, 255 = more) | first id << 40 (24 bits)
+    std::vector<std::uint64_t> outinfo;
     std::uint32_t id_bits = 1;           // bits for a pattern id in a packed record
     std::uint32_t halo = 0;              // round_up(max_len, 16): warm-up bytes before each chunk
     std::uint32_t max_len = 0;

@@ -45,6 +45,86 @@ __device__ __forceinline__ std::uint32_t qcodes(const uint4& w) {
     return __byte_perm(__byte_perm(m0, m1, 0x0073u), __byte_perm(m2, m3, 0x7300u), 0x7610u);
 }
 
+// The q-gram code of the sample at byte j of the survivor's 16-byte word
+// (jw = j & 15) from its 32-base code window.
+__device__ __forceinline__ std::uint32_t qwin_code(unsigned long long win, std::uint32_t jw, std::uint32_t q) {
+    const unsigned long long c = win >> (2 * jw);
+    return static_cast<std::uint32_t>(q >= 32 ? c : c & ((1ull << (2 * q)) - 1));
+}
+
+// Pre-check in code space: pattern p (2-bit codes pc0 = bases 0..31, pc1 =
+// 32..63) placed at text byte i against the survivor's 32-base window that
+// starts at byte wstart (d = i - wstart in [-3, 12]); compares every base
+// both cover. A mismatch rejects the occurrence without reading the text.
+__device__ __forceinline__ bool qwin_match(unsigned long long win, int d, std::uint32_t len, unsigned long long pc0,
+                                           unsigned long long pc1) {
+    unsigned long long al;  // pattern codes aligned to window bases
+    if (d >= 0) al = pc0 << (2 * d);
+    else al = (pc0 >> (-2 * d)) | (pc1 << (64 + 2 * d));
+    const int kmin = d > 0 ? d : 0;
+    const int kmax = min(32, d + static_cast<int>(min(len, 64u)));
+    if (kmax <= kmin) return true;
+    const unsigned long long hi = kmax >= 32 ? ~0ull : (1ull << (2 * kmax)) - 1;
+    const unsigned long long mask = hi & ~((1ull << (2 * kmin)) - 1);
+    return ((win ^ al) & mask) == 0;
+}
+
+// Exact check of pattern p (bytes [lo, lo+len) of the dictionary) against
+// text[i, i+len): 16 independent byte pairs per round, so a match costs
+// ceil(len/16) dependent memory round trips rather than len.
+__device__ __forceinline__ bool qmatch(const ScanArgs& a, long long i, std::uint32_t lo, std::uint32_t len) {
+    for (std::uint32_t k0 = 0; k0 < len; k0 += 16) {
+        std::uint32_t diff = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k0 + k < len) diff |= static_cast<std::uint32_t>(__ldg(a.text + i + k0 + k) ^ __ldg(a.pat_bytes + lo + k0 + k));
+        if (diff) return false;
+    }
+    return true;
+}
+
+// Confirms survivor slot t (region w) exactly and appends its matches to w's slab.
+__device__ __forceinline__ void qconfirm_slot(const ScanArgs& a, long long w, unsigned long long t) {
+    const std::uint32_t tmask = (1u << a.qtab_bits) - 1u;
+    const long long j = static_cast<long long>(__ldcg(a.qcands + t));
+    const unsigned long long win = __ldcg(a.qcand_win + t);
+    const std::uint32_t code = qwin_code(win, static_cast<std::uint32_t>(j & 15), a.q);
+    std::uint32_t slot = qslot(code, a.qtab_bits), bucket = kQEmpty;
+    for (;;) {
+        const uint2 e = *reinterpret_cast<const uint2*>(a.qtab + 2 * slot);
+        if (e.y == kQEmpty) break;
+        if (e.x == code) {
+            bucket = e.y;
+            break;
+        }
+        slot = (slot + 1) & tmask;
+    }
+    if (bucket == kQEmpty) return;
+    const long long rend = (w + 1) * a.qreg;
+    const bool single = bucket & kQSingle;
+    const std::uint32_t e0 = single ? 0u : a.qb_off[bucket], e1 = single ? 1u : a.qb_off[bucket + 1];
+    for (std::uint32_t e = e0; e < e1; ++e) {
+        const std::uint32_t ent = single ? bucket & ~kQSingle : a.qb_ent[e];
+        const long long i = j - static_cast<long long>(ent & 3u);
+        const std::uint32_t p = ent >> 2;
+        const std::uint32_t lo = a.pat_off[p], len = a.pat_off[p + 1] - lo;
+        if (i < 0 || i + len > a.n) continue;
+        const long long end = i + len - 1;
+        if (end < a.emit_from) continue;
+        // pre-check in code space against the survivor's window (no text read;
+        // random text passes 4^-(bases compared beyond the q-gram)), then the
+        // whole pattern byte by byte
+        const ulonglong2 pc = *reinterpret_cast<const ulonglong2*>(a.pat_code + 2ull * p);
+        if (!qwin_match(win, static_cast<int>(i - (j & ~15LL)), len, pc.x, pc.y) || !qmatch(a, i, lo, len)) continue;
+        const std::uint32_t k = atomicAdd(a.reg_n + w, 1u);
+        if (k < a.mcap)
+            a.qscratch[static_cast<unsigned long long>(w) * a.mcap + k] =
+                ((a.base + static_cast<unsigned long long>(end)) << a.id_bits) | p;
+        if (end >= rend) atomicAdd(a.reg_hi + w, 1u);
+        if (a.pcounts) atomicAdd(a.pcounts + p, 1ull);
+    }
+}
+
 // KQ. No text staging in shared memory (all of it is left to the Bloom
 // filter): every warp streams its own contiguous
 // region of 2 KiB blocks with 128-bit streaming loads straight into
@@ -60,18 +140,12 @@ __device__ __forceinline__ uint4 ldg_stream(const std::uint8_t* p) {
     return v;
 }
 
-template <int NW, int R, bool L2F>
-__global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs a) {
+__device__ __forceinline__ const std::uint32_t* tab_of() { return reinterpret_cast<const std::uint32_t*>(acg_hot_smem); }
+
+template <int NW, int R, bool L2F, bool FUSED>
+__device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::uint32_t* tab, std::uint32_t* wcnt,
+                                                std::uint32_t* pub, std::uint32_t* nfin) {
     constexpr long long kBlk = 2048;
-    __shared__ std::uint32_t wcnt[NW];
-    const std::uint32_t* tab = reinterpret_cast<const std::uint32_t*>(acg_hot_smem);
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(a.qbloom);
-        uint4* dst = reinterpret_cast<uint4*>(acg_hot_smem);
-        for (std::uint32_t i = threadIdx.x; i < a.qwords / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-        if (threadIdx.x < NW) wcnt[threadIdx.x] = 0;
-    }
-    __syncthreads();
     const long long n = a.n;
     const long long nb = (n + kBlk - 1) / kBlk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -162,7 +236,8 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
                 z = min(min(z, t[13]), t[14]);
                 z = min(z, t[15]);
                 const bool hit = z == 0u;
-                if (__any_sync(0xFFFFFFFFu, hit) && hit) {
+                const bool anyhit = __any_sync(0xFFFFFFFFu, hit);
+                if (anyhit && hit) {
                     std::uint32_t pm = 0;
 #pragma unroll
                     for (int o = 0; o < 16; ++o) pm |= (t[o] == 0u ? 1u : 0u) << o;
@@ -181,6 +256,13 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
                         }
                     }
                 }
+                if (FUSED && anyhit) {  // publish this warp's survivors to the consumer warp
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        *static_cast<volatile std::uint32_t*>(&pub[warp]) = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
             }
@@ -190,9 +272,68 @@ __global__ void __launch_bounds__(32 * NW, 1) qfilter_ldg_kernel(const ScanArgs 
     if (lane == 0) {
         const std::uint32_t found = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
         a.qwarp_n[gw] = found;
-        if (a.reg_n) a.reg_n[gw] = a.reg_hi[gw] = 0u;  // V1's per-region counters
+        if (!FUSED && a.reg_n) a.reg_n[gw] = a.reg_hi[gw] = 0u;  // V1's per-region counters
         atomicAdd(a.qcand_n, found);
         atomicMax(a.qcand_max, static_cast<unsigned long long>(found));
+        if (FUSED) {
+            __threadfence_block();
+            *static_cast<volatile std::uint32_t*>(&pub[warp]) = found;
+            __threadfence_block();
+            atomicAdd(nfin, 1u);
+        }
+    }
+}
+
+// The consumer warp of the fused KQ: confirms the producers' published
+// survivors while they stream (V1's work overlapped with the scan), until all
+// producers have finished; what is left is drained by the whole CTA.
+template <int NW>
+__device__ __forceinline__ void qfilter_consume(const ScanArgs& a, const std::uint32_t* pub, std::uint32_t* done_sh,
+                                                std::uint32_t* nfin) {
+    const int lane = threadIdx.x & 31;
+    std::uint32_t done[NW];
+#pragma unroll
+    for (int p = 0; p < NW; ++p) done[p] = 0;
+    for (;;) {
+        const bool fin = *static_cast<volatile std::uint32_t*>(nfin) == NW;
+        if (fin) break;  // the rest goes to the cooperative drain
+        bool any = false;
+#pragma unroll
+        for (int p = 0; p < NW; ++p) {
+            const std::uint32_t avail = min(*static_cast<const volatile std::uint32_t*>(&pub[p]), a.qcand_cap);
+            if (done[p] < avail) {
+                __threadfence_block();
+                const long long w = static_cast<long long>(blockIdx.x) * NW + p;
+                const std::uint32_t k = done[p] + lane;
+                if (k < avail) qconfirm_slot(a, w, static_cast<unsigned long long>(w) * a.qcand_cap + k);
+                done[p] = min(avail, done[p] + 32u);
+                any = true;
+            }
+        }
+        if (!any) __nanosleep(256);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int p = 0; p < NW; ++p) done_sh[p] = done[p];
+}
+
+// After every producer finished: the whole CTA confirms the survivors the
+// consumer warp had not reached.
+template <int NW>
+__device__ __forceinline__ void qfilter_drain(const ScanArgs& a, const std::uint32_t* pub, const std::uint32_t* done_sh) {
+    std::uint32_t total = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p) total += min(pub[p], a.qcand_cap) - done_sh[p];
+    for (std::uint32_t f = threadIdx.x; f < total; f += blockDim.x) {
+        std::uint32_t g = f;
+        int p = 0;
+        for (; p < NW; ++p) {
+            const std::uint32_t len = min(pub[p], a.qcand_cap) - done_sh[p];
+            if (g < len) break;
+            g -= len;
+        }
+        const long long w = static_cast<long long>(blockIdx.x) * NW + p;
+        qconfirm_slot(a, w, static_cast<unsigned long long>(w) * a.qcand_cap + done_sh[p] + g);
     }
 }
 
@@ -210,93 +351,41 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
     return v;
 }
 
-// The q-gram code of the sample at byte j of the survivor's 16-byte word
-// (jw = j & 15) from its 32-base code window.
-__device__ __forceinline__ std::uint32_t qwin_code(unsigned long long win, std::uint32_t jw, std::uint32_t q) {
-    const unsigned long long c = win >> (2 * jw);
-    return static_cast<std::uint32_t>(q >= 32 ? c : c & ((1ull << (2 * q)) - 1));
-}
-
-// Pre-check in code space: pattern p (2-bit codes pc0 = bases 0..31, pc1 =
-// 32..63) placed at text byte i against the survivor's 32-base window that
-// starts at byte wstart (d = i - wstart in [-3, 12]); compares every base
-// both cover. A mismatch rejects the occurrence without reading the text.
-__device__ __forceinline__ bool qwin_match(unsigned long long win, int d, std::uint32_t len, unsigned long long pc0,
-                                           unsigned long long pc1) {
-    unsigned long long al;  // pattern codes aligned to window bases
-    if (d >= 0) al = pc0 << (2 * d);
-    else al = (pc0 >> (-2 * d)) | (pc1 << (64 + 2 * d));
-    const int kmin = d > 0 ? d : 0;
-    const int kmax = min(32, d + static_cast<int>(min(len, 64u)));
-    if (kmax <= kmin) return true;
-    const unsigned long long hi = kmax >= 32 ? ~0ull : (1ull << (2 * kmax)) - 1;
-    const unsigned long long mask = hi & ~((1ull << (2 * kmin)) - 1);
-    return ((win ^ al) & mask) == 0;
-}
-
-// Exact check of pattern p (bytes [lo, lo+len) of the dictionary) against
-// text[i, i+len): 16 independent byte pairs per round, so a match costs
-// ceil(len/16) dependent memory round trips rather than len.
-__device__ __forceinline__ bool qmatch(const ScanArgs& a, long long i, std::uint32_t lo, std::uint32_t len) {
-    for (std::uint32_t k0 = 0; k0 < len; k0 += 16) {
-        std::uint32_t diff = 0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (k0 + k < len) diff |= static_cast<std::uint32_t>(__ldg(a.text + i + k0 + k) ^ __ldg(a.pat_bytes + lo + k0 + k));
-        if (diff) return false;
-    }
-    return true;
-}
-
 // V1: confirms every survivor exactly (the q-gram's (pattern, offset)
 // bucket, then a byte compare at i = j - offset); threads stride over the
 // survivor regions' slots. A match found from region w's survivors ends in
 // w or, at most 63 bytes on, in w + 1 (reg_hi counts those); it is appended
 // to w's slab (reg_n[w], zeroed by KQ, counts them even past the capacity).
+template <int NW, int R, bool L2F, bool FUSED>
+__global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_kernel(const ScanArgs a) {
+    constexpr long long kBlk = 2048;
+    __shared__ std::uint32_t wcnt[NW], pub[NW], done_sh[NW], nfin;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.qbloom);
+        uint4* dst = reinterpret_cast<uint4*>(acg_hot_smem);
+        for (std::uint32_t i = threadIdx.x; i < a.qwords / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+        if (threadIdx.x < NW) wcnt[threadIdx.x] = pub[threadIdx.x] = 0;
+        if (threadIdx.x == 0) nfin = 0;
+    }
+    __syncthreads();
+    if (FUSED && (threadIdx.x >> 5) == NW) {  // the consumer warp
+        qfilter_consume<NW>(a, pub, done_sh, &nfin);
+    } else {
+        qfilter_produce<NW, R, L2F, FUSED>(a, tab_of(), wcnt, pub, &nfin);
+    }
+    if (FUSED) {
+        __syncthreads();
+        qfilter_drain<NW>(a, pub, done_sh);
+    }
+}
+
 __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) {
-    const std::uint32_t tmask = (1u << a.qtab_bits) - 1u;
     const long long total = static_cast<long long>(a.qwarps) * a.qcand_cap;
     for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long w = t / a.qcand_cap;
         if (static_cast<std::uint32_t>(t - w * a.qcand_cap) >= a.qwarp_n[w]) continue;
-        const long long j = static_cast<long long>(a.qcands[t]);
-        const unsigned long long win = a.qcand_win[t];
-        const std::uint32_t code = qwin_code(win, static_cast<std::uint32_t>(j & 15), a.q);
-        std::uint32_t slot = qslot(code, a.qtab_bits), bucket = kQEmpty;
-        for (;;) {
-            const uint2 e = *reinterpret_cast<const uint2*>(a.qtab + 2 * slot);
-            if (e.y == kQEmpty) break;
-            if (e.x == code) {
-                bucket = e.y;
-                break;
-            }
-            slot = (slot + 1) & tmask;
-        }
-        if (bucket == kQEmpty) continue;
-        const long long rend = (w + 1) * a.qreg;
-        const bool single = bucket & kQSingle;
-        const std::uint32_t e0 = single ? 0u : a.qb_off[bucket], e1 = single ? 1u : a.qb_off[bucket + 1];
-        for (std::uint32_t e = e0; e < e1; ++e) {
-            const std::uint32_t ent = single ? bucket & ~kQSingle : a.qb_ent[e];
-            const long long i = j - static_cast<long long>(ent & 3u);
-            const std::uint32_t p = ent >> 2;
-            const std::uint32_t lo = a.pat_off[p], len = a.pat_off[p + 1] - lo;
-            if (i < 0 || i + len > a.n) continue;
-            const long long end = i + len - 1;
-            if (end < a.emit_from) continue;
-            // pre-check in code space against the survivor's window (no text
-            // read; random text passes 4^-(bases compared beyond the q-gram)),
-            // then the whole pattern byte by byte
-            const ulonglong2 pc = *reinterpret_cast<const ulonglong2*>(a.pat_code + 2ull * p);
-            if (!qwin_match(win, static_cast<int>(i - (j & ~15LL)), len, pc.x, pc.y) || !qmatch(a, i, lo, len)) continue;
-            const std::uint32_t k = atomicAdd(a.reg_n + w, 1u);
-            if (k < a.mcap)
-                a.qscratch[static_cast<unsigned long long>(w) * a.mcap + k] =
-                    ((a.base + static_cast<unsigned long long>(end)) << a.id_bits) | p;
-            if (end >= rend) atomicAdd(a.reg_hi + w, 1u);
-            if (a.pcounts) atomicAdd(a.pcounts + p, 1ull);
-        }
+        qconfirm_slot(a, w, static_cast<unsigned long long>(t));
     }
 }
 

@@ -69,6 +69,7 @@ struct ScanArgs {
     const std::uint16_t* hotH;     // H*K truncated-automaton rows: id | 0x8000 attention
     const std::uint32_t* out_off;  // S+1
     const std::uint32_t* out_ids;
+    const unsigned long long* outinfo;  // S: out_off | count << 32 | first id << 40 (automaton.hpp)
     const std::uint32_t* depth;    // S: trie depth per device state (sparse-mode dedup)
     const std::uint16_t* follows;      // S*K (stats only)
     const std::uint16_t* follows_esc;  // S (stats only, dna4 mode)
@@ -134,6 +135,7 @@ struct ScanArgs {
     // exact mode, single pass (kScratch): chunk c's slab is scratch[c*scap, (c+1)*scap)
     unsigned long long* scratch;
     unsigned long long scap;
+    unsigned long long* chunk_max;          // COUNT / kScratch: max over chunks of the record count
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {
@@ -198,19 +200,25 @@ __device__ __forceinline__ int column_of(std::uint32_t b, const std::uint8_t* sm
 template <int PASS>
 __device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned long long& cnt, unsigned long long& wr,
                                      const ScanArgs& a) {
-    const std::uint32_t lo = __ldg(a.out_off + s), hi = __ldg(a.out_off + s + 1);
+    // one load: the state's output count, first id and list offset
+    const unsigned long long info = __ldg(a.outinfo + s);
+    std::uint32_t n = static_cast<std::uint32_t>(info >> 32) & 0xFFu;
+    const std::uint32_t lo = static_cast<std::uint32_t>(info);
+    if (n == 255u) n = __ldg(a.out_off + s + 1) - lo;
     // per-state visits are recorded by whichever pass the host enables them for
     if (a.visits) atomicAdd(a.visits + out_rank(s, a), 1ull);
     if (PASS == kCount) {
-        cnt += hi - lo;
+        cnt += n;
     } else {
         // kWrite: wr = global record slot; kScratch: wr = slot in the chunk's slab (cnt = its fill)
         const unsigned long long endk = (a.base + static_cast<unsigned long long>(pos)) << a.id_bits;
         const unsigned long long lim = PASS == kWrite ? a.rec_cap : a.scap;
         unsigned long long* dst = PASS == kWrite ? a.records : a.scratch + (wr - cnt);
-        for (std::uint32_t j = lo; j < hi; ++j) {
+        const std::uint32_t first = static_cast<std::uint32_t>(info >> 40);
+        for (std::uint32_t j = 0; j < n; ++j) {
             const unsigned long long at = PASS == kWrite ? wr : cnt;
-            if (at < lim) dst[at] = endk | __ldg(a.out_ids + j);
+            const std::uint32_t id = (j == 0 && (first || a.id_bits <= 24)) ? first : __ldg(a.out_ids + lo + j);
+            if (at < lim) dst[at] = endk | id;
             ++wr;
             if (PASS == kScratch) ++cnt;
         }
@@ -222,7 +230,7 @@ __device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned lo
 // (cold source rows clamp to the all-escape row H), then U L2 loads for the
 // escapes, so a warp waits for at most one L2 latency per step.
 template <int U, int MODE, int PASS, bool STATS>
-__global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_scan_kernel(const ScanArgs a) {
     extern __shared__ __align__(16) std::uint8_t smem[];
     const std::uint32_t hot_s = smem_u32(smem);
     const std::uint8_t* smap = smem + a.smem_table_bytes;
@@ -356,6 +364,12 @@ __global__ void __launch_bounds__(kTPB, 1) exact_scan_kernel(const ScanArgs a) {
             f += fol[u];
         }
         if (STATS && a.follows_total && f) atomicAdd(a.follows_total, f);
+        if (a.chunk_max) {  // largest chunk count (sizes the next run's slabs)
+            unsigned long long m = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) m = max(m, act[u] ? cnt[u] : 0ull);
+            if (m > *static_cast<volatile unsigned long long*>(a.chunk_max)) atomicMax(a.chunk_max, m);
+        }
     }
 }
 
