@@ -245,6 +245,7 @@ struct acg_scanner {
     int mode_run = 0;
     double last_event_rate = -1.0;
     double last_filter_rate = -1.0;  // filter mode: passing samples per text byte
+    unsigned long long last_filter_max = 0, last_filter_n = 0;  // fullest survivor region, text size
     // filter mode: KQ survivors (count in scalars32[3]), V0 record scratch
     // (count in scalars64[5]), per-chunk fill counters, heavy chunks (count in scalars32[2])
     DevBuf<unsigned long long> qcands, qscratch;
@@ -264,6 +265,8 @@ struct acg_scanner {
     // scratch_run = the last run used the single-pass slabs
     double exact_density = -1.0;
     unsigned long long exact_max = 0, exact_chunk = 0;  // largest chunk count of the last exact run, its chunk size
+    unsigned long long exact_chunks = 0;                 // ... and its number of chunks
+    DevBuf<unsigned long long> slab_size, slab_off;      // per-chunk slabs (sizes, prefix)
     bool scratch_run = false;
     DevBuf<unsigned long long> scratch;
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
@@ -470,7 +473,18 @@ std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 // Filter mode: KQ geometry.
 constexpr unsigned long long kTaskBudget = 48ull << 30;
 constexpr double kSparseMaxEventRate = 0.005;  // AUTO: sparse mode below this event rate
-constexpr unsigned long long kScratchBudget = 24ull << 30;  // exact-mode single-pass slabs (bytes)  // sparse fix-up task memory cap (bytes)
+constexpr unsigned long long kScratchBudget = 64ull << 30;  // exact-mode single-pass slabs (bytes)
+
+// Slab budget: at most kScratchBudget and 60 % of the device memory free now
+// (plus what the scanner's slabs already hold).
+double scratch_budget(double held) {
+    std::size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return static_cast<double>(kScratchBudget) / 4;
+    }
+    return std::min(static_cast<double>(kScratchBudget), 0.6 * static_cast<double>(free_b) + held);
+}  // sparse fix-up task memory cap (bytes)
 
 // KQ geometry: NW warps per SM, R blocks in flight per warp. ACG_QKERNEL
 // picks another instantiation (experiments only).
@@ -677,6 +691,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // 0.0625 (cfg2: fix-up replay dominates)
         mode = (s->last_event_rate < 0 || s->last_event_rate < kSparseMaxEventRate) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
     s->mode_run = mode;
+    if (mode != ACG_MODE_EXACT) s->exact_chunks = 0;  // chunk_counts no longer hold an exact run's counts
     // default interleave: sparse 1; exact 4 on DNA, 2 on generic alphabets (cfg3
     // at 512 MiB: U=1 5.70 ms, U=2 4.87 ms, U=4 6.77 ms — cold-row L2 waits grow with U)
     s->U_run = stats ? 2u
@@ -780,8 +795,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // and the scan re-run with larger regions
         const unsigned warps_per_sm = qfilter_warps();
         const unsigned long long warps = static_cast<unsigned long long>(dd.num_sms) * warps_per_sm;
+        // (after a run of the same size: 1.25 x its fullest region — V1 strides over
+        // every slot, so slack costs it time)
         const double rate = s->last_filter_rate > 0 ? s->last_filter_rate : 1.0 / 4096;
         unsigned long long cap = static_cast<unsigned long long>(4.0 * rate * static_cast<double>(n) / warps) + 64;
+        if (s->last_filter_max && s->last_filter_n == n)
+            cap = std::min(cap, s->last_filter_max + s->last_filter_max / 4 + 32);
         cap = std::min<unsigned long long>(0x7FFFFFFFull / warps, std::max(cap, s->min_task_cap));
         ACG_CUDA(s->qcands.reserve(cap * warps, st));
         ACG_CUDA(s->qcand_win.reserve(cap * warps, st));
@@ -889,16 +908,38 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // record density and the slabs fit the budget; count + write otherwise
         a.chunk_max = s->scalars64.p + 7;
         ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 7, 0, sizeof(unsigned long long), st));
-        if (want_list && !stats && s->exact_density >= 0) {
+        // slabs sized chunk by chunk from the previous run's counts when it had the
+        // same geometry (its counts are still in chunk_counts): total ~1.125 x its matches
+        const double budget = scratch_budget(s->scratch.n * 8.0);
+        const bool per_chunk = want_list && !stats && s->exact_chunk == s->chunk && s->exact_chunks == s->n_chunks &&
+                               s->exact_density >= 0 &&
+                               (1.125 * static_cast<double>(s->m_total) + 16.0 * s->n_chunks + 1) * 8.0 <= budget;
+        if (per_chunk) {
+            const unsigned long long cap = s->m_total + s->m_total / 8 + 16ull * s->n_chunks + 1;
+            ACG_CUDA(s->scratch.reserve(cap, st));
+            ACG_CUDA(s->slab_size.reserve(s->n_chunks + 1, st));
+            ACG_CUDA(s->slab_off.reserve(s->n_chunks + 1, st));
+            const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((s->n_chunks + 255) / 256, 8ull * dd.num_sms));
+            slab_sizes_kernel<<<std::max(g, 1u), 256, 0, st>>>(s->chunk_counts.p, static_cast<long long>(s->n_chunks),
+                                                                s->slab_size.p);
+            ACG_CUDA(cudaGetLastError());
+            ACG_CUDA(cudaMemsetAsync(s->slab_off.p, 0, sizeof(unsigned long long), st));
+            std::size_t tmp2 = s->cub_tmp.n;
+            ACG_CUDA(cub::DeviceScan::InclusiveSum(s->cub_tmp.p, tmp2, s->slab_size.p + 1, s->slab_off.p + 1,
+                                                   static_cast<int>(s->n_chunks), st));
+            a.scratch = s->scratch.p;
+            a.slab_off = s->slab_off.p;
+            s->scratch_run = true;
+        } else if (want_list && !stats && s->exact_density >= 0) {
             // slab = the larger of 1.25 x the mean and 1.1 x the largest chunk of the last run
             const double mean = s->exact_density * static_cast<double>(s->chunk);
             const double big = s->exact_chunk > 0 ? 1.1 * static_cast<double>(s->exact_max) *
                                                         static_cast<double>(s->chunk) / static_cast<double>(s->exact_chunk)
                                                   : 0.0;
             unsigned long long scap = static_cast<unsigned long long>(std::max(1.25 * mean, big)) + 32;
-            if (static_cast<double>(scap) * s->n_chunks * 8.0 > static_cast<double>(kScratchBudget))
+            if (static_cast<double>(scap) * s->n_chunks * 8.0 > budget)
                 scap = static_cast<unsigned long long>(1.25 * mean) + 32;
-            if (static_cast<double>(scap) * s->n_chunks * 8.0 <= static_cast<double>(kScratchBudget)) {
+            if (static_cast<double>(scap) * s->n_chunks * 8.0 <= budget) {
                 ACG_CUDA(s->scratch.reserve(scap * s->n_chunks, st));
                 a.scratch = s->scratch.p;
                 a.scap = scap;
@@ -1007,10 +1048,14 @@ int scanner_sync(acg_scanner* s) {
         ACG_CUDA(cudaStreamSynchronize(st));
         s->exact_max = s->pinned[1];
         s->exact_chunk = s->chunk;
+        s->exact_chunks = s->n_chunks;
     }
-    if (s->mode_run == ACG_MODE_FILTER && s->run_n)
+    if (s->mode_run == ACG_MODE_FILTER && s->run_n) {
         s->last_filter_rate = static_cast<double>(reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[3]) /
                               static_cast<double>(s->run_n);
+        s->last_filter_max = s->pinned[4];
+        s->last_filter_n = s->run_n;
+    }
     if (s->mode_run == ACG_MODE_SPARSE && s->n_chunks) {
         const double walked = static_cast<double>(s->n_chunks) * static_cast<double>(s->chunk + s->dd->dfa->halo);
         s->last_event_rate = static_cast<double>(s->pinned[5]) / walked;

@@ -358,7 +358,6 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
 // to w's slab (reg_n[w], zeroed by KQ, counts them even past the capacity).
 template <int NW, int R, bool L2F, bool FUSED>
 __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_kernel(const ScanArgs a) {
-    constexpr long long kBlk = 2048;
     __shared__ std::uint32_t wcnt[NW], pub[NW], done_sh[NW], nfin;
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.qbloom);

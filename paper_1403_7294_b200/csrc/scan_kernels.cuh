@@ -132,9 +132,11 @@ struct ScanArgs {
     std::uint32_t* reg_hi;                  // ... of which end in the next region
     std::uint32_t mcap;                     // per-region slab capacity (qscratch)
     std::uint32_t* qscal;                   // [0] max reg_n (overflow), [1] regions too big for ORDER
-    // exact mode, single pass (kScratch): chunk c's slab is scratch[c*scap, (c+1)*scap)
+    // exact mode, single pass (kScratch): chunk c's slab is scratch[c*scap, (c+1)*scap),
+    // or [slab_off[c], slab_off[c+1]) when sized from the previous run's chunk counts
     unsigned long long* scratch;
     unsigned long long scap;
+    const unsigned long long* slab_off;
     unsigned long long* chunk_max;          // COUNT / kScratch: max over chunks of the record count
 };
 
@@ -199,7 +201,7 @@ __device__ __forceinline__ int column_of(std::uint32_t b, const std::uint8_t* sm
 // Output handling at owned buffer position `pos` for state s (has outputs).
 template <int PASS>
 __device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned long long& cnt, unsigned long long& wr,
-                                     const ScanArgs& a) {
+                                     const ScanArgs& a, unsigned long long slab_end = 0) {
     // one load: the state's output count, first id and list offset
     const unsigned long long info = __ldg(a.outinfo + s);
     std::uint32_t n = static_cast<std::uint32_t>(info >> 32) & 0xFFu;
@@ -210,15 +212,14 @@ __device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned lo
     if (PASS == kCount) {
         cnt += n;
     } else {
-        // kWrite: wr = global record slot; kScratch: wr = slot in the chunk's slab (cnt = its fill)
+        // kWrite: wr = global record slot; kScratch: wr = slot in scratch, below the chunk's slab end
         const unsigned long long endk = (a.base + static_cast<unsigned long long>(pos)) << a.id_bits;
-        const unsigned long long lim = PASS == kWrite ? a.rec_cap : a.scap;
-        unsigned long long* dst = PASS == kWrite ? a.records : a.scratch + (wr - cnt);
+        const unsigned long long lim = PASS == kWrite ? a.rec_cap : slab_end;
+        unsigned long long* dst = PASS == kWrite ? a.records : a.scratch;
         const std::uint32_t first = static_cast<std::uint32_t>(info >> 40);
         for (std::uint32_t j = 0; j < n; ++j) {
-            const unsigned long long at = PASS == kWrite ? wr : cnt;
             const std::uint32_t id = (j == 0 && (first || a.id_bits <= 24)) ? first : __ldg(a.out_ids + lo + j);
-            if (at < lim) dst[at] = endk | id;
+            if (wr < lim) dst[wr] = endk | id;
             ++wr;
             if (PASS == kScratch) ++cnt;
         }
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_scan_kernel
     if (!act[0]) return;
 
     std::uint32_t st[U];
-    unsigned long long cnt[U], wr[U], fol[U];
+    unsigned long long cnt[U], wr[U], fol[U], send[U];
     long long pos0[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -266,8 +267,12 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_scan_kernel
         cnt[u] = 0;
         fol[u] = 0;
         wr[u] = (PASS == kWrite && act[u]) ? a.chunk_offs[chunk_id[u]]
-                : PASS == kScratch             ? static_cast<unsigned long long>(chunk_id[u]) * a.scap
+                : PASS == kScratch             ? (a.slab_off ? (act[u] ? a.slab_off[chunk_id[u]] : 0ull)
+                                                             : static_cast<unsigned long long>(chunk_id[u]) * a.scap)
                                                : 0ull;
+        send[u] = PASS != kScratch ? 0ull
+                  : a.slab_off     ? (act[u] ? a.slab_off[chunk_id[u] + 1] : 0ull)
+                                   : static_cast<unsigned long long>(chunk_id[u] + 1) * a.scap;
         pos0[u] = a.emit_from + chunk_id[u] * a.chunk - a.halo;
     }
     const std::uint32_t K = a.K, H = a.H, Hn = a.Hn;
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_scan_kernel
                 for (int u = 0; u < U; ++u) {
                     st[u] = v[u];
                     if (owned_blk && st[u] >= Hn && act[u] && has_out(st[u], a))
-                        emit<PASS>(st[u], pos0[u] + off + k, cnt[u], wr[u], a);
+                        emit<PASS>(st[u], pos0[u] + off + k, cnt[u], wr[u], a, send[u]);
                 }
             }
         } else {
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_scan_kernel
                         if (nx == kEsc16) nx = __ldg(a.next + st[u] * K + c);
                     }
                     st[u] = nx;
-                    if (owned_blk && nx >= Hn && has_out(nx, a)) emit<PASS>(nx, p, cnt[u], wr[u], a);
+                    if (owned_blk && nx >= Hn && has_out(nx, a)) emit<PASS>(nx, p, cnt[u], wr[u], a, send[u]);
                 }
             }
         }
@@ -1220,14 +1225,28 @@ __global__ void __launch_bounds__(256) scratch_copy_kernel(const ScanArgs a, std
     for (long long c = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
         const unsigned long long k = a.chunk_counts[c];
         if (k == 0) continue;
-        if (k > a.scap) {
+        const unsigned long long base = a.slab_off ? a.slab_off[c] : static_cast<unsigned long long>(c) * a.scap;
+        const unsigned long long cap = a.slab_off ? a.slab_off[c + 1] - base : a.scap;
+        if (k > cap) {
             if (lane == 0) list[atomicAdd(n_list, 1u)] = static_cast<std::uint32_t>(c);
             continue;
         }
         const unsigned long long o = a.chunk_offs[c];
-        const unsigned long long* src = a.scratch + static_cast<unsigned long long>(c) * a.scap;
+        const unsigned long long* src = a.scratch + base;
         for (unsigned long long j = lane; j < k; j += 32)
             if (o + j < a.rec_cap) a.records[o + j] = src[j];
+    }
+}
+
+// Slab sizes for the next single-pass exact run from this run's chunk counts
+// (+1/8 + 16 slack): out[c + 1] = size of chunk c; out[0] = 0 (prefix by CUB).
+__global__ void __launch_bounds__(256) slab_sizes_kernel(const unsigned long long* counts, long long n,
+                                                         unsigned long long* out) {
+    for (long long c = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x; c < n;
+         c += static_cast<long long>(gridDim.x) * 256) {
+        const unsigned long long k = counts[c];
+        out[c + 1] = k + (k >> 3) + 16;
+        if (c == 0) out[0] = 0;
     }
 }
 
