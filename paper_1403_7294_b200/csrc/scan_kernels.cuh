@@ -1250,5 +1250,20 @@ __global__ void __launch_bounds__(256) slab_sizes_kernel(const unsigned long lon
     }
 }
 
+// Clears up to kMax word-aligned regions in one launch (run-start counters).
+struct ZeroList {
+    static constexpr int kMax = 16;
+    std::uint32_t* ptr[kMax];
+    unsigned long long words[kMax];
+    int n;
+};
+__global__ void __launch_bounds__(256) zero_regions_kernel(const ZeroList zl) {
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * 256;
+    for (int r = 0; r < zl.n; ++r)
+        for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * 256 + threadIdx.x; i < zl.words[r];
+             i += stride)
+            zl.ptr[r][i] = 0u;
+}
+
 }  // namespace kern
 }  // namespace acg
