@@ -196,9 +196,14 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
                 if (b >= b1) break;
                 const int sl = (k + 1) % R;  // slot holding block b+1
                 std::uint32_t nxt[4];
+                // lane 0 needs the next block's first word now (lane 31's last neighbour);
+                // the rest of the next block is packed later (L2F: while level-2 probes fly)
+                nxt[0] = qcodes(buf[sl][0]);
+                if (!L2F) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) nxt[r] = qcodes(buf[sl][r]);
-                load(buf[sl]);  // block b + 1 + R
+                    for (int r = 1; r < 4; ++r) nxt[r] = qcodes(buf[sl][r]);
+                    load(buf[sl]);  // block b + 1 + R
+                }
                 // neighbour codes: lane+1's word of the same row; lane 31 gets lane 0's next row
                 std::uint32_t nb_[4];
 #pragma unroll
@@ -224,6 +229,10 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
                             m2[i] = qmask(h2);
                             v2[i] = t[i] == 0u ? __ldg(a.qbloom2 + qword(h2, a.qwords2)) : 0xFFFFFFFFu;
                         }
+                    // pack the next block and issue its load while the probes are in flight
+#pragma unroll
+                    for (int r = 1; r < 4; ++r) nxt[r] = qcodes(buf[sl][r]);
+                    load(buf[sl]);  // block b + 1 + R
 #pragma unroll
                     for (int i = 0; i < 16; ++i) t[i] |= m2[i] & ~v2[i];
                 }
