@@ -199,8 +199,13 @@ __device__ __forceinline__ int column_of(std::uint32_t b, const std::uint8_t* sm
 }
 
 // Output handling at owned buffer position `pos` for state s (has outputs).
+#ifdef ACG_EMIT_NOINLINE  // experiment: one out-of-line copy instead of one per unrolled step
+#define ACG_EMIT_INLINE __noinline__
+#else
+#define ACG_EMIT_INLINE __forceinline__
+#endif
 template <int PASS>
-__device__ __forceinline__ void emit(std::uint32_t s, long long pos, unsigned long long& cnt, unsigned long long& wr,
+__device__ ACG_EMIT_INLINE void emit(std::uint32_t s, long long pos, unsigned long long& cnt, unsigned long long& wr,
                                      const ScanArgs& a, unsigned long long slab_end = 0) {
     // one load: the state's output count, first id and list offset
     const unsigned long long info = __ldg(a.outinfo + s);
