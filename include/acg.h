@@ -125,6 +125,11 @@ int acg_scanner_digest(acg_scanner* s, uint64_t* dsum, uint64_t* dxor, uint64_t*
  * K1f excursion fix-up (sparse mode; 0 in exact mode), K2 prefix, K3
  * compact+write, K4 pattern counts] (scanner created with ACG_SCAN_PROFILE). */
 int acg_scanner_kernel_ms(acg_scanner* s, float* ms5);
+/* Turns the per-stage event timing (ACG_SCAN_PROFILE) on or off for the next
+ * runs (events are recorded between the stages, so leave it off for timing
+ * whole runs). No reference counterpart (the reference times with
+ * std::chrono around whole calls, partition.hpp:110-111). */
+int acg_scanner_set_profiling(acg_scanner* s, int on);
 /* Scan mode. SPARSE walks the truncated hot automaton from shared memory and
  * replays the rare cold excursions exactly; EXACT walks the full DFA in
  * lockstep (hot rows in shared memory, cold rows from L2); FILTER streams the

@@ -59,6 +59,7 @@ ACG_SYMBOLS = {
     "acg_scanner_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
     "acg_scanner_copy_pattern_counts": (C.c_int, [vp, vp, vp]),
     "acg_scanner_set_mode": (C.c_int, [vp, C.c_int]),
+    "acg_scanner_set_profiling": (C.c_int, [vp, C.c_int]),
     "acg_scanner_last_mode": (C.c_int, [vp, C.POINTER(C.c_double)]),
     "acg_automaton_layout": (C.c_int, [vp, u32p, u32p, u32p, u32p, C.POINTER(C.c_int)]),
     "acg_automaton_filter_info": (C.c_int, [vp, u32p, C.POINTER(C.c_double)]),

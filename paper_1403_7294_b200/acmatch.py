@@ -346,6 +346,10 @@ class Scanner:
     def set_mode(self, mode: int) -> None:
         _check(_lib.acg().acg_scanner_set_mode(self._h, mode))
 
+    def set_profiling(self, on: bool) -> None:
+        """Per-stage event timing for the next runs (kernel_ms)."""
+        _check(_lib.acg().acg_scanner_set_profiling(self._h, 1 if on else 0))
+
     def last_mode(self) -> tuple[str, float]:
         rate = C.c_double()
         m = _lib.acg().acg_scanner_last_mode(self._h, C.byref(rate))

@@ -1535,6 +1535,19 @@ int acg_scanner_kernel_ms(acg_scanner* s, float* ms5) {
     return ACG_OK;
 }
 
+int acg_scanner_set_profiling(acg_scanner* s, int on) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (on) {
+        ACG_CUDA(cudaSetDevice(s->device));
+        for (auto& e : s->ev)
+            if (!e) ACG_CUDA(cudaEventCreate(&e));
+        s->flags |= ACG_SCAN_PROFILE;
+    } else {
+        s->flags &= ~static_cast<std::uint32_t>(ACG_SCAN_PROFILE);
+    }
+    return ACG_OK;
+}
+
 int acg_scanner_set_mode(acg_scanner* s, int mode) {
     if (!s) return fail(ACG_ERR_INVALID, "null scanner");
     if (mode < ACG_MODE_AUTO || mode > ACG_MODE_FILTER) return fail(ACG_ERR_INVALID, "unknown mode");

@@ -142,7 +142,11 @@ struct ScanArgs {
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {
     uint4 v;
+#ifdef ACG_EXACT_TEXT_NORMAL  // experiment: normal L2 priority for the streamed text
     asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else  // streamed once: evict-first, so it does not push out the record lines being filled
+    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+#endif
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
     return v;

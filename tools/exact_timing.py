@@ -13,7 +13,10 @@ a = am.Automaton.from_arrays(concat, offs)
 h = torch.empty(w.n, dtype=torch.uint8, pin_memory=True)
 synth.text(w, out=h.numpy())
 d = h.cuda()
-for flags in (am.SCAN_LIST | am.SCAN_COUNTS | am.SCAN_PROFILE, am.SCAN_LIST | am.SCAN_COUNTS):
+order = (am.SCAN_LIST | am.SCAN_COUNTS | am.SCAN_PROFILE, am.SCAN_LIST | am.SCAN_COUNTS)
+if len(sys.argv) > 3 and sys.argv[3] == "swap":
+    order = order[::-1]
+for flags in order + order:
     sc = am.Scanner(a, 0, flags)
     st = torch.cuda.Stream()
     for _ in range(4):
