@@ -29,6 +29,10 @@
 namespace {
 
 thread_local std::string g_last_error;
+const bool g_debug = [] {  // ACG_DEBUG=1: per-run decisions on stderr (experiments)
+    const char* e = std::getenv("ACG_DEBUG");
+    return e && e[0] == '1';
+}();
 
 // Device start-up happens when the library is loaded rather than inside the
 // caller's first scan: driver initialisation (cuInit, ~0.6 s on a B200 node),
@@ -1098,6 +1102,11 @@ int scanner_sync(acg_scanner* s) {
     }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
     if (s->mode_run == ACG_MODE_EXACT && s->run_n > s->run_emit) {
+        if (g_debug) {
+            const std::uint32_t over = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[0];
+            std::fprintf(stderr, "[acg] exact run: scratch %d per_chunk %d scap %llu chunks %llu matches %llu overflowed %u\n",
+                         s->scratch_run ? 1 : 0, s->args.slab_off ? 1 : 0, s->args.scap, s->n_chunks, s->m_total, over);
+        }
         s->exact_density = static_cast<double>(s->m_total) / static_cast<double>(s->run_n - s->run_emit);
         ACG_CUDA(cudaMemcpyAsync(s->pinned + 1, s->scalars64.p + 7, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         ACG_CUDA(cudaStreamSynchronize(st));
