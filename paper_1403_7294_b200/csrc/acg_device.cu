@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -1296,7 +1297,9 @@ int acg_build(const std::uint8_t* concat, const std::uint64_t* offsets, std::uin
         if (offsets[i + 1] < offsets[i]) return fail(ACG_ERR_INVALID, "pattern offsets must be non-decreasing");
     auto a = std::make_unique<acg_automaton>();
     try {
+        const auto t0 = std::chrono::steady_clock::now();
         const int rc = acg::build_nfa(concat, offsets, n_patterns, a->nfa);
+        const auto t1 = std::chrono::steady_clock::now();
         if (rc == acg::kErrEmptyPattern) {
             std::uint32_t i = 0;
             while (offsets[i + 1] != offsets[i]) ++i;
@@ -1306,6 +1309,11 @@ int acg_build(const std::uint8_t* concat, const std::uint64_t* offsets, std::uin
         if (rc != acg::kOk) return fail(rc, "invalid dictionary");
         std::lock_guard<std::mutex> lock(a->mu);
         host_dfa_locked(a.get(), kSm100SmemOptin);
+        if (g_debug)
+            std::fprintf(stderr, "[acg] build: nfa %.3f s, dfa+filter %.3f s (%u states)\n",
+                         std::chrono::duration<double>(t1 - t0).count(),
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count(),
+                         a->nfa.state_count());
     } catch (const std::bad_alloc&) {
         return fail(ACG_ERR_OUT_OF_MEMORY, "host allocation failed while building the automaton");
     }
