@@ -52,6 +52,11 @@ namespace kern {
 // its own scratch slab (scap per chunk; a fuller chunk keeps counting and is
 // re-walked by a WRITE pass over the overflow list).
 enum Pass : int { kCount = 0, kWrite = 1, kScratch = 2 };
+#ifndef ACG_EXACT_UNROLL
+#define ACG_EXACT_UNROLL 16  // steps of the exact walk's fast path unrolled (code size vs ILP)
+#endif
+#define ACG_PRAGMA(x) _Pragma(#x)
+#define ACG_UNROLL(n) ACG_PRAGMA(unroll n)
 constexpr int kTPB = 512;  // threads per block of the scan kernels
 constexpr std::uint32_t kEsc16 = 0xFFFFu;
 
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_scan_kernel
             }
         }
         if (fast) {
-#pragma unroll
+            ACG_UNROLL(ACG_EXACT_UNROLL)
             for (int k = 0; k < 16; ++k) {
                 std::uint32_t col[U], v[U];
 #pragma unroll

@@ -17,5 +17,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"qfilter_ldg|qconfirm_region|qorder_region" -s 9 -c 3 -o $O/prof_cfg1 $CMD > $O/ncu_full.log 2>&1
 CMD3="python bench.py --config 3 --text-mib 256 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 timeout 600 $CMD3 > $O/plain3.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"exact_scan" -s 8 -c 1 -o $O/prof_cfg3 $CMD3 > $O/ncu_full3.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"exact_scan_kernel<\(int\)2, \(int\)1, \(int\)2" -c 1 -o $O/prof_cfg3 $CMD3 > $O/ncu_full3.log 2>&1
 echo done
