@@ -286,6 +286,7 @@ struct acg_scanner {
     unsigned long long exact_chunks = 0;                 // ... and its number of chunks
     DevBuf<unsigned long long> slab_size, slab_off;      // per-chunk slabs (sizes, prefix)
     bool scratch_run = false;
+    bool hist_run = false;  // per-pattern counts by a histogram of the records (exact mode with a list)
     DevBuf<unsigned long long> scratch;
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
@@ -490,7 +491,8 @@ std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
 // Filter mode: KQ geometry.
 constexpr unsigned long long kTaskBudget = 48ull << 30;
-constexpr double kSparseMaxEventRate = 0.005;  // AUTO: sparse mode below this event rate
+constexpr double kSparseMaxEventRate = 0.005;
+constexpr std::uint32_t kHistMaxPatterns = 56 * 1024;  // record histogram: u32 bins in shared memory  // AUTO: sparse mode below this event rate
 constexpr unsigned long long kScratchBudget = 64ull << 30;  // exact-mode single-pass slabs (bytes)
 
 // Slab budget: at most kScratchBudget and 60 % of the device memory free now
@@ -620,6 +622,19 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb_run, smem_bytes(dd), st));
     }
     ++s->launches;
+    if (s->hist_run) {
+        // per-pattern counts = histogram of the final record list (instead of
+        // per-state visit atomics in the walk); re-run with the records after a regrowth
+        const std::uint32_t P = s->a->nfa.n_patterns;
+        ACG_CUDA(cudaMemsetAsync(s->counts.p, 0, P * sizeof(unsigned long long), st));
+        auto k = acg::kern::record_hist_kernel;
+        const std::size_t smem = static_cast<std::size_t>(P) * 4;
+        ACG_CUDA(prepare_smem(k, smem));
+        k<<<2 * dd.num_sms, 1024, smem, st>>>(s->records.p, s->chunk_offs.p + s->n_chunks, s->records.n, dd.dfa->id_bits, P,
+                                               s->counts.p);
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
+    }
     return ACG_OK;
 }
 
@@ -722,6 +737,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     const bool want_counts = s->flags & ACG_SCAN_COUNTS;
     const bool stats = s->flags & ACG_SCAN_STATS;
     s->launches = 0;
+    s->hist_run = false;
     s->zeros.clear();
     s->scratch_run = false;
     s->synced = false;
@@ -965,6 +981,10 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     } else {
         // single pass (count + per-chunk slabs) once the previous run told the
         // record density and the slabs fit the budget; count + write otherwise
+        // per-pattern counts from the written records when the list is produced
+        // (the walk then issues no per-state visit atomics)
+        s->hist_run = want_list && want_counts && s->a->nfa.n_patterns <= kHistMaxPatterns;
+        if (s->hist_run) a.visits = nullptr;
         a.chunk_max = s->scalars64.p + 7;
         zero_later(s, s->scalars64.p + 7, sizeof(unsigned long long));
         // slabs sized chunk by chunk from the previous run's counts when it had the
@@ -1024,7 +1044,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     }
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[4], st));
     // K4: per-pattern counts
-    if (want_counts && n_out_states && mode != ACG_MODE_FILTER) {
+    if (want_counts && n_out_states && mode != ACG_MODE_FILTER && !s->hist_run) {
         const unsigned tb = 256;
         const unsigned g = std::min<unsigned>((n_out_states + tb - 1) / tb, 8 * dd.num_sms);
         pattern_counts_kernel<<<g, tb, 0, st>>>(s->visits.p, dd.out_off.p, dd.out_ids.p, d.Hn, d.H, d.Cn, d.S,

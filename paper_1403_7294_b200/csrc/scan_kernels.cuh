@@ -1279,5 +1279,24 @@ __global__ void __launch_bounds__(256) zero_regions_kernel(const ZeroList zl) {
             zl.ptr[r][i] = 0u;
 }
 
+// Per-pattern counts from the final record list: per-CTA shared-memory bins
+// (one u32 per pattern), flushed into the u64 counts. m = *m_ptr records,
+// at most cap of them stored.
+__global__ void __launch_bounds__(1024) record_hist_kernel(const unsigned long long* rec, const unsigned long long* m_ptr,
+                                                           unsigned long long cap, std::uint32_t id_bits,
+                                                           std::uint32_t P, unsigned long long* counts) {
+    extern __shared__ std::uint32_t bins[];
+    for (std::uint32_t i = threadIdx.x; i < P; i += blockDim.x) bins[i] = 0;
+    __syncthreads();
+    const unsigned long long m = min(*m_ptr, cap);
+    const unsigned long long mask = (1ull << id_bits) - 1;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long t = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < m; t += stride)
+        atomicAdd(&bins[static_cast<std::uint32_t>(rec[t] & mask)], 1u);
+    __syncthreads();
+    for (std::uint32_t i = threadIdx.x; i < P; i += blockDim.x)
+        if (bins[i]) atomicAdd(counts + i, static_cast<unsigned long long>(bins[i]));
+}
+
 }  // namespace kern
 }  // namespace acg
