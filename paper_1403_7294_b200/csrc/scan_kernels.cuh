@@ -147,10 +147,17 @@ struct ScanArgs {
 
 __device__ __forceinline__ uint4 ld_stream16(const std::uint8_t* p) {
     uint4 v;
-#ifdef ACG_EXACT_TEXT_NORMAL  // experiment: normal L2 priority for the streamed text
-    asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-#else  // streamed once: evict-first, so it does not push out the record lines being filled
+// Each stream reads 16 bytes of its own chunk per 16 steps, so a warp's load
+// touches 32 different sectors: the L2 prefetch hint makes the first load of
+// a stream fetch the next 256 (or 128) bytes of it, which its next loads then
+// hit (ncu, cfg3: evict-first streaming loads without the hint read the text
+// 6.7x from DRAM).
+#if defined(ACG_EXACT_TEXT_CS)  // experiment
     asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+#elif defined(ACG_EXACT_TEXT_128)
+    asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else
+    asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
 #endif
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
