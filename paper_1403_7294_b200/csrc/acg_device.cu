@@ -287,6 +287,7 @@ struct acg_scanner {
     DevBuf<unsigned long long> slab_size, slab_off;      // per-chunk slabs (sizes, prefix)
     bool scratch_run = false;
     bool hist_run = false;  // per-pattern counts by a histogram of the records (exact mode with a list)
+    bool hist_fused = false;  // ... taken by the slab copy (+ K4 over the re-walked chunks' visits)
     DevBuf<unsigned long long> scratch;
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
@@ -611,10 +612,23 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         k<<<g, 256, smem_sparse(dd), st>>>(wa);
         ACG_CUDA(cudaGetLastError());
     } else if (s->scratch_run) {
-        // slabs -> slot ranges; overflowed chunks are re-walked by the WRITE pass
-        const unsigned g = static_cast<unsigned>(
-            std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 16ull * dd.num_sms)));
-        acg::kern::scratch_copy_kernel<<<g, 256, 0, st>>>(wa, s->active_list.p, s->scalars32.p);
+        // slabs -> slot ranges; overflowed chunks are re-walked by the WRITE pass.
+        // Per-pattern counts (not after a regrowth): histogram of what the copy
+        // moves + the re-walked chunks' visits (K4)
+        s->hist_fused = s->hist_run && !s->regrow;
+        if (s->hist_fused) {
+            const std::uint32_t P = s->a->nfa.n_patterns;
+            ACG_CUDA(cudaMemsetAsync(s->counts.p, 0, P * sizeof(unsigned long long), st));
+            auto k = acg::kern::scratch_copy_kernel<true>;
+            const std::size_t smem = static_cast<std::size_t>(P) * 4;
+            ACG_CUDA(prepare_smem(k, smem));
+            k<<<2 * dd.num_sms, 1024, smem, st>>>(wa, s->active_list.p, s->scalars32.p, P, s->counts.p);
+            wa.visits = s->visits.p;
+        } else {
+            const unsigned g = static_cast<unsigned>(
+                std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 16ull * dd.num_sms)));
+            acg::kern::scratch_copy_kernel<false><<<g, 256, 0, st>>>(wa, s->active_list.p, s->scalars32.p, 0, nullptr);
+        }
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
         ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb_run, smem_bytes(dd), st));
@@ -622,7 +636,7 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         ACG_CUDA(launch_exact_pass(dd.dfa->mode, kWrite, false, s->U_run, wa, s->grid, s->tpb_run, smem_bytes(dd), st));
     }
     ++s->launches;
-    if (s->hist_run) {
+    if (s->hist_run && !s->hist_fused) {
         // per-pattern counts = histogram of the final record list (instead of
         // per-state visit atomics in the walk); re-run with the records after a regrowth
         const std::uint32_t P = s->a->nfa.n_patterns;
@@ -738,6 +752,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     const bool stats = s->flags & ACG_SCAN_STATS;
     s->launches = 0;
     s->hist_run = false;
+    s->hist_fused = false;
     s->zeros.clear();
     s->scratch_run = false;
     s->synced = false;
@@ -1044,7 +1059,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     }
     if (prof) ACG_CUDA(cudaEventRecord(s->ev[4], st));
     // K4: per-pattern counts
-    if (want_counts && n_out_states && mode != ACG_MODE_FILTER && !s->hist_run) {
+    if (want_counts && n_out_states && mode != ACG_MODE_FILTER && (!s->hist_run || s->hist_fused)) {
         const unsigned tb = 256;
         const unsigned g = std::min<unsigned>((n_out_states + tb - 1) / tb, 8 * dd.num_sms);
         pattern_counts_kernel<<<g, tb, 0, st>>>(s->visits.p, dd.out_off.p, dd.out_ids.p, d.Hn, d.H, d.Cn, d.S,
@@ -1278,7 +1293,8 @@ void warm_up_device(int device) {
     load(reinterpret_cast<const void*>(compact_active_kernel));
     load(reinterpret_cast<const void*>(pattern_counts_kernel));
     load(reinterpret_cast<const void*>(zero_regions_kernel));
-    load(reinterpret_cast<const void*>(scratch_copy_kernel));
+    load(reinterpret_cast<const void*>(scratch_copy_kernel<false>));
+    load(reinterpret_cast<const void*>(scratch_copy_kernel<true>));
     load(reinterpret_cast<const void*>(qfilter_ldg_kernel<16, 2, false, false>));
     load(reinterpret_cast<const void*>(qconfirm_region_kernel));
     load(reinterpret_cast<const void*>(qorder_region_kernel));

@@ -1240,10 +1240,23 @@ __global__ void digest_kernel(const unsigned long long* rec, unsigned long long 
 // K3 of the single-pass exact mode: every chunk's slab goes to its slot range
 // (one warp per chunk, coalesced); chunks whose records overflowed their slab
 // are listed for the exact WRITE pass.
-__global__ void __launch_bounds__(256) scratch_copy_kernel(const ScanArgs a, std::uint32_t* list, std::uint32_t* n_list) {
+// With HIST, the CTA also histograms the ids it copies (shared-memory bins,
+// P = n_patterns) into `counts` — the per-pattern counts without re-reading
+// the records (the overflowed chunks' counts come from the WRITE pass's visits).
+template <bool HIST>
+__global__ void __launch_bounds__(HIST ? 1024 : 256) scratch_copy_kernel(const ScanArgs a, std::uint32_t* list,
+                                                                         std::uint32_t* n_list, std::uint32_t P,
+                                                                         unsigned long long* counts) {
+    extern __shared__ std::uint32_t bins[];
+    if (HIST) {
+        for (std::uint32_t i = threadIdx.x; i < P; i += blockDim.x) bins[i] = 0;
+        __syncthreads();
+    }
+    const unsigned long long mask = (1ull << a.id_bits) - 1;
     const int lane = threadIdx.x & 31;
-    const long long warps = static_cast<long long>(gridDim.x) * 8;
-    for (long long c = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
+    const long long wpb = blockDim.x >> 5;
+    const long long warps = static_cast<long long>(gridDim.x) * wpb;
+    for (long long c = static_cast<long long>(blockIdx.x) * wpb + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
         const unsigned long long k = a.chunk_counts[c];
         if (k == 0) continue;
         const unsigned long long base = a.slab_off ? a.slab_off[c] : static_cast<unsigned long long>(c) * a.scap;
@@ -1254,8 +1267,16 @@ __global__ void __launch_bounds__(256) scratch_copy_kernel(const ScanArgs a, std
         }
         const unsigned long long o = a.chunk_offs[c];
         const unsigned long long* src = a.scratch + base;
-        for (unsigned long long j = lane; j < k; j += 32)
-            if (o + j < a.rec_cap) a.records[o + j] = src[j];
+        for (unsigned long long j = lane; j < k; j += 32) {
+            const unsigned long long r = src[j];
+            if (o + j < a.rec_cap) a.records[o + j] = r;
+            if (HIST) atomicAdd(&bins[static_cast<std::uint32_t>(r & mask)], 1u);
+        }
+    }
+    if (HIST) {
+        __syncthreads();
+        for (std::uint32_t i = threadIdx.x; i < P; i += blockDim.x)
+            if (bins[i]) atomicAdd(counts + i, static_cast<unsigned long long>(bins[i]));
     }
 }
 
