@@ -293,3 +293,35 @@ def test_exact_single_pass_slab_overflow():
         oi, oe, _, cnt = o.scan(text, counts=True)
         assert recs(ids, ends) == recs(oi, oe)
         assert np.array_equal(s.pattern_counts(), cnt)
+
+
+def test_concurrent_scans_share_one_automaton():
+    """Any number of concurrent scans on one immutable automaton
+    (aho_corasick.hpp:50-52; SPEC: scan is reentrant): 8 host threads, each
+    with its own text, through the one-shot API (scanner pool per automaton)."""
+    import threading
+    w = synth.CONFIGS[0].scaled(1 << 20, 300)
+    concat, offs = synth.patterns(w)
+    a = am.Automaton.from_arrays(concat, offs)
+    o = oracle.OracleAutomaton(concat, offs)
+    texts = [synth.text(w.scaled((1 << 20) + 4096 * k)) for k in range(8)]
+    results = [None] * len(texts)
+    errors = []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                results[k] = am.scan_arrays(a, texts[k], am.SCAN_LIST | am.SCAN_COUNTS)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(texts))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k, text in enumerate(texts):
+        oi, oe, _, cnt = o.scan(text, counts=True)
+        assert recs(results[k].ids, results[k].ends) == recs(oi, oe)
+        assert np.array_equal(results[k].counts, cnt)
