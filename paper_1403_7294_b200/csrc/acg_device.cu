@@ -928,7 +928,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
                 ACG_CUDA(flush_zeros(s, st));
                 ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
                 if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
-                qconfirm_region_kernel<<<8 * dd.num_sms, 256, 0, st>>>(a);
+                static const unsigned v1_ctas = [] {  // CTAs per SM (ACG_V1_CTAS: experiments)
+                    const char* e = std::getenv("ACG_V1_CTAS");
+                    const int v = e ? std::atoi(e) : 0;
+                    return v > 0 && v <= 64 ? static_cast<unsigned>(v) : 8u;
+                }();
+                qconfirm_region_kernel<<<v1_ctas * dd.num_sms, 256, 0, st>>>(a);
                 ACG_CUDA(cudaGetLastError());
             }
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[2], st));
