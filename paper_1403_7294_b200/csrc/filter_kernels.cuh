@@ -408,24 +408,29 @@ constexpr int kQOrderMax = 1024;
 constexpr int kQOrderWarps = 4;
 
 __global__ void __launch_bounds__(32 * kQOrderWarps) qorder_region_kernel(const ScanArgs a, unsigned long long* offs) {
+    static_assert(kQOrderWarps == 4, "the CTA prefix below reads whole uint4 groups of regions");
     __shared__ unsigned long long buf[kQOrderWarps][kQOrderMax];
+    __shared__ unsigned long long part[kQOrderWarps];
     const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long w = static_cast<long long>(blockIdx.x) * kQOrderWarps + wl;
-    if (w >= a.qwarps) return;
+    const long long w0 = static_cast<long long>(blockIdx.x) * kQOrderWarps;
+    const long long w = w0 + wl;
     const long long W = a.qwarps;
-    unsigned long long sum = 0;
-    {  // sum of reg_n[0, w): 16-byte loads, several in flight per lane
-        const long long w4 = w >> 2;
+    {  // the CTA's prefix: sum of reg_n[0, w0) by all its threads (16-byte loads)
         const uint4* r4 = reinterpret_cast<const uint4*>(a.reg_n);
+        unsigned long long ps = 0;
 #pragma unroll 4
-        for (long long v = lane; v < w4; v += 32) {
+        for (long long v = threadIdx.x; v < (w0 >> 2); v += blockDim.x) {
             const uint4 q = r4[v];
-            sum += static_cast<unsigned long long>(q.x) + q.y + q.z + q.w;
+            ps += static_cast<unsigned long long>(q.x) + q.y + q.z + q.w;
         }
-        if (lane < (w & 3)) sum += a.reg_n[(w4 << 2) + lane];
-    }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xFFFFFFFFu, ps, o);
+        if (lane == 0) part[wl] = ps;
+    }
+    __syncthreads();
+    if (w >= W) return;
+    unsigned long long sum = part[0] + part[1] + part[2] + part[3];
+    for (long long v = w0; v < w; ++v) sum += a.reg_n[v];  // this CTA's earlier regions (< 4)
     const std::uint32_t hprev = w > 0 ? a.reg_hi[w - 1] : 0u;
     const std::uint32_t nw = min(a.reg_n[w], a.mcap), np = w > 0 ? min(a.reg_n[w - 1], a.mcap) : 0u;
     const unsigned long long off = sum - hprev;
