@@ -388,22 +388,29 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
     std::vector<std::uint32_t> delta(static_cast<std::size_t>(S) * K);
     std::vector<std::uint32_t> fol(static_cast<std::size_t>(S) * K);
     std::vector<std::uint32_t> fesc(S, 0);
+    // (row = the fail state's row, one more follow per column, then the state's
+    // own goto edges; the fail state precedes s in BFS order)
+    int col_of[256];
+    std::fill(std::begin(col_of), std::end(col_of), -1);
+    for (std::uint32_t c = 0; c < K; ++c)
+        if (col_byte[c] >= 0) col_of[col_byte[c]] = static_cast<int>(c);
     for (std::uint32_t s : nfa.bfs) {
         const std::size_t row = static_cast<std::size_t>(s) * K;
-        const std::size_t frow = static_cast<std::size_t>(nfa.fail[s]) * K;
-        for (std::uint32_t c = 0; c < K; ++c) {
-            const int b = col_byte[c];
-            StateId t;
-            if (b >= 0 && nfa.goto_transition(s, static_cast<std::uint8_t>(b), &t)) {
-                delta[row + c] = t;
-                fol[row + c] = 0;
-            } else if (s == 0) {
-                delta[row + c] = 0;
-                fol[row + c] = 0;
-            } else {
+        if (s == 0) {
+            std::fill_n(delta.begin() + row, K, 0u);
+            std::fill_n(fol.begin() + row, K, 0u);
+        } else {
+            const std::size_t frow = static_cast<std::size_t>(nfa.fail[s]) * K;
+            for (std::uint32_t c = 0; c < K; ++c) {
                 delta[row + c] = delta[frow + c];
                 fol[row + c] = 1 + fol[frow + c];  // reference follows one failure link, then retries
             }
+        }
+        for (std::uint32_t j = nfa.edge_off[s]; j < nfa.edge_off[s + 1]; ++j) {
+            const int c = col_of[nfa.edge_byte[j]];
+            if (c < 0) continue;  // (every pattern byte has a column)
+            delta[row + c] = nfa.edge_to[j];
+            fol[row + c] = 0;
         }
         fesc[s] = s == 0 ? 0 : 1 + fesc[nfa.fail[s]];
     }
