@@ -415,7 +415,7 @@ def main() -> None:
                    "scan_mode": mode_name, "excursion_event_rate": round(ev_rate, 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": {"sparse": "sparse_scan_kernel (K1s)", "filter": "qfilter_kernel (KQ)"}.get(
+                     "kernel": {"sparse": "sparse_scan_kernel (K1s)", "filter": "qfilter_ldg_kernel (KQ)"}.get(
                          mode_name, "exact_scan_kernel<COUNT> (K1x)"),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                      "algorithmic_bytes_per_launch": int(d_text.numel()),
