@@ -1,17 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark: Aho-Corasick text-scan throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--scaling weak|strong] [--mode auto|filter|sparse|exact]
 
-One step = one full pass of the hot path over the workload's text: K1 count
-pass, K2 record-slot prefix, K3 ordered record emission, K4 per-pattern counts
-(+ an NCCL all-reduce of the counts when N > 1). `value` is text GB/s with the
-text already resident in HBM; `e2e` is the same metric through the public
-scanner API from pinned host memory (H2D of the text and D2H of the counts and
-the match list inside the timed region). The workload is BASELINE.json
-configs[1] (1 GiB iid ACGT, 10,000 patterns of 16-64 bytes) unless --config
-says otherwise; with N GPUs every rank scans its own 1 GiB shard of one
-N GiB text (weak scaling, shards overlap by the automaton's halo).
+One step = one full pass of the hot path over the workload's text, producing
+the canonical (end, pattern id) match list and the per-pattern counts (+ an
+NCCL all-reduce of the counts when N > 1). `value` is text GB/s of the whole
+job with the text already resident in HBM, device-timed (CUDA events, max over
+ranks); `e2e` is the same metric through the public scanner API from pinned
+host memory (H2D of the text and D2H of the counts and the match list inside
+the timed region). The workload is BASELINE.json configs[1] (1 GiB iid ACGT,
+10,000 patterns of 16-64 bytes) unless --config says otherwise.
+
+Multi-GPU (one process per GPU): --scaling weak (default; cfg1) gives every
+rank its own 1 GiB shard of one N GiB text; --scaling strong (default for
+--config 2, BASELINE configs[2]) splits the config's text across the ranks
+(shards.shard_span, overlap = the automaton's halo). In both, the combined
+result of all ranks is checked: count, order-independent digest, order across
+rank boundaries, all-reduced per-pattern counts (and the reference's golden
+for the full-size strong split).
 
 --impl reference times the reference's own CPU scan (oracle/_ref, the
 unmodified reference headers compiled here) on the host cores: its only
@@ -36,6 +44,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+# one metric string for both arms (BASELINE.json "metric": text-scan GB/s); how
+# each arm is timed goes in its "timing" field
+METRIC = "AC text-scan GB/s"
 
 
 # per-stage labels of acg_scanner_kernel_ms by scan mode
@@ -215,6 +226,8 @@ def cpu_reference_single(w, concat, offs, sample_bytes: int) -> dict:
 
 
 def run_reference_arm(args, w, concat, offs) -> None:
+    """--impl reference: the reference's own CPU scan on the host cores (rank 0
+    only; other ranks exit without work), same metric / config as our arm."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -222,7 +235,7 @@ def run_reference_arm(args, w, concat, offs) -> None:
     cb = cpu_reference(w, concat, offs, args.cpu_sample_mib << 20, threads, args.steps, args.warmup)
     line = {
         "impl": "reference",
-        "metric": "AC text-scan GB/s",
+        "metric": METRIC,
         "value": round(cb["value"], 6),
         "unit": "GB/s",
         "n_gpus": args.gpus,
@@ -230,16 +243,24 @@ def run_reference_arm(args, w, concat, offs) -> None:
         "warmup": args.warmup,
         "ms_per_step": round(cb["seconds_per_step"] * 1e3, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling_of(args),
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
+        "timing": "host wall clock per step (std::chrono inside the reference's run)",
         "config": {"workload": w.name, "text_bytes": w.n, "patterns": w.patterns,
-                   "pattern_len": [w.len_lo, w.len_hi], "timed_sample_bytes": args.cpu_sample_mib << 20},
+                   "pattern_len": [w.len_lo, w.len_hi], "timed_sample_bytes": min(args.cpu_sample_mib << 20, w.n)},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": round(cb["value"], 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def scaling_of(args) -> str:
+    return args.scaling or ("strong" if args.config == 2 else "weak")
+
+
+MODE_NAMES = ("auto", "sparse", "exact", "filter")
 
 
 def main() -> None:
@@ -249,6 +270,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"])
     ap.add_argument("--cpu-sample-mib", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -258,7 +280,7 @@ def main() -> None:
     ap.add_argument("--profile-layout", action="store_true", help="profile-guided hot-state order")
     ap.add_argument("--text-mib", type=int, default=0, help="experiments: scale the workload's text (MiB)")
     ap.add_argument("--no-counts", action="store_true", help="experiments: match list only (no per-pattern counts)")
-    ap.add_argument("--mode", default="auto", choices=["auto", "sparse", "exact", "filter"])
+    ap.add_argument("--mode", default="auto", choices=list(MODE_NAMES))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -281,17 +303,23 @@ def main() -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    scaling = scaling_of(args)
 
-    # weak scaling: rank r owns [r*n, (r+1)*n) of a world*n byte text; the
-    # dictionary is the workload's (its substrings come from the first n bytes)
-    n = w.n
     a = am.Automaton.from_arrays(concat, offs)
     halo_guess = ((int((offs[1:] - offs[:-1]).max()) + 15) // 16) * 16
-    sh = shards.weak_shard(n, world, rank, halo_guess)
-    start, emit_from = sh.start, sh.emit_from
     from dataclasses import replace
-    wt = replace(w, n=world * n)
-    h_text = torch.empty(sh.window, dtype=torch.uint8, pin_memory=True)
+    if scaling == "weak":
+        # rank r owns [r*n, (r+1)*n) of a world*n byte text (the dictionary is the workload's)
+        sh = shards.weak_shard(w.n, world, rank, halo_guess)
+        wt = replace(w, n=world * w.n)
+        job_bytes = world * w.n
+    else:
+        # the config's text split across the ranks
+        sh = shards.shard_span(w.n, world, rank, halo_guess)
+        wt = w
+        job_bytes = w.n
+    owned = sh.hi - sh.lo
+    h_text = torch.empty(max(sh.window, 16), dtype=torch.uint8, pin_memory=True)
     synth.text(wt, sh.start, sh.hi, out=h_text.numpy())
     if args.profile_layout:
         a.optimize_layout(h_text.numpy()[: 1 << 20])
@@ -302,14 +330,15 @@ def main() -> None:
     flags = am.SCAN_LIST | am.SCAN_PROFILE | (0 if args.no_counts else am.SCAN_COUNTS)
     sc = am.Scanner(a, local, flags)
     sc.set_geometry(args.streams_per_thread, args.threads_per_block, args.chunk_bytes)
-    sc.set_mode({"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT,
-                 "filter": am.MODE_FILTER}[args.mode])
+    mode_req = {"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT,
+                "filter": am.MODE_FILTER}[args.mode]
+    sc.set_mode(mode_req)
     stream = torch.cuda.Stream()
     P = a.pattern_count()
     counts_all = torch.zeros(P, dtype=torch.int64, device="cuda")
 
     def step():
-        sc.run(d_text.data_ptr(), d_text.numel(), emit_from=emit_from, base_offset=start, stream=stream.cuda_stream)
+        shards.run_shard(sc, d_text.data_ptr(), sh, stream=stream.cuda_stream)
         if world > 1:
             sc.copy_pattern_counts(counts_all.data_ptr(), stream.cuda_stream)
             with torch.cuda.stream(stream):
@@ -319,8 +348,7 @@ def main() -> None:
     for _ in range(args.warmup):
         step()
         sc.sync()  # adaptive sizes settle (record buffer, survivor regions, slabs) before timing
-    m_total = sc.match_count()
-    k_ms = np.zeros(5)
+    replays0 = sc.replays()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -335,44 +363,75 @@ def main() -> None:
         ev1.record(stream)
         torch.cuda.synchronize()
     elapsed_ms = ev0.elapsed_time(ev1)
-    # per-kernel times from in-stream events: profiled steps right after the
-    # timed region, same scanner, stream and inputs
+    # the timed runs' own result: sync (a workspace overflow would replay the run
+    # here and show in the replay counter) and the size-independent checks
+    sc.sync()
+    timed_replayed = sc.replays() - replays0
+    m_local = sc.match_count()
+    dsum, dxor, unsorted = sc.digest()
+    edge = [int(x) for x in sc.copy_records(0, 1)] + [int(x) for x in sc.copy_records(m_local - 1, 1)] \
+        if m_local else []
+    if args.no_counts:
+        counts = np.zeros(P, dtype=np.uint64)
+    elif world > 1:
+        counts = counts_all.cpu().numpy().astype(np.uint64)  # all-reduced by the last timed step
+    else:
+        counts = sc.pattern_counts()
+    mode_name, ev_rate = sc.last_mode()
+    geo = sc.geometry()
+    # per-stage times: profiled steps right after the timed region (same scanner,
+    # stream, inputs and pipeline; CUDA events between the stages)
     sc.set_profiling(True)
-    k1 = []
+    k1, prof_step = [], []
     for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         step()
+        e1.record(stream)
         sc.sync()
         k1.append(sc.kernel_ms())
+        prof_step.append(e0.elapsed_time(e1))
     k_ms = np.mean(np.array(k1), axis=0)
+    prof_step_ms = float(np.mean(prof_step))
+    replays_prof = sc.replays() - replays0 - timed_replayed
     if world > 1:
         t = torch.tensor([elapsed_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
-    geo = sc.geometry()
-    mode_name, ev_rate = sc.last_mode()
     ms_per_step = elapsed_ms / args.steps
-    value = world * n / (ms_per_step * 1e-3) / 1e9
+    value = job_bytes / (ms_per_step * 1e-3) / 1e9
 
-    # correctness of the timed run (size-independent properties)
-    dsum, dxor, unsorted = sc.digest()
-    counts_local = sc.pattern_counts() if not args.no_counts else np.zeros(P, dtype=np.uint64)
-    mode_req = {"auto": am.MODE_AUTO, "sparse": am.MODE_SPARSE, "exact": am.MODE_EXACT, "filter": am.MODE_FILTER}[args.mode]
+    # the whole job's result (all ranks): count, digest, order across shards
+    mine = {"m": int(m_local), "dsum": int(dsum), "dxor": int(dxor), "unsorted": int(unsorted), "edge": edge,
+            "replayed": int(timed_replayed)}
+    parts = [mine]
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+    m_job = sum(p["m"] for p in parts)
+    dsum_job = sum(p["dsum"] for p in parts) % (1 << 64)
+    dxor_job = 0
+    for p in parts:
+        dxor_job ^= p["dxor"]
+    edges = [p["edge"] for p in parts if p["edge"]]
+    cross = sum(1 for x, y in zip(edges, edges[1:]) if not x[1] < y[0])
+    unsorted_job = sum(p["unsorted"] for p in parts) + cross
+    replayed_job = sum(p["replayed"] for p in parts)
     sc.__del__()  # release the timed scanner's workspace before the e2e scanner allocates its own
 
     # e2e: the public scanner API from pinned host memory, H2D + D2H inside
     sc_e2e = am.Scanner(a, local, am.SCAN_LIST | am.SCAN_COUNTS)
     sc_e2e.set_mode(mode_req)
     h_counts = np.empty(P, dtype=np.uint64)
-    for _ in range(1):
-        sc_e2e.run_host_ptr(h_text.data_ptr(), h_text.numel())
-        sc_e2e.sync()
+    sc_e2e.run_host_ptr(h_text.data_ptr(), sh.window)
+    sc_e2e.sync()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     d2h = 0
     for _ in range(args.e2e_steps):
-        sc_e2e.run_host_ptr(h_text.data_ptr(), h_text.numel())
+        sc_e2e.run_host_ptr(h_text.data_ptr(), sh.window)
         packed, _bits = sc_e2e.packed_records()
         h_counts[:] = sc_e2e.pattern_counts()
         d2h = packed.nbytes + h_counts.nbytes
@@ -381,10 +440,18 @@ def main() -> None:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * h_text.numel() / e2e_s / 1e9
+    e2e_value = job_bytes / e2e_s / 1e9
 
     hbm, src = peaks()
-    k1_ms = float(k_ms[0])
+    # roofline: algorithmic bytes of this rank's step = owned
+    # text read once + 8 B per match record written + 8 B per pattern count,
+    # over the device-timed step
+    alg_bytes = owned + 8 * m_local + 8 * P
+    achieved = alg_bytes / (ms_per_step * 1e-3) / 1e9
+    stage_names = STAGES.get(mode_name, STAGES["exact"])
+    kname = {"sparse": "sparse_scan_kernel (K1s)", "filter": "qfilter_ldg_kernel (KQ)"}.get(
+        mode_name, "exact_scan_kernel (K1x)")
+    k_top = float(k_ms[0])
     traffic = None
     tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tf):
@@ -392,9 +459,8 @@ def main() -> None:
             traffic = json.load(open(tf)).get(f"config{args.config}:{mode_name}")
         except Exception:
             traffic = None
-    achieved = d_text.numel() / (k1_ms * 1e-3) / 1e9
     line = {
-        "metric": "AC text-scan GB/s (device-timed)",
+        "metric": METRIC,
         "value": round(value, 3),
         "unit": "GB/s",
         "n_gpus": world,
@@ -402,40 +468,53 @@ def main() -> None:
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": w.name, "text_bytes_per_gpu": n, "patterns": P,
-                   "pattern_len": [w.len_lo, w.len_hi], "dfa_states": lay["states"], "hot_rows_smem": lay["hot_rows"],
-                   "alphabet": lay["alphabet"], "halo": lay["halo"], "chunks": geo["n_chunks"],
-                   "chunk_bytes": geo["chunk_bytes"], "matches_per_gpu": int(m_total),
-                   "l2": "text 1 GiB per GPU > 126 MB L2: no flush needed",
-                   "parallelism": f"text shards x{world} (halo {lay['halo']} B), DFA replicated",
-                   "scan_mode": mode_name, "excursion_event_rate": round(ev_rate, 5)},
+        "timing": "device: CUDA events on the scan stream around the timed steps, max over ranks",
+        "config": {"workload": w.name, "text_bytes_job": job_bytes, "text_bytes_rank0": owned, "patterns": P,
+                   "pattern_len": [w.len_lo, w.len_hi], "dfa_states": lay["states"],
+                   "hot_rows_smem": lay["hot_rows"], "alphabet": lay["alphabet"], "halo": lay["halo"],
+                   "chunks": geo["n_chunks"], "chunk_bytes": geo["chunk_bytes"], "matches_job": m_job,
+                   "l2": ("text per GPU > 126 MB L2: no flush needed" if owned > (126 << 20)
+                          else "text per GPU fits L2: no flush (small parity config)"),
+                   "parallelism": f"text shards x{world} ({scaling} scaling, halo {lay['halo']} B), DFA replicated",
+                   "scan_mode": mode_name, "mode_requested": args.mode,
+                   "excursion_event_rate": round(ev_rate, 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": {"sparse": "sparse_scan_kernel (K1s)", "filter": "qfilter_ldg_kernel (KQ)"}.get(
-                         mode_name, "exact_scan_kernel<COUNT> (K1x)"),
+                     "bytes": "SURVEY 8(d): owned text + 8*M + 8*P per step of rank 0",
+                     "algorithmic_bytes_per_step": int(alg_bytes),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                     "algorithmic_bytes_per_launch": int(d_text.numel()),
-                     "host_enqueue_ms_per_step": round(host_ms, 4),
-                     "stage_ms": dict(zip(STAGES.get(mode_name, STAGES["exact"]), (round(float(x), 4) for x in k_ms)))},
-        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h_text.numel()),
+                     "kernel": {"name": kname, "ms": round(k_top, 4),
+                                "achieved": round(owned / (k_top * 1e-3) / 1e9, 2) if k_top > 0 else None,
+                                "frac": round(owned / (k_top * 1e-3) / 1e9 / hbm, 4) if k_top > 0 else None,
+                                "bytes": "owned text bytes per launch (the kernel reads the text once)"},
+                     "stage_ms": dict(zip(stage_names, (round(float(x), 4) for x in k_ms))),
+                     "profiled_step_ms": round(prof_step_ms, 4),
+                     "host_enqueue_ms_per_step": round(host_ms, 4)},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(sh.window),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(geo["launches"]) * args.steps,
         "clocks": clk.summary(),
-        "check": {"digest_sum": dsum, "digest_xor": dxor, "unsorted_pairs": unsorted,
-                  "count_sum": int(counts_local.sum())},
+        "check": {"matches": m_job, "digest_sum": dsum_job, "digest_xor": dxor_job,
+                  "unsorted_pairs": unsorted_job, "count_sum": int(counts.sum()),
+                  "timed_runs_replayed": replayed_job, "profiled_runs_replayed": int(replays_prof)},
     }
-    if world == 1:
-        line["check"]["golden"] = golden_check(w, int(m_total), dsum, dxor, counts_local)
+    if scaling == "strong" or world == 1:
+        line["check"]["golden"] = golden_check(w, m_job, dsum_job, dxor_job, counts)
+    else:
+        line["check"]["golden"] = "no golden for the weak-scaled N GiB text (per-shard checks above)"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(w, concat, offs, args.cpu_sample_mib << 20, os.cpu_count(), 1, 0)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         single = cpu_reference_single(w, concat, offs, min(args.cpu_sample_mib, 16) << 20)
         if single:
             line["cpu_baseline"]["single_thread"] = {k: single[k] for k in ("value", "unit", "cores", "sample")}
+        if args.config == 0 and (os.cpu_count() or 1) != 16:  # BASELINE configs[0]: 1 and 16 threads
+            c16 = cpu_reference(w, concat, offs, args.cpu_sample_mib << 20, 16, 1, 0)
+            line["cpu_baseline"]["threads_16"] = {k: c16[k] for k in ("value", "unit", "cores", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

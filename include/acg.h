@@ -113,6 +113,9 @@ uint64_t acg_scanner_match_count(acg_scanner* s);            /* after sync */
 int acg_scanner_records(acg_scanner* s, uint32_t* ids, uint64_t* ends, uint64_t cap);   /* D2H + widen */
 int acg_scanner_packed_records(acg_scanner* s, uint64_t* host, uint64_t cap, uint32_t* id_bits);
 int acg_scanner_pattern_counts(acg_scanner* s, uint64_t* host_counts);           /* P entries */
+/* Packed records [first, first+count) of the list (a window of it; e.g. to
+ * stream a long list out in pieces). ACG_ERR_INVALID past the list's end. */
+int acg_scanner_copy_records(acg_scanner* s, uint64_t first, uint64_t count, uint64_t* host_packed);
 /* device pointers (valid until the next run / destroy) */
 const uint64_t* acg_scanner_device_pattern_counts(acg_scanner* s);
 const uint64_t* acg_scanner_device_records(acg_scanner* s, uint32_t* id_bits);
@@ -147,6 +150,10 @@ int acg_scanner_last_mode(acg_scanner* s, double* event_rate);
 /* Copies the P per-pattern counts (u64) into a caller device buffer, enqueued
  * on `stream` (NULL = the stream of the last run) — e.g. for an NCCL all-reduce. */
 int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream);
+/* Number of runs this scanner had to replay (or re-emit) at sync because a
+ * workspace buffer sized from earlier runs overflowed; results are exact
+ * either way. A benchmark checks it is unchanged across its timed runs. */
+uint64_t acg_scanner_replays(const acg_scanner* s);
 /* Geometry of the last run: chunks, chunk bytes, and launches issued. */
 int acg_scanner_last_geometry(acg_scanner* s, uint64_t* n_chunks, uint64_t* chunk_bytes, uint32_t* launches);
 /* Filter-mode eligibility (diagnostics): returns 1 when the sampled q-gram

@@ -51,11 +51,13 @@ ACG_SYMBOLS = {
     "acg_scanner_records": (C.c_int, [vp, vp, vp, C.c_uint64]),
     "acg_scanner_packed_records": (C.c_int, [vp, vp, C.c_uint64, u32p]),
     "acg_scanner_pattern_counts": (C.c_int, [vp, vp]),
+    "acg_scanner_copy_records": (C.c_int, [vp, C.c_uint64, C.c_uint64, vp]),
     "acg_scanner_device_pattern_counts": (vp, [vp]),
     "acg_scanner_device_records": (vp, [vp, u32p]),
     "acg_scanner_failure_follows": (C.c_uint64, [vp]),
     "acg_scanner_digest": (C.c_int, [vp, u64p, u64p, u64p]),
     "acg_scanner_last_geometry": (C.c_int, [vp, u64p, u64p, u32p]),
+    "acg_scanner_replays": (C.c_uint64, [vp]),
     "acg_scanner_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
     "acg_scanner_copy_pattern_counts": (C.c_int, [vp, vp, vp]),
     "acg_scanner_set_mode": (C.c_int, [vp, C.c_int]),

@@ -316,6 +316,12 @@ class Scanner:
         _check(_lib.acg().acg_scanner_packed_records(self._h, out.ctypes.data_as(C.c_void_p), m, C.byref(bits)))
         return out, bits.value
 
+    def copy_records(self, first: int, count: int) -> np.ndarray:
+        """Packed records [first, first+count) of the list (acg_scanner_copy_records)."""
+        out = np.empty(count, dtype=np.uint64)
+        _check(_lib.acg().acg_scanner_copy_records(self._h, first, count, out.ctypes.data_as(C.c_void_p)))
+        return out
+
     def pattern_counts(self) -> np.ndarray:
         out = np.empty(self.automaton.pattern_count(), dtype=np.uint64)
         _check(_lib.acg().acg_scanner_pattern_counts(self._h, out.ctypes.data_as(C.c_void_p)))
@@ -357,6 +363,10 @@ class Scanner:
 
     def copy_pattern_counts(self, d_dst_ptr: int, stream: int = 0) -> None:
         _check(_lib.acg().acg_scanner_copy_pattern_counts(self._h, C.c_void_p(d_dst_ptr), C.c_void_p(stream or None)))
+
+    def replays(self) -> int:
+        """Runs replayed at sync after a workspace overflow (acg_scanner_replays)."""
+        return int(_lib.acg().acg_scanner_replays(self._h))
 
     def geometry(self) -> dict:
         nc, cb, la = C.c_uint64(), C.c_uint64(), C.c_uint32()

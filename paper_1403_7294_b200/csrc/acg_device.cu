@@ -246,6 +246,7 @@ struct acg_scanner {
     unsigned grid = 0;
     bool have_run = false;
     bool synced = false;
+    unsigned long long replays = 0;  // sync-time re-runs / re-emissions (an overflowed buffer was regrown)
     unsigned long long m_total = 0;
     // tuning
     std::uint32_t U = 0, tpb = acg::kern::kTPB;  // U = 0: per-mode default
@@ -490,8 +491,11 @@ cudaError_t launch_sparse_u(std::uint32_t U, const ScanArgs& args, unsigned grid
 std::size_t smem_bytes(const DeviceDfa& dd) { return dd.hot_bytes + 256; }
 std::size_t smem_sparse(const DeviceDfa& dd) { return dd.hotH_bytes; }
 
-// Filter mode: KQ geometry.
 constexpr unsigned long long kTaskBudget = 48ull << 30;
+// sparse mode: walk offsets (halo + chunk) are 17-bit fields of the K1s events
+// and F1 tasks; a chunk is at least kSparseMinChunk bytes
+constexpr unsigned long long kSparseMaxWalk = 1ull << 17;
+constexpr unsigned long long kSparseMinChunk = 256 + 64;
 constexpr double kSparseMaxEventRate = 0.005;
 constexpr std::uint32_t kHistMaxPatterns = 56 * 1024;  // record histogram: u32 bins in shared memory  // AUTO: sparse mode below this event rate
 constexpr unsigned long long kScratchBudget = 64ull << 30;  // exact-mode single-pass slabs (bytes)
@@ -681,7 +685,7 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     // sparse mode: walk length (halo + chunk) a multiple of the 64-byte refill
     // (an explicit chunk override is kept as is: odd walks take the per-byte path)
     if (s->mode_run == ACG_MODE_SPARSE) {
-        chunk = std::min<unsigned long long>(chunk, (1ull << 17) - halo - 64);  // event offsets are 17-bit
+        chunk = std::min<unsigned long long>(chunk, kSparseMaxWalk - halo - 64);  // event offsets are 17-bit
         if (!s->chunk_override) chunk = ((chunk + halo + 63) & ~63ull) - halo;
     }
     s->chunk = chunk;
@@ -769,7 +773,11 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if (mode == ACG_MODE_FILTER && !filter_ok) mode = ACG_MODE_AUTO;
     if (mode == ACG_MODE_AUTO && filter_ok && (s->last_filter_rate < 0 || s->last_filter_rate < 1.0 / 256))
         mode = ACG_MODE_FILTER;
-    if (stats || (mode != ACG_MODE_FILTER && !d.sparse_ok)) mode = ACG_MODE_EXACT;
+    // sparse mode's event log and fix-up tasks carry 17-bit walk offsets
+    // (scan_kernels.cuh: K1s events, F1 tasks): walks of halo + chunk bytes must
+    // fit, so a dictionary with a pattern longer than ~128 KiB runs EXACT
+    const bool sparse_walk_ok = d.sparse_ok && static_cast<unsigned long long>(d.halo) + kSparseMinChunk <= kSparseMaxWalk;
+    if (stats || (mode != ACG_MODE_FILTER && !sparse_walk_ok)) mode = ACG_MODE_EXACT;
     if (mode == ACG_MODE_AUTO)
         // measured on the BASELINE configs: sparse wins at 8.5e-4 events per walked
         // byte (cfg0: 3x faster than exact) and loses badly at 0.025 (cfg4) and
@@ -823,7 +831,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     a.emit_from = static_cast<long long>(emit_from);
     a.base = base;
     a.chunk = static_cast<long long>(s->chunk);
-    a.halo = static_cast<int>(d.halo);
+    a.halo = static_cast<long long>(d.halo);
     a.n_chunks = static_cast<long long>(s->n_chunks);
     a.next = dd.next.p;
     a.hot16 = dd.hot16.p;
@@ -910,17 +918,16 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             const std::uint32_t mcap = std::max<std::uint32_t>(64, s->min_mcap);
             s->last_mcap = mcap;
             ACG_CUDA(s->qscratch.reserve(static_cast<std::size_t>(W) * mcap, st));
-            ACG_CUDA(s->qreg_n.reserve(2ull * W, st));
+            ACG_CUDA(s->qreg_n.reserve(W, st));
             ACG_CUDA(s->qscal.reserve(2, st));
             zero_later(s, s->qscal.p, 2 * sizeof(std::uint32_t));
             a.qscratch = s->qscratch.p;
             a.mcap = mcap;
             a.qreg = static_cast<long long>(s->chunk);
             a.reg_n = s->qreg_n.p;
-            a.reg_hi = s->qreg_n.p + W;
             a.qscal = s->qscal.p;
             if (qfilter_fused(a)) {  // V1 runs inside KQ: its region counters start at zero
-                zero_later(s, s->qreg_n.p, 2ull * W * sizeof(std::uint32_t));
+                zero_later(s, s->qreg_n.p, W * sizeof(std::uint32_t));
                 ACG_CUDA(flush_zeros(s, st));
                 ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
                 if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
@@ -1105,6 +1112,7 @@ int scanner_sync(acg_scanner* s) {
                 s->min_task_cap = 0;
                 s->last_event_rate = 1.0;  // AUTO: exact from now on
             }
+            ++s->replays;
             const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
             s->mode_req = req;
             if (rc) return rc;
@@ -1123,6 +1131,7 @@ int scanner_sync(acg_scanner* s) {
             else s->min_mcap = slab_max + slab_max / 4 + 32;
             const int req = s->mode_req;
             s->mode_req = ACG_MODE_FILTER;
+            ++s->replays;
             const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
             s->mode_req = req;
             if (rc) return rc;
@@ -1135,6 +1144,7 @@ int scanner_sync(acg_scanner* s) {
             s->min_task_cap = worst + worst / 4 + 64;
             const int req = s->mode_req;
             s->mode_req = ACG_MODE_FILTER;
+            ++s->replays;
             const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
             s->mode_req = req;
             if (rc) return rc;
@@ -1168,6 +1178,7 @@ int scanner_sync(acg_scanner* s) {
     if ((s->flags & ACG_SCAN_LIST) && s->m_total > s->records.n) {
         // record buffer overflowed: grow and re-emit (chunk counts and offsets are final)
         ACG_CUDA(s->records.reserve(s->m_total + s->m_total / 4, st));
+        ++s->replays;
         s->regrow = true;
         const int rc = enqueue_write(s, st);
         s->regrow = false;
@@ -1347,6 +1358,8 @@ int acg_build(const std::uint8_t* concat, const std::uint64_t* offsets, std::uin
             return fail(rc, "pattern " + std::to_string(i) + " is empty");
         }
         if (rc == acg::kErrEmptyDictionary) return fail(rc, "dictionary is empty");
+        if (rc == acg::kErrTooLarge)
+            return fail(ACG_ERR_INVALID, "dictionary of 4 GiB or more: its trie would exceed 32-bit state ids");
         if (rc != acg::kOk) return fail(rc, "invalid dictionary");
         std::lock_guard<std::mutex> lock(a->mu);
         host_dfa_locked(a.get(), kSm100SmemOptin);
@@ -1522,6 +1535,18 @@ int acg_scanner_packed_records(acg_scanner* s, std::uint64_t* host, std::uint64_
     return ACG_OK;
 }
 
+int acg_scanner_copy_records(acg_scanner* s, std::uint64_t first, std::uint64_t count, std::uint64_t* host) {
+    if (!s || (!host && count)) return fail(ACG_ERR_INVALID, "null argument");
+    if (!(s->flags & ACG_SCAN_LIST)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_LIST");
+    if (const int rc = scanner_sync(s)) return rc;
+    if (first > s->m_total || count > s->m_total - first) return fail(ACG_ERR_INVALID, "record range beyond the match list");
+    if (count) {
+        ACG_CUDA(cudaMemcpyAsync(host, s->records.p + first, count * sizeof(std::uint64_t), cudaMemcpyDeviceToHost, s->last));
+        ACG_CUDA(cudaStreamSynchronize(s->last));
+    }
+    return ACG_OK;
+}
+
 int acg_scanner_records(acg_scanner* s, std::uint32_t* ids, std::uint64_t* ends, std::uint64_t cap) {
     if (!s) return fail(ACG_ERR_INVALID, "null scanner");
     if (const int rc = scanner_sync(s)) return rc;
@@ -1627,6 +1652,8 @@ int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream) {
                              cudaMemcpyDeviceToDevice, st));
     return ACG_OK;
 }
+
+std::uint64_t acg_scanner_replays(const acg_scanner* s) { return s ? s->replays : 0; }
 
 int acg_scanner_last_geometry(acg_scanner* s, std::uint64_t* n_chunks, std::uint64_t* chunk_bytes,
                               std::uint32_t* launches) {

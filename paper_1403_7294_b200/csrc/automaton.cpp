@@ -82,11 +82,11 @@ int build_nfa(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32
     for (std::uint32_t i = 0; i < count; ++i) {
         const std::uint64_t len = offs[i + 1] - offs[i];
         if (len == 0) return kErrEmptyPattern;  // :133-134
-        if (len > 0xFFFFFFull) return kErrInvalid;
         total += len;
         max_len = std::max<std::uint32_t>(max_len, static_cast<std::uint32_t>(len));
     }
-    if (total >= 0xFFFFFFF0ull) return kErrInvalid;
+    // states are u32 (StateId, aho_corasick.hpp:18): up to total + 1 of them
+    if (total >= 0xFFFFFFF0ull) return kErrTooLarge;
 
     // Phase 1: keyword trie, children in insertion order.
     std::vector<std::uint32_t> first_kid(1, 0), next_sib(1, 0), last_kid(1, 0), tdepth(1, 0);

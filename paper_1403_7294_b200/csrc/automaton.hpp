@@ -51,6 +51,7 @@ enum : int {
     kErrCuda = 5,
     kErrOutOfMemory = 6,
     kErrNoDevice = 7,
+    kErrTooLarge = 8,  // dictionary of >= 4 GiB: more states than a u32 StateId numbers (maps to kErrInvalid)
 };
 
 // build: reference aho_corasick.hpp:130-233. Returns an error code.

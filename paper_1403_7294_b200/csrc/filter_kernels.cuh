@@ -83,7 +83,8 @@ __device__ __forceinline__ bool qmatch(const ScanArgs& a, long long i, std::uint
     return true;
 }
 
-// Confirms survivor slot t (region w) exactly and appends its matches to w's slab.
+// Confirms survivor slot t (found in region w) exactly and appends each match
+// to the slab of the region its end lies in.
 __device__ __forceinline__ void qconfirm_slot(const ScanArgs& a, long long w, unsigned long long t) {
     const std::uint32_t tmask = (1u << a.qtab_bits) - 1u;
     const long long j = static_cast<long long>(__ldcg(a.qcands + t));
@@ -100,7 +101,7 @@ __device__ __forceinline__ void qconfirm_slot(const ScanArgs& a, long long w, un
         slot = (slot + 1) & tmask;
     }
     if (bucket == kQEmpty) return;
-    const long long rend = (w + 1) * a.qreg;
+    const long long wlast = static_cast<long long>(a.qwarps) - 1;
     const bool single = bucket & kQSingle;
     const std::uint32_t e0 = single ? 0u : a.qb_off[bucket], e1 = single ? 1u : a.qb_off[bucket + 1];
     for (std::uint32_t e = e0; e < e1; ++e) {
@@ -116,11 +117,13 @@ __device__ __forceinline__ void qconfirm_slot(const ScanArgs& a, long long w, un
         // whole pattern byte by byte
         const ulonglong2 pc = *reinterpret_cast<const ulonglong2*>(a.pat_code + 2ull * p);
         if (!qwin_match(win, static_cast<int>(i - (j & ~15LL)), len, pc.x, pc.y) || !qmatch(a, i, lo, len)) continue;
-        const std::uint32_t k = atomicAdd(a.reg_n + w, 1u);
+        // filed under the region holding its END (any pattern length: a long
+        // occurrence found from region w's survivors may end many regions on)
+        const long long d = min(end / a.qreg, wlast);
+        const std::uint32_t k = atomicAdd(a.reg_n + d, 1u);
         if (k < a.mcap)
-            a.qscratch[static_cast<unsigned long long>(w) * a.mcap + k] =
+            a.qscratch[static_cast<unsigned long long>(d) * a.mcap + k] =
                 ((a.base + static_cast<unsigned long long>(end)) << a.id_bits) | p;
-        if (end >= rend) atomicAdd(a.reg_hi + w, 1u);
         if (a.pcounts) atomicAdd(a.pcounts + p, 1ull);
     }
 }
@@ -281,7 +284,7 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
     if (lane == 0) {
         const std::uint32_t found = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
         a.qwarp_n[gw] = found;
-        if (!FUSED && a.reg_n) a.reg_n[gw] = a.reg_hi[gw] = 0u;  // V1's per-region counters
+        if (!FUSED && a.reg_n) a.reg_n[gw] = 0u;  // V1's per-region counters
         atomicAdd(a.qcand_n, found);
         atomicMax(a.qcand_max, static_cast<unsigned long long>(found));
         if (FUSED) {
@@ -360,11 +363,7 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
     return v;
 }
 
-// V1: confirms every survivor exactly (the q-gram's (pattern, offset)
-// bucket, then a byte compare at i = j - offset); threads stride over the
-// survivor regions' slots. A match found from region w's survivors ends in
-// w or, at most 63 bytes on, in w + 1 (reg_hi counts those); it is appended
-// to w's slab (reg_n[w], zeroed by KQ, counts them even past the capacity).
+
 template <int NW, int R, bool L2F, bool FUSED>
 __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_kernel(const ScanArgs a) {
     __shared__ std::uint32_t wcnt[NW], pub[NW], done_sh[NW], nfin;
@@ -387,6 +386,12 @@ __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_ke
     }
 }
 
+// V1: confirms every survivor exactly (the q-gram's (pattern, offset)
+// bucket, then a byte compare at i = j - offset); threads stride over the
+// survivor regions' slots. Each match is appended to the slab of the region
+// holding its end (reg_n[d], zeroed by KQ, counts them even past the
+// capacity), so every slab holds exactly its region's matches whatever the
+// pattern length.
 __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) {
     const long long total = static_cast<long long>(a.qwarps) * a.qcand_cap;
     for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
@@ -398,12 +403,11 @@ __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) 
 }
 
 // ORDER: one warp per region. Its slot range starts at the sum of the
-// matches owned by earlier regions (summed directly from reg_n / reg_hi: no
-// separate scan pass); it gathers its matches (its own slab's entries ending
-// in it, the previous slab's ending past that region) and sorts them: one
-// bitonic round in registers for <= 32, a warp bitonic sort in shared memory
-// for <= kQOrderMax; a bigger region sets qscal[1] and the host replays the
-// run through the per-chunk pipeline (V0/K2/K3).
+// matches owned by earlier regions (summed directly from reg_n: no separate
+// scan pass); it reads its slab (every match ending in the region) and sorts
+// it: one bitonic round in registers for <= 32, a warp bitonic sort in shared
+// memory for <= kQOrderMax; a bigger region sets qscal[1] and the host replays
+// the run through the per-chunk pipeline (V0/K2/K3).
 constexpr int kQOrderMax = 1024;
 constexpr int kQOrderWarps = 4;
 
@@ -429,12 +433,9 @@ __global__ void __launch_bounds__(32 * kQOrderWarps) qorder_region_kernel(const 
     }
     __syncthreads();
     if (w >= W) return;
-    unsigned long long sum = part[0] + part[1] + part[2] + part[3];
-    for (long long v = w0; v < w; ++v) sum += a.reg_n[v];  // this CTA's earlier regions (< 4)
-    const std::uint32_t hprev = w > 0 ? a.reg_hi[w - 1] : 0u;
-    const std::uint32_t nw = min(a.reg_n[w], a.mcap), np = w > 0 ? min(a.reg_n[w - 1], a.mcap) : 0u;
-    const unsigned long long off = sum - hprev;
-    const std::uint32_t own = a.reg_n[w] - a.reg_hi[w] + hprev;
+    unsigned long long off = part[0] + part[1] + part[2] + part[3];
+    for (long long v = w0; v < w; ++v) off += a.reg_n[v];  // this CTA's earlier regions (< 4)
+    const std::uint32_t own = a.reg_n[w];
     if (lane == 0) {
         if (a.reg_n[w] > a.mcap) atomicMax(a.qscal, a.reg_n[w]);  // slab overflow: the host re-runs
         offs[w] = off;
@@ -445,40 +446,18 @@ __global__ void __launch_bounds__(32 * kQOrderWarps) qorder_region_kernel(const 
         if (lane == 0) atomicMax(a.qscal + 1, own);
         return;
     }
-    const long long rlo = w * a.qreg, rhi = rlo + a.qreg;
+    if (own > a.mcap) return;  // slab overflowed: the host re-runs with larger slabs
     const unsigned long long* sw = a.qscratch + static_cast<unsigned long long>(w) * a.mcap;
-    const unsigned long long* sp = sw - a.mcap;
     unsigned long long* b = buf[wl];
-    const unsigned lt = (1u << lane) - 1u;
-    std::uint32_t pos = 0;
-    auto gather = [&](const unsigned long long* src, std::uint32_t cntv, bool own_slab) {
-        for (std::uint32_t base = 0; base < cntv; base += 32) {
-            const std::uint32_t idx = base + lane;
-            unsigned long long key = 0;
-            bool take = false;
-            if (idx < cntv) {
-                key = src[idx];
-                const long long end = static_cast<long long>((key >> a.id_bits) - a.base);
-                take = own_slab ? end < rhi : end >= rlo;
-            }
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
-            if (take) {
-                const std::uint32_t at = pos + __popc(m & lt);
-                if (at < static_cast<std::uint32_t>(kQOrderMax)) b[at] = key;
-            }
-            pos += __popc(m);
-        }
-    };
-    if (w > 0 && hprev) gather(sp, np, false);
-    gather(sw, nw, true);
-    __syncwarp();
-    const std::uint32_t k = min(pos, static_cast<std::uint32_t>(kQOrderMax));
+    const std::uint32_t k = own;
     if (k <= 32) {
-        unsigned long long v = lane < static_cast<int>(k) ? b[lane] : ~0ull;
+        unsigned long long v = lane < static_cast<int>(k) ? sw[lane] : ~0ull;
         v = bitonic32(v, lane);
         if (lane < static_cast<int>(k) && off + lane < a.rec_cap) a.records[off + lane] = v;
         return;
     }
+    for (std::uint32_t t = lane; t < k; t += 32) b[t] = sw[t];
+    __syncwarp();
     std::uint32_t p2 = 64;
     while (p2 < k) p2 <<= 1;
     for (std::uint32_t t = k + lane; t < p2; t += 32) b[t] = ~0ull;

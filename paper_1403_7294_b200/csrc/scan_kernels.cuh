@@ -66,7 +66,7 @@ struct ScanArgs {
     long long emit_from;       // first owned byte (multiple of 16)
     unsigned long long base;   // global offset of text[0] (added to record ends)
     long long chunk;           // owned bytes per chunk (multiple of 16)
-    int halo;                  // warm-up bytes (multiple of 16)
+    long long halo;            // warm-up bytes (multiple of 16)
     long long n_chunks;
     // DFA
     const std::uint32_t* next;     // S*K exact transitions (device ids)
@@ -133,8 +133,7 @@ struct ScanArgs {
     // filter mode, region pipeline (V1 + ORDER): KQ warp w's region of the
     // buffer [w*qreg, (w+1)*qreg) owns the matches that END in it
     long long qreg;                         // region bytes (multiple of 2048)
-    std::uint32_t* reg_n;                   // per region: matches confirmed from its survivors
-    std::uint32_t* reg_hi;                  // ... of which end in the next region
+    std::uint32_t* reg_n;                   // per region: confirmed matches that end in it
     std::uint32_t mcap;                     // per-region slab capacity (qscratch)
     std::uint32_t* qscal;                   // [0] max reg_n (overflow), [1] regions too big for ORDER
     // exact mode, single pass (kScratch): chunk c's slab is scratch[c*scap, (c+1)*scap),

@@ -80,30 +80,44 @@ def gather_matches(ids, ends, group=None, dst: int = 0):
     """Host gather of the per-rank match lists to rank `dst`, concatenated in
     rank order (= canonical order, since owned end ranges ascend with rank).
     ids/ends: 1-D torch tensors (uint32-compatible int64 / int64) on the
-    collective's device. Returns (ids, ends) numpy arrays on `dst`, None on
-    the other ranks."""
+    collective's device. Only `dst` receives list data: the list sizes are
+    all-gathered (one int64 per rank), then every other rank sends its exact
+    (2, k) slice point-to-point. Returns (ids, ends) numpy arrays on `dst`,
+    None on the other ranks."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
         return ids.cpu().numpy().astype(np.uint32), ends.cpu().numpy().astype(np.uint64)
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
+    if dist.get_backend(group) == "gloo":  # gloo's point-to-point path takes host tensors
+        ids, ends = ids.cpu(), ends.cpu()
     dev = ids.device
     n_local = torch.tensor([ids.numel()], dtype=torch.int64, device=dev)
     sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, n_local, group=group)
     sizes = [int(s.item()) for s in sizes]
-    cap = max(max(sizes), 1)
-    packed = torch.zeros(2, cap, dtype=torch.int64, device=dev)
-    packed[0, : ids.numel()] = ids.to(torch.int64)
-    packed[1, : ends.numel()] = ends.to(torch.int64)
-    parts = [torch.empty_like(packed) for _ in range(world)]
-    dist.all_gather(parts, packed, group=group)
+    ranks = list(range(world)) if group is None else dist.get_process_group_ranks(group)
     if me != dst:
+        if sizes[me]:
+            mine = torch.stack([ids.to(torch.int64), ends.to(torch.int64)])
+            dist.send(mine.contiguous(), dst=ranks[dst], group=None)
         return None
-    out_ids = np.concatenate([p[0, :k].cpu().numpy() for p, k in zip(parts, sizes)]).astype(np.uint32)
-    out_ends = np.concatenate([p[1, :k].cpu().numpy() for p, k in zip(parts, sizes)]).astype(np.uint64)
-    return out_ids, out_ends
+    out_ids, out_ends = [], []
+    for r in range(world):
+        k = sizes[r]
+        if r == me:
+            out_ids.append(ids.cpu().numpy())
+            out_ends.append(ends.cpu().numpy())
+        elif k:
+            buf = torch.empty(2, k, dtype=torch.int64, device=dev)
+            dist.recv(buf, src=ranks[r], group=None)
+            b = buf.cpu().numpy()
+            out_ids.append(b[0])
+            out_ends.append(b[1])
+    if not out_ids:
+        return np.zeros(0, np.uint32), np.zeros(0, np.uint64)
+    return np.concatenate(out_ids).astype(np.uint32), np.concatenate(out_ends).astype(np.uint64)
 
 
 def run_shard(scanner, d_window_ptr: int, shard: Shard, stream: int = 0) -> None:
