@@ -148,7 +148,10 @@ int acg_scanner_set_mode(acg_scanner* s, int mode);
  * text byte (-1 before the first sync of that mode). */
 int acg_scanner_last_mode(acg_scanner* s, double* event_rate);
 /* Copies the P per-pattern counts (u64) into a caller device buffer, enqueued
- * on `stream` (NULL = the stream of the last run) — e.g. for an NCCL all-reduce. */
+ * on `stream` (NULL = the stream of the last run) — e.g. for an NCCL all-reduce.
+ * Enqueued without a host wait: if the run is later replayed at sync (an
+ * overflowed workspace; acg_scanner_replays grows), copy again after the sync.
+ * Repeating a synced run on the same input does not replay. */
 int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream);
 /* Number of runs this scanner had to replay (or re-emit) at sync because a
  * workspace buffer sized from earlier runs overflowed; results are exact

@@ -50,6 +50,7 @@ def _worker(rank: int, world: int, port: int, out_dir: str, cfg: int, n: int, mo
         stream = torch.cuda.Stream()
         counts = torch.zeros(a.pattern_count(), dtype=torch.int64, device="cuda")
         shards.run_shard(sc, d_text.data_ptr(), sh, stream=stream.cuda_stream)
+        sc.sync()  # a first run may replay at sync (workspace sizing): counts are final after it
         sc.copy_pattern_counts(counts.data_ptr(), stream.cuda_stream)
         stream.synchronize()
         shards.reduce_counts(counts)
