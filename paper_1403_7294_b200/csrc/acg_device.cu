@@ -26,6 +26,7 @@
 #include "automaton.hpp"
 #include "scan_kernels.cuh"
 #include "filter_kernels.cuh"
+#include "exact_kernels.cuh"
 
 namespace {
 
@@ -290,6 +291,14 @@ struct acg_scanner {
     bool hist_run = false;  // per-pattern counts by a histogram of the records (exact mode with a list)
     bool hist_fused = false;  // ... taken by the slab copy (+ K4 over the re-walked chunks' visits)
     DevBuf<unsigned long long> scratch;
+    // exact mode, event pipeline (exact_kernels.cuh): event slabs + pool, per-chunk
+    // event counts, per-chunk slab offsets, pool counter; the last event run's
+    // geometry and totals size the next one's slabs
+    DevBuf<std::uint32_t> xev, xev_count, xev_slab, xev_pool;
+    acg::kern::EventArgs eargs{};
+    bool ev_run = false;
+    unsigned long long xev_chunk = 0, xev_chunks = 0, xev_total = 0, xev_n = 0;
+    std::uint32_t xev_min_pool = 0;
     DevBuf<std::uint32_t> events, ev_count, cands, cand_n, cand_list, cand_cnt, tasks, task_cnt;
     std::uint32_t ev_cap = 0;
     // optional per-kernel timing (ACG_SCAN_PROFILE)
@@ -431,6 +440,33 @@ cudaError_t launch_exact_pass(int alpha, int pass, bool stats, std::uint32_t U, 
                             : launch_exact_u<1, kScratch>(U, args, grid, tpb, smem, st);
 }
 
+template <int U, int MODE>
+cudaError_t launch_event(const ScanArgs& a, const acg::kern::EventArgs& e, unsigned grid, unsigned tpb,
+                         std::size_t smem, cudaStream_t st) {
+    auto k = acg::kern::exact_event_kernel<U, MODE>;
+    if (cudaError_t err = prepare_smem(k, smem)) return err;
+    k<<<grid, tpb, smem, st>>>(a, e);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_event_walk(int alpha, std::uint32_t U, const ScanArgs& a, const acg::kern::EventArgs& e,
+                              unsigned grid, unsigned tpb, std::size_t smem, cudaStream_t st) {
+    if (alpha == acg::kAlphaDna4) {
+        switch (U) {
+            case 1: return launch_event<1, 0>(a, e, grid, tpb, smem, st);
+            case 2: return launch_event<2, 0>(a, e, grid, tpb, smem, st);
+            case 8: return launch_event<8, 0>(a, e, grid, tpb, smem, st);
+            default: return launch_event<4, 0>(a, e, grid, tpb, smem, st);
+        }
+    }
+    switch (U) {
+        case 1: return launch_event<1, 1>(a, e, grid, tpb, smem, st);
+        case 4: return launch_event<4, 1>(a, e, grid, tpb, smem, st);
+        case 8: return launch_event<8, 1>(a, e, grid, tpb, smem, st);
+        default: return launch_event<2, 1>(a, e, grid, tpb, smem, st);
+    }
+}
+
 constexpr unsigned sparse_tpb(unsigned U) { return U == 1 ? 1024u : 512u; }
 
 template <int U>
@@ -565,7 +601,7 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
     using namespace acg::kern;
     const DeviceDfa& dd = *s->dd;
     ACG_CUDA(cudaMemsetAsync(s->scalars32.p, 0, sizeof(std::uint32_t), st));
-    if (s->mode_run != ACG_MODE_FILTER && !s->scratch_run) {  // (filter mode sweeps the chunk offsets itself)
+    if (s->mode_run != ACG_MODE_FILTER && !s->scratch_run && !s->ev_run) {  // (filter mode sweeps the chunk offsets itself)
         const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((s->n_chunks + 2047) / 2048, 1024ull));
         compact_active_kernel<<<std::max(g, 1u), 256, 0, st>>>(s->chunk_counts.p, static_cast<long long>(s->n_chunks),
                                                                s->active_list.p, s->scalars32.p);
@@ -614,6 +650,12 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         const unsigned g = static_cast<unsigned>(std::max<unsigned long long>(
             1, std::min<unsigned long long>((s->n_chunks + 255) / 256, static_cast<unsigned long long>(dd.num_sms))));
         k<<<g, 256, smem_sparse(dd), st>>>(wa);
+        ACG_CUDA(cudaGetLastError());
+    } else if (s->ev_run) {
+        // E2: events -> ordered records at each chunk's slot range
+        const unsigned g = static_cast<unsigned>(
+            std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 16ull * dd.num_sms)));
+        acg::kern::event_expand_kernel<<<g, 256, 0, st>>>(wa, s->eargs);
         ACG_CUDA(cudaGetLastError());
     } else if (s->scratch_run) {
         // slabs -> slot ranges; overflowed chunks are re-walked by the WRITE pass.
@@ -741,6 +783,81 @@ cudaError_t adopt_stream(acg_scanner* s, cudaStream_t st) {
     return cudaSuccess;
 }
 
+// Event pipeline eligibility: an event packs the owned offset in its chunk and
+// the output rank into 32 bits; the exact ScanStats walk keeps its own kernel.
+// ACG_EXACT_EVENTS=0 keeps the inline-emission walk (experiments).
+constexpr std::size_t kEventBinsMax = 200 * 1024;  // E1 visit bins in shared memory up to this
+unsigned bits_for(unsigned long long v) {
+    unsigned b = 1;
+    while (b < 63 && (1ull << b) < v) ++b;
+    return b;
+}
+bool event_slots_ok(const acg_scanner* s, std::uint32_t n_out, bool stats) {
+    static const bool on = [] {
+        const char* e = std::getenv("ACG_EXACT_EVENTS");
+        return !(e && e[0] == '0');
+    }();
+    return on && !stats && n_out > 0 && bits_for(n_out) + bits_for(s->chunk) <= 32;
+}
+
+// Event slabs for this run: per chunk from the previous event run's counts
+// when the geometry repeats (exact + 1/8 + 17 slots), else uniform from its
+// density (x 1.25 + 17; chunk/16 + 33 without history); overflow goes to the
+// 256-event block pool (a pool overflow replays the run at sync).
+cudaError_t plan_events(acg_scanner* s, std::uint32_t n_out, cudaStream_t st) {
+    using acg::kern::kEvBlock;
+    const unsigned long long nc = s->n_chunks, owned = s->run_n - s->run_emit;
+    acg::kern::EventArgs& e = s->eargs;
+    e = acg::kern::EventArgs{};
+    const bool known = s->xev_n > 0;
+    const bool same = known && s->xev_chunk == s->chunk && s->xev_chunks == nc && s->xev_n == owned;
+    unsigned long long prim;
+    cudaError_t err = s->xev_count.reserve(nc, st);
+    if (err != cudaSuccess) return err;
+    if (same) {
+        if ((err = s->xev_slab.reserve(2 * (nc + 1), st)) != cudaSuccess) return err;
+        std::uint32_t* sizes = s->xev_slab.p;
+        std::uint32_t* offs = s->xev_slab.p + nc + 1;
+        const unsigned g = static_cast<unsigned>(std::min<unsigned long long>((nc + 255) / 256, 8ull * s->dd->num_sms));
+        acg::kern::event_slab_sizes_kernel<<<std::max(g, 1u), 256, 0, st>>>(s->xev_count.p, static_cast<long long>(nc),
+                                                                         sizes, offs);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        std::size_t tmp = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tmp, sizes, offs + 1, static_cast<int>(nc), st);
+        if ((err = s->cub_tmp.reserve(std::max(tmp, s->cub_tmp.n), st)) != cudaSuccess) return err;
+        tmp = s->cub_tmp.n;
+        if ((err = cub::DeviceScan::InclusiveSum(s->cub_tmp.p, tmp, sizes, offs + 1, static_cast<int>(nc), st)) !=
+            cudaSuccess)
+            return err;
+        prim = s->xev_total + s->xev_total / 8 + 17 * nc;  // >= the prefix's end
+        e.slab_off = offs;
+    } else {
+        const double dens = known ? static_cast<double>(s->xev_total) / static_cast<double>(s->xev_n) : 1.0 / 16;
+        unsigned long long cap = static_cast<unsigned long long>(1.25 * dens * static_cast<double>(s->chunk)) + 17;
+        if (!known) cap = s->chunk / 16 + 33;
+        cap = std::min<unsigned long long>(cap, 0xFFFFFFFull);
+        e.ecap = static_cast<std::uint32_t>(cap);
+        prim = cap * nc;
+    }
+    unsigned long long pool = std::max<unsigned long long>(1024, (known ? prim / 4 : prim) / kEvBlock);
+    pool = std::max<unsigned long long>(pool, s->xev_min_pool);
+    if (prim + pool * kEvBlock >= 0xFFFFFFF0ull) {  // 32-bit slot indices: shrink the pool, keep it >= 1024 blocks
+        if (prim + 1024ull * kEvBlock >= 0xFFFFFFF0ull) return cudaErrorInvalidValue;
+        pool = (0xFFFFFFF0ull - prim) / kEvBlock;
+    }
+    if ((err = s->xev.reserve(prim + pool * kEvBlock, st)) != cudaSuccess) return err;
+    if ((err = s->xev_pool.reserve(1, st)) != cudaSuccess) return err;
+    e.ev = s->xev.p;
+    e.ev_count = s->xev_count.p;
+    e.pool_used = s->xev_pool.p;
+    e.pool_base = static_cast<std::uint32_t>(prim);
+    e.pool_blocks = static_cast<std::uint32_t>(pool);
+    e.ob = bits_for(n_out);
+    e.n_out = n_out;
+    e.ev_total = s->scalars64.p + 8;
+    return cudaSuccess;
+}
+
 int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std::uint64_t emit_from,
                 std::uint64_t base, cudaStream_t st) {
     using namespace acg::kern;
@@ -759,6 +876,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     s->hist_fused = false;
     s->zeros.clear();
     s->scratch_run = false;
+    s->ev_run = false;
     s->synced = false;
     s->last = st;
     s->run_text = d_text;
@@ -1005,6 +1123,29 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
         ACG_CUDA(launch_fixup(s->U_run, a, smem_sparse(dd), dd.num_sms, st));
         s->launches += 3;
+    } else if (event_slots_ok(s, n_out_states, stats)) {
+        // event pipeline (exact_kernels.cuh): KE walk logs output visits, E1
+        // counts records per chunk + visits, K2 prefix, E2 expands (enqueue_write)
+        ACG_CUDA(plan_events(s, n_out_states, st));
+        zero_later(s, s->xev_pool.p, sizeof(std::uint32_t));
+        zero_later(s, s->scalars64.p + 8, sizeof(unsigned long long));
+        ACG_CUDA(flush_zeros(s, st));
+        s->ev_run = true;
+        ACG_CUDA(launch_event_walk(d.mode, s->U_run, a, s->eargs, s->grid, s->tpb_run, smem_bytes(dd), st));
+        ++s->launches;
+        if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+        const bool smem_bins = want_counts && static_cast<std::size_t>(n_out_states) * 4 <= kEventBinsMax;
+        const unsigned g1 = static_cast<unsigned>(
+            std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 15) / 16, 2ull * dd.num_sms)));
+        if (smem_bins) {
+            auto k = acg::kern::event_count_kernel<true>;
+            ACG_CUDA(prepare_smem(k, static_cast<std::size_t>(n_out_states) * 4));
+            k<<<g1, 512, static_cast<std::size_t>(n_out_states) * 4, st>>>(a, s->eargs);
+        } else {
+            acg::kern::event_count_kernel<false><<<g1, 512, 0, st>>>(a, s->eargs);
+        }
+        ACG_CUDA(cudaGetLastError());
+        ++s->launches;
     } else {
         // single pass (count + per-chunk slabs) once the previous run told the
         // record density and the slabs fit the budget; count + write otherwise
@@ -1151,8 +1292,26 @@ int scanner_sync(acg_scanner* s) {
             return scanner_sync(s);
         }
     }
+    if (s->ev_run && s->n_chunks) {
+        ACG_CUDA(cudaMemcpyAsync(s->pinned + 1, s->xev_pool.p, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+        ACG_CUDA(cudaMemcpyAsync(s->pinned + 2, s->scalars64.p + 8, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        ACG_CUDA(cudaStreamSynchronize(st));
+        const std::uint32_t used = static_cast<std::uint32_t>(s->pinned[1]);
+        if (used > s->eargs.pool_blocks) {  // the event pool overflowed: grow it and run again
+            s->xev_min_pool = used + used / 4 + 1024;
+            s->xev_n = 0;  // (no valid counts from this run: uniform slabs)
+            ++s->replays;
+            const int rc = scanner_run(s, s->run_text, s->run_n, s->run_emit, s->run_base, st);
+            if (rc) return rc;
+            return scanner_sync(s);
+        }
+        s->xev_total = s->pinned[2];
+        s->xev_chunk = s->chunk;
+        s->xev_chunks = s->n_chunks;
+        s->xev_n = s->run_n - s->run_emit;
+    }
     s->m_total = s->n_chunks ? s->pinned[0] : 0;
-    if (s->mode_run == ACG_MODE_EXACT && s->run_n > s->run_emit) {
+    if (s->mode_run == ACG_MODE_EXACT && !s->ev_run && s->run_n > s->run_emit) {
         if (g_debug) {
             const std::uint32_t over = reinterpret_cast<const std::uint32_t*>(s->pinned + 6)[0];
             std::fprintf(stderr, "[acg] exact run: scratch %d per_chunk %d scap %llu chunks %llu matches %llu overflowed %u\n",
@@ -1212,8 +1371,8 @@ int make_scanner(const acg_automaton* a, int device, std::uint32_t flags, acg_sc
     if (!s->pinned) return fail(ACG_ERR_OUT_OF_MEMORY, "pinned host allocation failed");
     ACG_CUDA(cudaEventCreateWithFlags(&s->order_ev, cudaEventDisableTiming));
     ACG_CUDA(s->scalars32.reserve(4, s->stream));
-    ACG_CUDA(s->scalars64.reserve(8, s->stream));
-    ACG_CUDA(cudaMemsetAsync(s->scalars64.p, 0, 8 * sizeof(unsigned long long), s->stream));
+    ACG_CUDA(s->scalars64.reserve(10, s->stream));  // [8] = events of the last event-pipeline run
+    ACG_CUDA(cudaMemsetAsync(s->scalars64.p, 0, 10 * sizeof(unsigned long long), s->stream));
     s->last = s->stream;
     if (flags & ACG_SCAN_PROFILE)
         for (auto& e : s->ev) ACG_CUDA(cudaEventCreate(&e));

@@ -1,0 +1,366 @@
+// EXACT mode, event pipeline (replaces the inline emission of
+// exact_scan_kernel for list / count runs; exact_scan_kernel keeps the exact
+// ScanStats walk).
+//
+// The reference's hot loop (acmatch::scan, proj/include/acmatch/
+// aho_corasick.hpp:250-272) emits out(s) at every position whose state has
+// outputs. On the GPU, doing that inside the lockstep walk made each lane load
+// its state's output list from global memory and store every record itself:
+// divergent, long-scoreboard bound, and a 13k-instruction kernel (ncu, cfg4:
+// long_scoreboard 53 %, no_instruction 22 %). Here the walk only LOGS the
+// output visits and three small passes produce the ordered list:
+//
+//  * KE  exact_event_kernel: the chunked lockstep DFA walk (hot rows in shared
+//        memory, cold rows from L2, as exact_scan_kernel). Whenever an owned
+//        step enters an output state it appends one 32-bit event
+//        (offset in chunk << ob | output rank) to its chunk's event slab;
+//        a full slab continues in 256-event blocks taken from a global pool
+//        (linked through the slab's last slot). Per chunk: the event count.
+//  * E1  event_count_kernel: per chunk, the number of records its events
+//        expand to (sum of |out(s)|) -> chunk_counts (K2 prefixes them), and
+//        the per-output-state visit histogram (K4 turns it into per-pattern
+//        counts).
+//  * E2  event_expand_kernel: one warp per chunk writes the chunk's records
+//        at its slot range, coalesced: a warp scan of the events' output
+//        counts, then record t of the batch is found by a binary search over
+//        the scan (out ids ascending per state, positions ascending per
+//        chunk: the canonical (end, id) order of aho_corasick.hpp:38-41).
+#pragma once
+
+#include "scan_kernels.cuh"
+
+namespace acg {
+namespace kern {
+
+constexpr std::uint32_t kEvBlock = 256;  // events per pool block (the last slot links onward)
+
+struct EventArgs {
+    std::uint32_t* ev;            // event storage: primary slabs, then the pool
+    const std::uint32_t* slab_off;  // per chunk primary slab start (null: uniform c * ecap)
+    std::uint32_t ecap;           // uniform primary slab size (slots incl. the link slot)
+    std::uint32_t* ev_count;      // per chunk: events logged (owned steps in output states)
+    std::uint32_t* pool_used;     // pool blocks taken (may exceed pool_blocks: overflow)
+    std::uint32_t pool_base;      // first pool slot
+    std::uint32_t pool_blocks;
+    std::uint32_t ob;             // bits of the output rank in an event
+    std::uint32_t n_out;          // output states (ranks)
+    unsigned long long* ev_total; // E1: events of the run (sizes the next run's slabs)
+};
+
+// A run whose pool overflowed left dangling links: E1/E2 skip it (the host
+// replays the run at sync with a larger pool).
+__device__ __forceinline__ bool ev_pool_ok(const EventArgs& e) {
+    return *static_cast<const volatile std::uint32_t*>(e.pool_used) <= e.pool_blocks;
+}
+
+__device__ __forceinline__ std::uint32_t slab_start(const EventArgs& e, long long c) {
+    return e.slab_off ? e.slab_off[c] : static_cast<std::uint32_t>(c) * e.ecap;
+}
+__device__ __forceinline__ std::uint32_t slab_end(const EventArgs& e, long long c) {
+    return e.slab_off ? e.slab_off[c + 1] : static_cast<std::uint32_t>(c + 1) * e.ecap;
+}
+
+// The slab (or block) is full: continue in a fresh pool block, linked from
+// the full region's last slot `lim`. Returns the new (write slot, limit); with
+// the pool exhausted it returns (1, 0) — nothing more is stored, counting goes
+// on, and the host replays the run with a larger pool. (Out of line and by
+// value: the walk's per-stream cursors stay in registers.)
+__device__ __noinline__ uint2 ev_grow(std::uint32_t* ev, std::uint32_t* pool_used, std::uint32_t pool_base,
+                                     std::uint32_t pool_blocks, std::uint32_t lim) {
+    const std::uint32_t b = atomicAdd(pool_used, 1u);
+    if (b >= pool_blocks) return make_uint2(1u, 0u);
+    const std::uint32_t p = pool_base + b * kEvBlock;
+    ev[lim] = p;
+    return make_uint2(p, p + kEvBlock - 1);
+}
+
+__device__ __forceinline__ void ev_put(const EventArgs& e, std::uint32_t v, std::uint32_t& wr, std::uint32_t& lim) {
+    if (wr == lim) {
+        const uint2 g = ev_grow(e.ev, e.pool_used, e.pool_base, e.pool_blocks, lim);
+        wr = g.x;
+        lim = g.y;
+    }
+    if (wr < lim) e.ev[wr++] = v;
+}
+
+__device__ __forceinline__ std::uint32_t out_rank_of(std::uint32_t s, std::uint32_t H, std::uint32_t Hn,
+                                                    std::uint32_t Cn) {
+    return s < H ? s - Hn : (H - Hn) + (s - Cn);
+}
+__device__ __forceinline__ std::uint32_t state_of_rank(std::uint32_t r, std::uint32_t H, std::uint32_t Hn,
+                                                      std::uint32_t Cn) {
+    return r < H - Hn ? Hn + r : Cn + (r - (H - Hn));
+}
+
+// ===================================================================== KE ==
+template <int U, int MODE>
+__global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_event_kernel(const ScanArgs a, const EventArgs e) {
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    const std::uint32_t hot_s = smem_u32(smem);
+    const std::uint8_t* smap = smem + a.smem_table_bytes;
+
+    const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (static_cast<long long>(blockIdx.x) * blockDim.x * U >= a.n_chunks) return;  // whole block idle
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.hot16);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        if (MODE == 1)
+            for (std::uint32_t i = threadIdx.x; i < 256; i += blockDim.x) smem[a.smem_table_bytes + i] = a.symmap[i];
+    }
+    __syncthreads();
+
+    bool act[U];
+    std::uint32_t st[U], wr[U], lim[U], cnt[U];
+    long long pos0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const long long c = tid * U + u;
+        act[u] = c < a.n_chunks;
+        st[u] = 0;
+        cnt[u] = 0;
+        wr[u] = act[u] ? slab_start(e, c) : 0u;
+        lim[u] = act[u] ? slab_end(e, c) - 1u : 0u;  // last slot = link to a pool block
+        pos0[u] = a.emit_from + c * a.chunk - a.halo;
+    }
+    if (!act[0]) return;
+    const std::uint32_t K = a.K, H = a.H, Hn = a.Hn, Cn = a.Cn, ob = e.ob;
+    const long long halo = a.halo, steps = a.halo + a.chunk;
+
+    uint4 w[U];
+    auto load = [&](long long off) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = pos0[u] + off;
+            w[u] = (act[u] && p >= 0 && p < a.n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    // an owned step that entered output state s at chunk offset o
+    auto log = [&](int u, std::uint32_t s, long long o) {
+        ev_put(e, (static_cast<std::uint32_t>(o - halo) << ob) | out_rank_of(s, H, Hn, Cn), wr[u], lim[u]);
+        ++cnt[u];
+    };
+    load(0);
+    for (long long off = 0; off < steps; off += 16) {
+        uint4 cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = w[u];
+        if (off + 16 < steps) load(off + 16);
+        const bool owned_blk = off >= halo;  // halo is a multiple of 16: blocks are all-owned or all-warm-up
+        bool fast = true;
+        std::uint32_t pk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = pos0[u] + off;
+            const bool full = p >= 0 && p + 16 <= a.n;
+            if (MODE == 0) {
+                std::uint32_t bad = 0;
+                pk[u] = dna4_pack(cur[u], bad);
+                fast = fast && (!act[u] || (full && bad == 0));
+            } else {
+                pk[u] = 0;
+                fast = fast && (!act[u] || full);
+            }
+        }
+        if (fast) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                std::uint32_t col[U], v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (MODE == 0) {
+                        col[u] = (pk[u] >> (2 * k)) & 3u;
+                    } else {
+                        const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
+                        col[u] = smap[(word >> ((k & 3) * 8)) & 0xFFu];
+                    }
+                    v[u] = lds_u16(hot_s + 2u * (min(st[u], H) * K + col[u]));
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (v[u] == kEsc16) v[u] = __ldg(a.next + st[u] * K + col[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    st[u] = v[u];
+                    if (owned_blk && act[u] && ((st[u] >= Hn && st[u] < H) || st[u] >= Cn)) log(u, st[u], off + k);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!act[u]) continue;
+#pragma unroll 1
+                for (int k = 0; k < 16; ++k) {
+                    const long long p = pos0[u] + off + k;
+                    const bool inside = p >= 0 && p < a.n;
+                    const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
+                    const int c = inside ? column_of<MODE>((word >> (8 * (k & 3))) & 0xFFu, smap, a) : -1;
+                    std::uint32_t nx = 0;
+                    if (c >= 0) {
+                        nx = lds_u16(hot_s + 2u * (min(st[u], H) * K + c));
+                        if (nx == kEsc16) nx = __ldg(a.next + st[u] * K + c);
+                    }
+                    st[u] = nx;
+                    if (owned_blk && ((nx >= Hn && nx < H) || nx >= Cn)) log(u, nx, off + k);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (act[u]) e.ev_count[tid * U + u] = cnt[u];
+}
+
+// Per-chunk slab sizes for the next run from this run's event counts:
+// sizes[c] = cnt + cnt/8 + 17 (incl. the link slot); offs[0] = 0 (CUB prefixes
+// sizes into offs[1..]).
+__global__ void __launch_bounds__(256) event_slab_sizes_kernel(const std::uint32_t* cnt, long long n,
+                                                               std::uint32_t* sizes, std::uint32_t* offs) {
+    for (long long c = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x; c < n;
+         c += static_cast<long long>(gridDim.x) * 256) {
+        const std::uint32_t k = cnt[c];
+        sizes[c] = k + (k >> 3) + 17;
+        if (c == 0) offs[0] = 0;
+    }
+}
+
+// Walks chunk c's event regions (primary slab, then linked pool blocks) in
+// warp-wide batches of up to 32 events: f(base_index, n_in_batch, event of
+// this lane or 0, lane valid).
+template <typename F>
+__device__ __forceinline__ void for_event_batches(const EventArgs& e, long long c, std::uint32_t total, int lane, F f) {
+    std::uint32_t p = slab_start(e, c), lim = slab_end(e, c) - 1u, done = 0;
+    while (done < total) {
+        const std::uint32_t here = min(total - done, lim - p);
+        for (std::uint32_t b = 0; b < here; b += 32) {
+            const std::uint32_t nb = min(32u, here - b);
+            const bool ok = static_cast<std::uint32_t>(lane) < nb;
+            const std::uint32_t v = ok ? __ldcs(e.ev + p + b + lane) : 0u;
+            f(done + b, nb, v, ok);
+        }
+        done += here;
+        if (done < total) {
+            p = e.ev[lim];
+            lim = p + kEvBlock - 1;
+        }
+    }
+}
+
+// Output count of state s from its packed output info (automaton.hpp).
+__device__ __forceinline__ std::uint32_t n_out_of(std::uint32_t s, unsigned long long info, const ScanArgs& a) {
+    const std::uint32_t n = static_cast<std::uint32_t>(info >> 32) & 0xFFu;
+    return n == 255u ? __ldg(a.out_off + s + 1) - static_cast<std::uint32_t>(info) : n;
+}
+
+// ===================================================================== E1 ==
+// One warp per chunk: records per chunk (-> chunk_counts, u64 for the CUB
+// prefix) and visits per output rank (shared-memory bins when they fit).
+template <bool SMEM_BINS>
+__global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, const EventArgs e) {
+    extern __shared__ std::uint32_t bins[];
+    if (SMEM_BINS) {
+        for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x) bins[i] = 0;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const long long wpb = blockDim.x >> 5;
+    const long long warps = static_cast<long long>(gridDim.x) * wpb;
+    const std::uint32_t rmask = (1u << e.ob) - 1u, H = a.H, Hn = a.Hn, Cn = a.Cn;
+    const bool visits = a.visits != nullptr;
+    const bool pool_ok = ev_pool_ok(e);
+    unsigned long long evs = 0;
+    for (long long c = static_cast<long long>(blockIdx.x) * wpb + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
+        const std::uint32_t total = pool_ok ? e.ev_count[c] : 0u;
+        evs += total;
+        unsigned long long recs = 0;
+        if (total) {
+            for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t, std::uint32_t v, bool ok) {
+                if (!ok) return;
+                const std::uint32_t r = v & rmask;
+                const std::uint32_t s = state_of_rank(r, H, Hn, Cn);
+                recs += n_out_of(s, __ldg(a.outinfo + s), a);
+                if (visits) {
+                    if (SMEM_BINS) atomicAdd(&bins[r], 1u);
+                    else atomicAdd(a.visits + r, 1ull);
+                }
+            });
+#pragma unroll
+            for (int o = 16; o; o >>= 1) recs += __shfl_xor_sync(0xFFFFFFFFu, recs, o);
+        }
+        if (lane == 0) a.chunk_counts[c] = recs;
+    }
+    if (lane == 0 && evs) atomicAdd(e.ev_total, evs);
+    if (SMEM_BINS && visits) {
+        __syncthreads();
+        for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x)
+            if (bins[i]) atomicAdd(a.visits + i, static_cast<unsigned long long>(bins[i]));
+    }
+}
+
+// ===================================================================== E2 ==
+// One warp per chunk with records: the events' records at the chunk's slot
+// range, written by consecutive lanes (coalesced).
+__global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, const EventArgs e) {
+    const int lane = threadIdx.x & 31;
+    const long long wpb = blockDim.x >> 5;
+    const long long warps = static_cast<long long>(gridDim.x) * wpb;
+    const std::uint32_t rmask = (1u << e.ob) - 1u, H = a.H, Hn = a.Hn, Cn = a.Cn;
+    if (!ev_pool_ok(e)) return;
+    for (long long c = static_cast<long long>(blockIdx.x) * wpb + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
+        const std::uint32_t total = e.ev_count[c];
+        if (!total) continue;
+        unsigned long long o = a.chunk_offs[c];
+        const unsigned long long cbase = a.base + static_cast<unsigned long long>(a.emit_from + c * a.chunk);
+        for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t nb, std::uint32_t v, bool ok) {
+            std::uint32_t n = 0, lo = 0, first = 0;
+            unsigned long long key = 0;
+            if (ok) {
+                const std::uint32_t s = state_of_rank(v & rmask, H, Hn, Cn);
+                const unsigned long long info = __ldg(a.outinfo + s);
+                lo = static_cast<std::uint32_t>(info);
+                n = n_out_of(s, info, a);
+                first = static_cast<std::uint32_t>(info >> 40);
+                if (!(first || a.id_bits <= 24)) first = __ldg(a.out_ids + lo);
+                key = (cbase + (v >> e.ob)) << a.id_bits;
+            }
+            const unsigned single = __ballot_sync(0xFFFFFFFFu, n == 1u || !ok);
+            if (single == 0xFFFFFFFFu) {  // every event has one output: record = lane
+                if (ok && o + lane < a.rec_cap) a.records[o + lane] = key | first;
+                o += nb;
+                return;
+            }
+            // inclusive scan of the output counts
+            std::uint32_t incl = n;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const std::uint32_t T = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            for (std::uint32_t t0 = 0; t0 < T; t0 += 32) {
+                const std::uint32_t t = t0 + lane;
+                // owner j = the first lane with incl_j > t (binary search over the scan)
+                int j = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const std::uint32_t iv = __shfl_sync(0xFFFFFFFFu, incl, j + step - 1);
+                    if (iv <= t) j += step;
+                }
+                const std::uint32_t ij = __shfl_sync(0xFFFFFFFFu, incl, j);
+                const std::uint32_t nj = __shfl_sync(0xFFFFFFFFu, n, j);
+                const std::uint32_t loj = __shfl_sync(0xFFFFFFFFu, lo, j);
+                const std::uint32_t fj = __shfl_sync(0xFFFFFFFFu, first, j);
+                const unsigned long long kj = __shfl_sync(0xFFFFFFFFu, key, j);
+                if (t < T) {
+                    const std::uint32_t k = t - (ij - nj);
+                    const std::uint32_t id = k == 0 ? fj : __ldg(a.out_ids + loj + k);
+                    if (o + t < a.rec_cap) a.records[o + t] = kj | id;
+                }
+            }
+            o += T;
+        });
+    }
+}
+
+}  // namespace kern
+}  // namespace acg
