@@ -1036,7 +1036,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             const std::uint32_t mcap = std::max<std::uint32_t>(64, s->min_mcap);
             s->last_mcap = mcap;
             ACG_CUDA(s->qscratch.reserve(static_cast<std::size_t>(W) * mcap, st));
-            ACG_CUDA(s->qreg_n.reserve(W, st));
+            ACG_CUDA(s->qreg_n.reserve(std::max<unsigned long long>(W, warps), st));  // (KQ warps past the last region touch nothing)
             ACG_CUDA(s->qscal.reserve(2, st));
             zero_later(s, s->qscal.p, 2 * sizeof(std::uint32_t));
             a.qscratch = s->qscratch.p;
@@ -1265,6 +1265,9 @@ int scanner_sync(acg_scanner* s) {
         ACG_CUDA(cudaStreamSynchronize(st));
         const std::uint32_t* qs = reinterpret_cast<const std::uint32_t*>(s->pinned + 1);
         const std::uint32_t slab_max = qs[0], too_big = qs[1];
+        if (g_debug)
+            std::fprintf(stderr, "[acg] filter region run: survivors max %llu cap %u slab_max %u mcap %u too_big %u\n",
+                         s->pinned[4], s->args.qcand_cap, slab_max, s->last_mcap, too_big);
         if (s->pinned[4] <= s->args.qcand_cap && (slab_max > s->last_mcap || too_big)) {
             // a region's slab overflowed (grow it) or held more than ORDER sorts
             // (replay through the per-chunk pipeline from now on): run again
@@ -1281,6 +1284,37 @@ int scanner_sync(acg_scanner* s) {
     }
     if (s->mode_run == ACG_MODE_FILTER && s->n_chunks) {
         const unsigned long long worst = s->pinned[4];
+        if (g_debug) {
+            std::fprintf(stderr, "[acg] filter run (legacy %d): survivors max %llu cap %u chunks %llu matches %llu records %zu\n",
+                         s->qlegacy ? 1 : 0, worst, s->args.qcand_cap, s->n_chunks, s->pinned[0], s->records.n);
+            if (s->qlegacy && worst <= s->args.qcand_cap) {  // survivor sanity: duplicates, out-of-region positions
+                const std::size_t W = s->args.qwarps, cap = s->args.qcand_cap;
+                std::vector<std::uint32_t> wn(W);
+                std::vector<unsigned long long> qc(W * cap), cc(s->n_chunks);
+                cudaMemcpy(wn.data(), s->qwarp_n.p, W * 4, cudaMemcpyDeviceToHost);
+                cudaMemcpy(qc.data(), s->qcands.p, W * cap * 8, cudaMemcpyDeviceToHost);
+                cudaMemcpy(cc.data(), s->chunk_counts.p, s->n_chunks * 8, cudaMemcpyDeviceToHost);
+                std::vector<unsigned long long> all;
+                unsigned long long bad = 0;
+                const unsigned long long nb = (s->run_n + 2047) / 2048, per = (nb + W - 1) / W;
+                for (std::size_t w = 0; w < W; ++w)
+                    for (std::size_t k = 0; k < wn[w]; ++k) {
+                        const unsigned long long pos = qc[w * cap + k];
+                        all.push_back(pos);
+                        if (pos / 2048 < w * per || pos / 2048 >= (w + 1) * per) ++bad;
+                    }
+                std::sort(all.begin(), all.end());
+                unsigned long long dups = 0;
+                for (std::size_t i = 1; i < all.size(); ++i) dups += all[i] == all[i - 1];
+                unsigned long long sum = 0, mx = 0, arg = 0;
+                for (std::size_t c = 0; c < cc.size(); ++c) {
+                    sum += cc[c];
+                    if (cc[c] > mx) mx = cc[c], arg = c;
+                }
+                std::fprintf(stderr, "[acg]   survivors %zu dups %llu out-of-region %llu; chunk counts sum %llu max %llu at %llu\n",
+                             all.size(), dups, bad, sum, mx, arg);
+            }
+        }
         if (worst > s->args.qcand_cap) {  // a survivor region overflowed: grow and run again
             s->min_task_cap = worst + worst / 4 + 64;
             const int req = s->mode_req;

@@ -253,12 +253,17 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
                     std::uint32_t pm = 0;
 #pragma unroll
                     for (int o = 0; o < 16; ++o) pm |= (t[o] == 0u ? 1u : 0u) << o;
-                    std::uint32_t slot = atomicAdd(&wcnt[warp], static_cast<std::uint32_t>(__popc(pm)));
                     const long long P = b * kBlk + 16 * lane;
+                    if (b >= nfull) {  // the text's partial last block: samples past its end are not survivors
+#pragma unroll
+                        for (int o = 0; o < 16; ++o)
+                            if (P + 512 * (o >> 2) + 4 * (o & 3) >= n) pm &= ~(1u << o);
+                    }
+                    std::uint32_t slot = atomicAdd(&wcnt[warp], static_cast<std::uint32_t>(__popc(pm)));
                     for (std::uint32_t m = pm; m; m &= m - 1, ++slot) {
                         const int i = __ffs(m) - 1, r = i >> 2, o = i & 3;
                         const long long pos = P + 512 * r + 4 * o;
-                        if (pos < n && slot < a.qcand_cap) {
+                        if (slot < a.qcand_cap) {
                             std::uint32_t lo = cur[0], hi = nb_[0];
                             if (r == 1) lo = cur[1], hi = nb_[1];
                             if (r == 2) lo = cur[2], hi = nb_[2];
@@ -284,7 +289,7 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
     if (lane == 0) {
         const std::uint32_t found = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
         a.qwarp_n[gw] = found;
-        if (!FUSED && a.reg_n) a.reg_n[gw] = 0u;  // V1's per-region counters
+        if (!FUSED && a.reg_n && gw < a.n_chunks) a.reg_n[gw] = 0u;  // V1's per-region counters (one per chunk)
         atomicAdd(a.qcand_n, found);
         atomicMax(a.qcand_max, static_cast<unsigned long long>(found));
         if (FUSED) {

@@ -36,9 +36,26 @@ def run_filter(words_or_arrays, text, expect_filter=True, emit_from=0):
         assert s.last_mode()[0] == "filter"
     o = oracle.OracleAutomaton(concat, offs)
     oi, oe, _, cnt = o.scan(text, counts=True)
-    assert recs(ids, ends) == recs(oi, oe)
+    assert recs(ids, ends) == recs(oi, oe), diff_report(s, ids, ends, oi, oe)
     assert np.array_equal(s.pattern_counts(), cnt)
     return len(oi)
+
+
+def diff_report(s, ids, ends, oi, oe) -> str:
+    """Why two match lists differ (duplicates, missing, extra, first difference)."""
+    from paper_1403_7294_b200 import _lib
+    key = np.asarray(ends, np.uint64) * np.uint64(1 << 20) + np.asarray(ids, np.uint64)
+    okey = np.asarray(oe, np.uint64) * np.uint64(1 << 20) + np.asarray(oi, np.uint64)
+    m = min(key.size, okey.size)
+    d = np.nonzero(key[:m] != okey[:m])[0]
+    first = int(d[0]) if d.size else m
+    fmt = lambda ks: [(int(k) >> 20, int(k) & 0xFFFFF) for k in ks]
+    return (f"gpu {key.size} oracle {okey.size} replays {_lib.acg().acg_scanner_replays(s._h)} "
+            f"mode {s.last_mode()} dups {key.size - np.unique(key).size} "
+            f"missing {np.setdiff1d(okey, key).size} extra {np.setdiff1d(key, okey).size} "
+            f"unsorted {int(np.sum(key[1:] <= key[:-1]))} first diff {first}: gpu {fmt(key[first:first + 4])} "
+            f"oracle {fmt(okey[first:first + 4])} extra {fmt(np.setdiff1d(key, okey)[:6])} "
+            f"missing {fmt(np.setdiff1d(okey, key)[:6])}")
 
 
 def rand_dna(rng, n):
@@ -201,3 +218,24 @@ def test_filter_two_level_cfg2_dictionary():
     assert info["eligible"] and info["q"] == 16
     m = run_filter((concat, offs), synth.text(w))
     assert m > 0
+
+
+def test_filter_no_phantom_survivors_past_the_text_end():
+    """KQ reads the partial last block with zero bytes past the end, whose
+    2-bit codes are 'A': an A-homopolymer pattern must not make those samples
+    survivors (they were counted but never stored, so V1/V0 read stale slots:
+    duplicate records after an earlier scanner left positions in that memory)."""
+    rng = np.random.default_rng(21)
+    words = [b"A" * 16, b"A" * 23]
+    for n in (100, 2048 * 3 + 100, (1 << 20) + 1000):
+        text = np.frombuffer(b"CGT", np.uint8)[rng.integers(0, 3, n)].copy()
+        text[n // 2:n // 2 + 20] = ord("A")  # one real run: 5 + 0 matches
+        m = run_filter(words, text)
+        assert m == 5
+        concat, offs = synth.pack_patterns(words)
+        s = am.Scanner(am.Automaton.from_arrays(concat, offs), 0, am.SCAN_LIST)
+        s.set_mode(am.MODE_FILTER)
+        s.run_host(text)
+        s.sync()
+        mode, rate = s.last_mode()
+        assert mode == "filter" and rate * n <= 8  # survivors: samples inside the one A-run only
