@@ -69,6 +69,12 @@ uint32_t acg_transitions(const acg_automaton* a, uint32_t s, const uint8_t** byt
 uint32_t acg_failure(const acg_automaton* a, uint32_t s);               /* :84-87 */
 uint32_t acg_outputs(const acg_automaton* a, uint32_t s, const uint32_t** ids); /* :92-95 */
 uint32_t acg_depth(const acg_automaton* a, uint32_t s);                 /* :98-101 */
+/* The whole NFA at once (the accessors above for every state): CSR views
+ * into the automaton, valid while it lives. Edges of state s are
+ * [edge_off[s], edge_off[s+1]) sorted by byte; outputs [out_off[s],
+ * out_off[s+1]) ascending. Any pointer argument may be NULL. */
+int acg_nfa_arrays(const acg_automaton* a, const uint32_t** fail, const uint32_t** depth, const uint32_t** edge_off,
+                   const uint8_t** edge_byte, const uint32_t** edge_to, const uint32_t** out_off, const uint32_t** out_ids);
 /* next_state (:238-245) */
 uint32_t acg_next_state(const acg_automaton* a, uint32_t s, uint8_t b);
 

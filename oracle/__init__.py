@@ -72,6 +72,7 @@ _REF_SYMS = {
     "ref_random_trial": (u32, [u64, u32, u32, u32, u64, vp, vp, vp, C.POINTER(u64)]),
     "ref_naive_find_all": (u64, [vp, vp, u32, vp, u64, vp, vp, u64]),
     "ref_hardware_concurrency": (C.c_uint, []),
+    "ref_export": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 _libs: dict = {}
@@ -281,6 +282,20 @@ class RefAutomaton:
         bb, tt = np.zeros(256, np.uint8), np.zeros(256, np.uint32)
         n = ref().ref_transitions(self._h, s, _ptr(bb), _ptr(tt), 256)
         return list(zip(bb[:n].tolist(), tt[:n].tolist()))
+
+    def export(self) -> dict:
+        """The whole machine through the reference's public accessors, as CSR arrays."""
+        sizes = np.zeros(3, np.uint64)
+        lib = ref()
+        lib.ref_export(self._h, _ptr(sizes), *([None] * 7))
+        S, E, O = (int(x) for x in sizes)
+        out = {"fail": np.zeros(S, np.uint32), "depth": np.zeros(S, np.uint32),
+               "edge_off": np.zeros(S + 1, np.uint32), "edge_byte": np.zeros(E, np.uint8),
+               "edge_to": np.zeros(E, np.uint32), "out_off": np.zeros(S + 1, np.uint32),
+               "out_ids": np.zeros(O, np.uint32)}
+        lib.ref_export(self._h, _ptr(sizes), *[_ptr(out[k]) for k in ("fail", "depth", "edge_off", "edge_byte",
+                                                                      "edge_to", "out_off", "out_ids")])
+        return out
 
     def scan(self, text) -> tuple[np.ndarray, np.ndarray, int]:
         t = _u8(text)

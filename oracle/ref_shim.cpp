@@ -94,6 +94,37 @@ std::uint32_t ref_transitions(void* h, std::uint32_t s, std::uint8_t* bytes, std
     return static_cast<std::uint32_t>(e.size());
 }
 
+// The whole machine through the public accessors (aho_corasick.hpp:77-101),
+// as CSR arrays: sizes first (any output pointer null), then the copy.
+void ref_export(void* h, std::uint64_t* sizes, std::uint32_t* fail, std::uint32_t* depth, std::uint32_t* edge_off,
+                std::uint8_t* edge_byte, std::uint32_t* edge_to, std::uint32_t* out_off, std::uint32_t* out_ids) {
+    const Automaton& a = *static_cast<Automaton*>(h);
+    const auto S = static_cast<std::uint32_t>(a.state_count());
+    std::uint64_t ne = 0, no = 0;
+    for (std::uint32_t s = 0; s < S; ++s) {
+        ne += a.transitions(s).size();
+        no += a.outputs(s).size();
+    }
+    sizes[0] = S;
+    sizes[1] = ne;
+    sizes[2] = no;
+    if (!fail) return;
+    std::uint32_t e = 0, o = 0;
+    for (std::uint32_t s = 0; s < S; ++s) {
+        fail[s] = a.failure(s);
+        depth[s] = a.depth(s);
+        edge_off[s] = e;
+        for (const auto& [b, t] : a.transitions(s)) {
+            edge_byte[e] = b;
+            edge_to[e++] = t;
+        }
+        out_off[s] = o;
+        for (const auto id : a.outputs(s)) out_ids[o++] = id;
+    }
+    edge_off[S] = e;
+    out_off[S] = o;
+}
+
 // acmatch::scan (include/acmatch/aho_corasick.hpp:250-272) over text[0, n).
 std::uint64_t ref_scan(void* h, const std::uint8_t* text, std::uint64_t n, std::uint64_t* follows,
                        std::uint32_t* ids, std::uint64_t* ends, std::uint64_t cap) {

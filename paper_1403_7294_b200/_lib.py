@@ -32,6 +32,7 @@ ACG_SYMBOLS = {
     "acg_failure": (C.c_uint32, [vp, C.c_uint32]),
     "acg_outputs": (C.c_uint32, [vp, C.c_uint32, C.POINTER(u32p)]),
     "acg_depth": (C.c_uint32, [vp, C.c_uint32]),
+    "acg_nfa_arrays": (C.c_int, [vp] + [vp] * 7),
     "acg_next_state": (C.c_uint32, [vp, C.c_uint32, C.c_uint8]),
     "acg_optimize_layout": (C.c_int, [vp, vp, C.c_uint64]),
     "acg_set_hot_limit": (C.c_int, [vp, C.c_uint32]),

@@ -157,6 +157,30 @@ class Automaton:
     def depth(self, s: int) -> int:
         return _lib.acg().acg_depth(self._h, s)
 
+    def nfa_arrays(self) -> dict:
+        """The whole NFA as numpy CSR arrays (copies): fail, depth, edge_off,
+        edge_byte, edge_to, out_off, out_ids (acg_nfa_arrays)."""
+        S = self.state_count()
+        ptrs = [C.c_void_p() for _ in range(7)]
+        _check(_lib.acg().acg_nfa_arrays(self._h, *[C.byref(p) for p in ptrs]))
+
+        def view(p, n, ct, dt):
+            if n == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), shape=(n,)).astype(dt, copy=True)
+
+        edge_off = view(ptrs[2], S + 1, C.c_uint32, np.uint32)
+        out_off = view(ptrs[5], S + 1, C.c_uint32, np.uint32)
+        return {
+            "fail": view(ptrs[0], S, C.c_uint32, np.uint32),
+            "depth": view(ptrs[1], S, C.c_uint32, np.uint32),
+            "edge_off": edge_off,
+            "edge_byte": view(ptrs[3], int(edge_off[-1]), C.c_uint8, np.uint8),
+            "edge_to": view(ptrs[4], int(edge_off[-1]), C.c_uint32, np.uint32),
+            "out_off": out_off,
+            "out_ids": view(ptrs[6], int(out_off[-1]), C.c_uint32, np.uint32),
+        }
+
     def optimize_layout(self, sample: bytes | np.ndarray) -> None:
         """Profile-guided device layout from a text sample (speed only)."""
         arr = np.frombuffer(sample, dtype=np.uint8) if isinstance(sample, (bytes, bytearray)) else sample

@@ -1597,6 +1597,20 @@ std::uint32_t acg_outputs(const acg_automaton* a, std::uint32_t s, const std::ui
     return hi - lo;
 }
 std::uint32_t acg_depth(const acg_automaton* a, std::uint32_t s) { return a->nfa.depth[s]; }
+
+int acg_nfa_arrays(const acg_automaton* a, const std::uint32_t** fail_links, const std::uint32_t** depth,
+                   const std::uint32_t** edge_off, const std::uint8_t** edge_byte, const std::uint32_t** edge_to,
+                   const std::uint32_t** out_off, const std::uint32_t** out_ids) {
+    if (!a) return fail(ACG_ERR_INVALID, "null automaton");
+    if (fail_links) *fail_links = a->nfa.fail.data();
+    if (depth) *depth = a->nfa.depth.data();
+    if (edge_off) *edge_off = a->nfa.edge_off.data();
+    if (edge_byte) *edge_byte = a->nfa.edge_byte.data();
+    if (edge_to) *edge_to = a->nfa.edge_to.data();
+    if (out_off) *out_off = a->nfa.out_off.data();
+    if (out_ids) *out_ids = a->nfa.out_ids.data();
+    return ACG_OK;
+}
 std::uint32_t acg_next_state(const acg_automaton* a, std::uint32_t s, std::uint8_t b) {
     return a->nfa.next_state(s, b);
 }

@@ -1,8 +1,11 @@
 // Host automaton build (reference algorithm) and dense-DFA compilation.
 #include "automaton.hpp"
+#include "parallel.hpp"
 #include "qfilter.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -33,194 +36,306 @@ StateId Nfa::next_state(StateId s, std::uint8_t b) const {
 
 namespace {
 
-// Open-addressing map (node, byte) -> child for trie insertion. Lookup only;
-// the insertion order of children is kept separately in sibling lists, which
-// is what the reference's preorder depends on (aho_corasick.hpp:139-166).
-struct EdgeMap {
-    std::vector<std::uint64_t> keys;
-    std::vector<std::uint32_t> vals;
-    std::uint64_t mask = 0;
-    std::size_t used = 0;
-
-    explicit EdgeMap(std::size_t expect) {
-        std::size_t cap = 1024;
-        while (cap < expect * 2) cap <<= 1;
-        keys.assign(cap, ~0ull);
-        vals.assign(cap, 0);
-        mask = cap - 1;
+using Clock = std::chrono::steady_clock;
+const bool g_build_prof = [] {  // ACG_BUILD_PROFILE=1: phase times of the build on stderr
+    const char* e = std::getenv("ACG_BUILD_PROFILE");
+    return e && e[0] == '1';
+}();
+struct Phase {
+    const char* what;
+    Clock::time_point t0 = Clock::now();
+    explicit Phase(const char* w) : what(w) {}
+    void next(const char* w) {  // close this phase, open the next
+        report();
+        what = w;
+        t0 = Clock::now();
     }
-    static std::uint64_t hash(std::uint64_t k) {
-        k ^= k >> 33;
-        k *= 0xff51afd7ed558ccdull;
-        k ^= k >> 33;
-        return k;
+    void report() const {
+        if (g_build_prof)
+            std::fprintf(stderr, "[acg build] %-22s %8.2f ms\n", what,
+                         std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
     }
-    std::uint32_t* find_or_slot(std::uint64_t key, bool* found) {
-        std::uint64_t i = hash(key) & mask;
-        for (;;) {
-            if (keys[i] == key) {
-                *found = true;
-                return &vals[i];
-            }
-            if (keys[i] == ~0ull) {
-                *found = false;
-                keys[i] = key;
-                ++used;
-                return &vals[i];
-            }
-            i = (i + 1) & mask;
-        }
-    }
+    ~Phase() { report(); }
 };
 
 }  // namespace
 
+// The reference's build (aho_corasick.hpp:130-233) inserts the patterns one by
+// one into a trie whose children keep insertion order, numbers the states in
+// DFS preorder, then walks BFS to set failure links (a chain walk per edge)
+// and suffix-closed output sets. The same machine is built here in bulk:
+//  1. patterns sorted by (bytes, id) on the pool; one sweep over the sorted
+//     list creates every distinct prefix (a trie node) in lexicographic order,
+//     with the smallest pattern id through it (= its creation time under the
+//     reference's id-order insertion: siblings are ordered by it);
+//  2. subtree sizes, then DFS-preorder ids with children in creation order;
+//     edges sorted by byte come for free from the lexicographic order;
+//  3. BFS levels: within a level every state is independent, so the failure
+//     link (delta(fail(parent), byte)), the dense transition row (the fail
+//     state's row with the state's own edges), the follow counts and the
+//     output-set sizes are computed in parallel; output sets are filled level
+//     by level (a merge of the state's own ids with its fail state's set).
 int build_nfa(const std::uint8_t* concat, const std::uint64_t* offs, std::uint32_t count, Nfa& nfa) {
     if (count == 0) return kErrEmptyDictionary;  // aho_corasick.hpp:131
     std::uint64_t total = 0;
-    std::uint32_t max_len = 0;
+    std::uint32_t max_len = 0, min_len = ~0u;
     for (std::uint32_t i = 0; i < count; ++i) {
         const std::uint64_t len = offs[i + 1] - offs[i];
         if (len == 0) return kErrEmptyPattern;  // :133-134
         total += len;
         max_len = std::max<std::uint32_t>(max_len, static_cast<std::uint32_t>(len));
+        min_len = std::min<std::uint32_t>(min_len, static_cast<std::uint32_t>(len));
     }
     // states are u32 (StateId, aho_corasick.hpp:18): up to total + 1 of them
     if (total >= 0xFFFFFFF0ull) return kErrTooLarge;
+    const std::uint8_t* const base = concat;
+    auto pat = [&](std::uint32_t id) { return base + offs[id]; };
+    auto plen = [&](std::uint32_t id) { return static_cast<std::uint32_t>(offs[id + 1] - offs[id]); };
 
-    // Phase 1: keyword trie, children in insertion order.
-    std::vector<std::uint32_t> first_kid(1, 0), next_sib(1, 0), last_kid(1, 0), tdepth(1, 0);
-    std::vector<std::uint8_t> tbyte(1, 0);
-    std::vector<std::uint32_t> own_head(1, ~0u);  // first pattern id ending here
-    std::vector<std::uint32_t> own_next(count, ~0u), own_tail(1, ~0u);
-    EdgeMap map(static_cast<std::size_t>(std::min<std::uint64_t>(total, 1ull << 30)) + 16);
-    for (std::uint32_t p = 0; p < count; ++p) {
-        std::uint32_t node = 0;
-        for (std::uint64_t k = offs[p]; k < offs[p + 1]; ++k) {
-            const std::uint8_t b = concat[k];
-            bool found;
-            std::uint32_t* slot = map.find_or_slot((static_cast<std::uint64_t>(node) << 8) | b, &found);
-            if (found) {
-                node = *slot;
+    // ---- 1. sorted sweep: trie nodes in lexicographic preorder ------------
+    std::vector<std::uint32_t> ord(count);
+    {
+        Phase ph("sort patterns");
+        std::iota(ord.begin(), ord.end(), 0u);
+        parallel_sort(ord, [&](std::uint32_t x, std::uint32_t y) {
+            const std::uint32_t lx = plen(x), ly = plen(y);
+            const int c = std::memcmp(pat(x), pat(y), std::min(lx, ly));
+            if (c) return c < 0;
+            if (lx != ly) return lx < ly;
+            return x < y;
+        });
+    }
+    std::vector<std::uint32_t> lpar, lmin, own_first, own_cnt;
+    std::vector<std::uint8_t> lbyte;
+    std::vector<std::uint32_t> ldepth;
+    {
+        Phase ph("trie sweep");
+        const std::size_t guess = static_cast<std::size_t>(std::min<std::uint64_t>(total + 1, 1ull << 28));
+        lpar.reserve(guess);
+        lmin.reserve(guess);
+        lbyte.reserve(guess);
+        ldepth.reserve(guess);
+        lpar.push_back(0);
+        lmin.push_back(0);
+        lbyte.push_back(0);
+        ldepth.push_back(0);
+        own_first.assign(1, ~0u);
+        own_cnt.assign(1, 0);
+        std::vector<std::uint32_t> path(static_cast<std::size_t>(max_len) + 1, 0);
+        const std::uint8_t* prev = nullptr;
+        std::uint32_t prev_len = 0;
+        for (std::uint32_t k = 0; k < count; ++k) {
+            const std::uint32_t id = ord[k], L = plen(id);
+            const std::uint8_t* s = pat(id);
+            std::uint32_t l = 0;
+            const std::uint32_t lim = std::min(L, prev_len);
+            if (prev)
+                while (l < lim && s[l] == prev[l]) ++l;
+            for (std::uint32_t d = 1; d <= l; ++d) lmin[path[d]] = std::min(lmin[path[d]], id);
+            for (std::uint32_t d = l + 1; d <= L; ++d) {
+                const auto t = static_cast<std::uint32_t>(lpar.size());
+                lpar.push_back(path[d - 1]);
+                lmin.push_back(id);
+                lbyte.push_back(s[d - 1]);
+                ldepth.push_back(d);
+                path[d] = t;
+            }
+            const std::uint32_t term = path[L];
+            if (term >= own_first.size()) {
+                own_first.resize(lpar.size(), ~0u);
+                own_cnt.resize(lpar.size(), 0);
+            }
+            if (own_cnt[term]++ == 0) own_first[term] = k;  // ids ascending (:165, :192)
+            prev = s;
+            prev_len = L;
+        }
+        own_first.resize(lpar.size(), ~0u);
+        own_cnt.resize(lpar.size(), 0);
+    }
+    const auto n = static_cast<std::uint32_t>(lpar.size());
+
+    // ---- 2. DFS preorder with children in creation order (:170-183) -------
+    std::vector<std::uint32_t> kid_off(n + 1, 0), kids, id_of(n);
+    {
+        Phase ph("preorder numbering");
+        for (std::uint32_t v = 1; v < n; ++v) ++kid_off[lpar[v] + 1];
+        for (std::uint32_t v = 0; v < n; ++v) kid_off[v + 1] += kid_off[v];
+        kids.resize(n ? n - 1 : 0);
+        {
+            std::vector<std::uint32_t> fill(kid_off.begin(), kid_off.end() - 1);
+            for (std::uint32_t v = 1; v < n; ++v) kids[fill[lpar[v]]++] = v;  // byte order (lexicographic)
+        }
+        std::vector<std::uint32_t> size(n, 1);
+        for (std::uint32_t v = n - 1; v >= 1; --v) size[lpar[v]] += size[v];
+        id_of[0] = 0;
+        std::vector<std::uint32_t> tmp;
+        for (std::uint32_t v = 0; v < n; ++v) {
+            const std::uint32_t k0 = kid_off[v], k1 = kid_off[v + 1];
+            std::uint32_t next = id_of[v] + 1;
+            if (k1 - k0 == 1) {
+                id_of[kids[k0]] = next;
                 continue;
             }
-            const auto child = static_cast<std::uint32_t>(first_kid.size());
-            *slot = child;
-            first_kid.push_back(0);
-            next_sib.push_back(0);
-            last_kid.push_back(0);
-            tdepth.push_back(tdepth[node] + 1);
-            tbyte.push_back(b);
-            own_head.push_back(~0u);
-            own_tail.push_back(~0u);
-            if (last_kid[node]) next_sib[last_kid[node]] = child;
-            else first_kid[node] = child;
-            last_kid[node] = child;
-            node = child;
-        }
-        // own ids in id order: ascending (:165, :192)
-        if (own_head[node] == ~0u) own_head[node] = p;
-        else own_next[own_tail[node]] = p;
-        own_tail[node] = p;
-    }
-    const auto n = static_cast<std::uint32_t>(first_kid.size());
-
-    // Phase 2: DFS preorder, children in insertion order (:170-183).
-    std::vector<std::uint32_t> order;
-    order.reserve(n);
-    {
-        std::vector<std::uint32_t> stack{0}, kids;
-        while (!stack.empty()) {
-            const std::uint32_t v = stack.back();
-            stack.pop_back();
-            order.push_back(v);
-            kids.clear();
-            for (std::uint32_t k = first_kid[v]; k; k = next_sib[k]) kids.push_back(k);
-            for (auto it = kids.rbegin(); it != kids.rend(); ++it) stack.push_back(*it);
-        }
-    }
-    std::vector<std::uint32_t> renum(n);
-    for (std::uint32_t s = 0; s < n; ++s) renum[order[s]] = s;
-
-    // Freeze: per-state edges sorted by byte (:185-196).
-    nfa.edge_off.assign(n + 1, 0);
-    nfa.edge_byte.resize(n - 1);
-    nfa.edge_to.resize(n - 1);
-    nfa.depth.assign(n, 0);
-    nfa.fail.assign(n, 0);
-    {
-        std::uint32_t e = 0;
-        std::vector<std::pair<std::uint8_t, std::uint32_t>> tmp;
-        for (std::uint32_t s = 0; s < n; ++s) {
-            const std::uint32_t t = order[s];
-            nfa.depth[s] = tdepth[t];
-            nfa.edge_off[s] = e;
-            tmp.clear();
-            for (std::uint32_t k = first_kid[t]; k; k = next_sib[k]) tmp.emplace_back(tbyte[k], renum[k]);
-            std::sort(tmp.begin(), tmp.end());
-            for (const auto& [b, c] : tmp) {
-                nfa.edge_byte[e] = b;
-                nfa.edge_to[e] = c;
-                ++e;
+            tmp.assign(kids.begin() + k0, kids.begin() + k1);
+            std::sort(tmp.begin(), tmp.end(), [&](std::uint32_t x, std::uint32_t y) { return lmin[x] < lmin[y]; });
+            for (const std::uint32_t c : tmp) {
+                id_of[c] = next;
+                next += size[c];
             }
         }
-        nfa.edge_off[n] = e;
     }
 
-    // Phase 3: BFS failure links + suffix-closed outputs (:201-226).
-    // fail(child of u by b) = next_state(fail(u), b); the reference finds it
-    // with the same chain walk (:205-215).
-    nfa.bfs.clear();
-    nfa.bfs.reserve(n);
-    nfa.bfs.push_back(0);
-    std::vector<std::uint32_t> out_start(n, 0), out_len(n, 0);
-    std::vector<std::uint32_t> pool;
-    pool.reserve(count * 2ull);
-    auto own_list = [&](std::uint32_t s, std::vector<std::uint32_t>& dst) {
-        dst.clear();
-        for (std::uint32_t p = own_head[order[s]]; p != ~0u; p = own_next[p]) dst.push_back(p);
-    };
-    std::vector<std::uint32_t> own, merged;
-    for (std::uint32_t j = nfa.edge_off[0]; j < nfa.edge_off[1]; ++j) {
-        const std::uint32_t c = nfa.edge_to[j];
-        nfa.fail[c] = 0;
-        nfa.bfs.push_back(c);
+    // ---- freeze: per-state edges sorted by byte (:185-196) ----------------
+    std::vector<std::uint32_t> par(n), own_lo(n), own_n(n);
+    std::vector<std::uint8_t> in_byte(n);
+    {
+        Phase ph("edges");
+        nfa.edge_off.assign(static_cast<std::size_t>(n) + 1, 0);
+        nfa.depth.assign(n, 0);
+        for (std::uint32_t v = 0; v < n; ++v) nfa.edge_off[id_of[v] + 1] = kid_off[v + 1] - kid_off[v];
+        for (std::uint32_t s = 0; s < n; ++s) nfa.edge_off[s + 1] += nfa.edge_off[s];
+        nfa.edge_byte.resize(n - 1);
+        nfa.edge_to.resize(n - 1);
+        parallel_for(n, 1 << 14, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t v = lo; v < hi; ++v) {
+                const std::uint32_t s = id_of[v];
+                nfa.depth[s] = ldepth[v];
+                par[s] = id_of[lpar[v]];
+                in_byte[s] = lbyte[v];
+                own_lo[s] = own_first[v];
+                own_n[s] = own_cnt[v];
+                std::uint32_t e = nfa.edge_off[s];
+                for (std::uint32_t k = kid_off[v]; k < kid_off[v + 1]; ++k, ++e) {
+                    nfa.edge_byte[e] = lbyte[kids[k]];
+                    nfa.edge_to[e] = id_of[kids[k]];
+                }
+            }
+        });
     }
-    for (std::size_t head = 1; head < nfa.bfs.size(); ++head) {
-        const std::uint32_t u = nfa.bfs[head];
-        // outputs of u: own merged with out(fail(u)) (fail(u) precedes u in BFS)
-        own_list(u, own);
-        const std::uint32_t f = nfa.fail[u];
-        merged.clear();
-        std::merge(own.begin(), own.end(), pool.begin() + out_start[f], pool.begin() + out_start[f] + out_len[f],
-                   std::back_inserter(merged));
-        out_start[u] = static_cast<std::uint32_t>(pool.size());
-        out_len[u] = static_cast<std::uint32_t>(merged.size());
-        pool.insert(pool.end(), merged.begin(), merged.end());
-        for (std::uint32_t j = nfa.edge_off[u]; j < nfa.edge_off[u + 1]; ++j) {
-            const std::uint8_t b = nfa.edge_byte[j];
-            const std::uint32_t child = nfa.edge_to[j];
-            if (u != 0) nfa.fail[child] = nfa.next_state(nfa.fail[u], b);
-            nfa.bfs.push_back(child);
+    // (lexicographic scratch no longer needed)
+    std::vector<std::uint32_t>().swap(lpar);
+    std::vector<std::uint32_t>().swap(lmin);
+    std::vector<std::uint32_t>().swap(kids);
+
+    // ---- alphabet: the symbol classes of the dense image -------------------
+    {
+        bool used[256] = {};
+        for (std::uint32_t s = 1; s < n; ++s) used[in_byte[s]] = true;
+        std::uint32_t n_sym = 0;
+        bool dna = true;
+        for (int b = 0; b < 256; ++b) {
+            n_sym += used[b];
+            if (used[b] && b != 'A' && b != 'C' && b != 'G' && b != 'T') dna = false;
+        }
+        nfa.n_sym = n_sym;
+        std::memset(nfa.symmap, 0, sizeof nfa.symmap);
+        if (dna) {
+            nfa.mode = kAlphaDna4;
+            nfa.K = 4;
+            nfa.col_byte = {'A', 'C', 'T', 'G'};  // column = (byte >> 1) & 3
+            for (int c = 0; c < 4; ++c) nfa.symmap[nfa.col_byte[c]] = static_cast<std::uint8_t>(c);
+        } else {
+            nfa.mode = kAlphaGeneric;
+            nfa.K = n_sym + 1;
+            nfa.col_byte.clear();
+            std::uint32_t c = 0;
+            for (int b = 0; b < 256; ++b)
+                if (used[b]) {
+                    nfa.symmap[b] = static_cast<std::uint8_t>(c++);
+                    nfa.col_byte.push_back(b);
+                }
+            for (int b = 0; b < 256; ++b)
+                if (!used[b]) nfa.symmap[b] = static_cast<std::uint8_t>(n_sym);  // escape column
+            nfa.col_byte.push_back(-1);
         }
     }
-    nfa.out_off.assign(n + 1, 0);
-    for (std::uint32_t s = 0; s < n; ++s) nfa.out_off[s + 1] = nfa.out_off[s] + out_len[s];
-    nfa.out_ids.resize(nfa.out_off[n]);
-    for (std::uint32_t s = 0; s < n; ++s)
-        std::copy_n(pool.begin() + out_start[s], out_len[s], nfa.out_ids.begin() + nfa.out_off[s]);
+    const std::uint32_t K = nfa.K;
+    int col_of[256];
+    std::fill(std::begin(col_of), std::end(col_of), -1);
+    for (std::uint32_t c = 0; c < K; ++c)
+        if (nfa.col_byte[c] >= 0) col_of[nfa.col_byte[c]] = static_cast<int>(c);
+
+    // ---- 3. BFS levels: failure links, dense rows, follows, output sizes ---
+    nfa.bfs.assign(1, 0);
+    nfa.bfs.reserve(n);
+    std::vector<std::uint32_t> level_at{0, 1};
+    {
+        Phase ph("bfs order");
+        for (std::size_t head = 0; head < nfa.bfs.size(); ++head) {
+            const std::uint32_t u = nfa.bfs[head];
+            for (std::uint32_t j = nfa.edge_off[u]; j < nfa.edge_off[u + 1]; ++j) nfa.bfs.push_back(nfa.edge_to[j]);
+            if (head + 1 == level_at.back() && nfa.bfs.size() > level_at.back())
+                level_at.push_back(static_cast<std::uint32_t>(nfa.bfs.size()));
+        }
+    }
+    nfa.fail.assign(n, 0);
+    nfa.delta.assign(static_cast<std::size_t>(n) * K, 0u);
+    nfa.fol.assign(static_cast<std::size_t>(n) * K, 0);
+    nfa.fesc.assign(n, 0);
+    std::vector<std::uint32_t> olen(n, 0);
+    auto own_edges = [&](std::uint32_t s) {
+        const std::size_t row = static_cast<std::size_t>(s) * K;
+        for (std::uint32_t j = nfa.edge_off[s]; j < nfa.edge_off[s + 1]; ++j) {
+            const int c = col_of[nfa.edge_byte[j]];
+            nfa.delta[row + c] = nfa.edge_to[j];
+            nfa.fol[row + c] = 0;
+        }
+    };
+    {
+        Phase ph("levels: fail + rows");
+        own_edges(0);  // root: its own edges, every other column stays at the root, no follows
+        for (std::size_t L = 1; L + 1 < level_at.size(); ++L) {
+            const std::uint32_t l0 = level_at[L], l1 = level_at[L + 1];
+            parallel_for(l1 - l0, 4096, [&](std::size_t lo, std::size_t hi) {
+                for (std::size_t i = l0 + lo; i < l0 + hi; ++i) {
+                    const std::uint32_t s = nfa.bfs[i], p = par[s];
+                    // fail(child of p by b) = next_state(fail(p), b) (:205-215)
+                    const std::uint32_t f =
+                        p == 0 ? 0u : nfa.delta[static_cast<std::size_t>(nfa.fail[p]) * K + col_of[in_byte[s]]];
+                    nfa.fail[s] = f;
+                    const std::size_t row = static_cast<std::size_t>(s) * K, frow = static_cast<std::size_t>(f) * K;
+                    for (std::uint32_t c = 0; c < K; ++c) {
+                        nfa.delta[row + c] = nfa.delta[frow + c];
+                        const std::uint32_t v = 1u + nfa.fol[frow + c];  // one failure link, then retry
+                        nfa.fol[row + c] = static_cast<std::uint16_t>(std::min<std::uint32_t>(v, 0xFFFF));
+                    }
+                    own_edges(s);
+                    nfa.fesc[s] = static_cast<std::uint16_t>(std::min<std::uint32_t>(1u + nfa.fesc[f], 0xFFFF));
+                    olen[s] = own_n[s] + olen[f];  // own ids and out(fail(s)) are disjoint (:219-225)
+                }
+            });
+        }
+    }
+    {
+        Phase ph("levels: outputs");
+        nfa.out_off.assign(static_cast<std::size_t>(n) + 1, 0);
+        for (std::uint32_t s = 0; s < n; ++s) nfa.out_off[s + 1] = nfa.out_off[s] + olen[s];
+        nfa.out_ids.resize(nfa.out_off[n]);
+        for (std::size_t L = 1; L + 1 < level_at.size(); ++L) {
+            const std::uint32_t l0 = level_at[L], l1 = level_at[L + 1];
+            parallel_for(l1 - l0, 4096, [&](std::size_t lo, std::size_t hi) {
+                for (std::size_t i = l0 + lo; i < l0 + hi; ++i) {
+                    const std::uint32_t s = nfa.bfs[i];
+                    if (!olen[s]) continue;
+                    const std::uint32_t f = nfa.fail[s];
+                    const std::uint32_t* own = ord.data() + (own_n[s] ? own_lo[s] : 0);
+                    std::merge(own, own + own_n[s], nfa.out_ids.begin() + nfa.out_off[f],
+                               nfa.out_ids.begin() + nfa.out_off[f] + olen[f], nfa.out_ids.begin() + nfa.out_off[s]);
+                }
+            });
+        }
+    }
 
     // dense root row (:230-231)
     std::fill(std::begin(nfa.root_row), std::end(nfa.root_row), 0u);
     for (std::uint32_t j = nfa.edge_off[0]; j < nfa.edge_off[1]; ++j) nfa.root_row[nfa.edge_byte[j]] = nfa.edge_to[j];
     nfa.n_patterns = count;
     nfa.max_len = max_len;
-    nfa.min_len = ~0u;
-    for (std::uint32_t i = 0; i < count; ++i)
-        nfa.min_len = std::min<std::uint32_t>(nfa.min_len, static_cast<std::uint32_t>(offs[i + 1] - offs[i]));
+    nfa.min_len = min_len;
     nfa.pat_bytes.assign(concat, concat + offs[count]);
     nfa.pat_off.assign(offs, offs + count + 1);
     for (auto& o : nfa.pat_off) o -= offs[0];
+    (void)base;
     return kOk;
 }
 
@@ -230,6 +345,7 @@ namespace {
 // 0..kQSample-1 into the blocked Bloom filter and the exact (code -> (pattern,
 // offset) list) hash table.
 void compile_qfilter(const Nfa& nfa, Dfa& d) {
+    Phase ph_all("compile_qfilter");
     d.filter_ok = false;
     d.qbloom.clear();
     d.qbloom2.clear();
@@ -252,7 +368,9 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
             grams.emplace_back(c, (p << 2) | o);
         }
     }
-    std::sort(grams.begin(), grams.end());
+    Phase ph_g("  grams sort+tables");
+    parallel_sort(grams, [](const std::pair<std::uint32_t, std::uint32_t>& x, const std::pair<std::uint32_t, std::uint32_t>& y) { return x < y; });
+    ph_g.next("  bloom level 1");
     std::uint32_t words = kQWords;
     if (const char* e = std::getenv("ACG_QWORDS")) {  // experiments only (Bloom size sweeps)
         const long v = std::strtol(e, nullptr, 10);
@@ -266,6 +384,7 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         const std::uint32_t h = qhash(qtop(grams[i].first, q));
         d.qbloom[qword(h, words)] |= qmask(h);
     }
+    ph_g.next("  q-gram table");
     // load factor <= 1/4: a random (non-key) code ends its probe in ~1.4 slots
     d.qtab_bits = 10;
     while (d.qtab_bits < 28 && (1ull << d.qtab_bits) < 4ull * keys) ++d.qtab_bits;
@@ -285,21 +404,29 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         if (i - first == 1 && grams[first].second < 0x7FFFFFFFu) d.qtab[2 * slot + 1] = kQSingle | grams[first].second;
     }
     d.qb_off.push_back(static_cast<std::uint32_t>(d.qb_ent.size()));
+    ph_g.next("  pattern codes");
     d.pat_off32.assign(nfa.pat_off.begin(), nfa.pat_off.end());
     d.pat_code.assign(2ull * nfa.n_patterns, 0ull);
-    for (std::uint32_t p = 0; p < nfa.n_patterns; ++p) {
-        const std::uint32_t lo = nfa.pat_off[p], len = std::min<std::uint32_t>(nfa.pat_off[p + 1] - lo, 64);
-        for (std::uint32_t k = 0; k < len; ++k)
-            d.pat_code[2ull * p + k / 32] |= static_cast<std::uint64_t>((nfa.pat_bytes[lo + k] >> 1) & 3u) << (2 * (k % 32));
-    }
+    parallel_for(nfa.n_patterns, 8192, [&](std::size_t p0, std::size_t p1) {
+        for (std::size_t p = p0; p < p1; ++p) {
+            const std::uint64_t lo = nfa.pat_off[p];
+            const std::uint32_t len = static_cast<std::uint32_t>(std::min<std::uint64_t>(nfa.pat_off[p + 1] - lo, 64));
+            for (std::uint32_t k = 0; k < len; ++k)
+                d.pat_code[2 * p + k / 32] |= static_cast<std::uint64_t>((nfa.pat_bytes[lo + k] >> 1) & 3u) << (2 * (k % 32));
+        }
+    });
     // pass rates of random q-grams (splitmix64 sample), level 1 and overall
     auto pass_rates = [&](double& fp1, double& fp) {
-        std::uint64_t z = 0x14037294ull, p1 = 0, p2 = 0;
-        const std::uint32_t trials = 1u << 20;
+        const std::uint32_t trials = 1u << 20, pieces = 64;
         const std::uint32_t words2 = static_cast<std::uint32_t>(d.qbloom2.size());
-        for (std::uint32_t t = 0; t < trials; ++t) {
-            z += 0x9E3779B97F4A7C15ull;
-            std::uint64_t r = z;
+        std::vector<std::uint64_t> c1(pieces, 0), c2(pieces, 0);
+        parallel_for(pieces, 1, [&](std::size_t k0, std::size_t k1) {
+          for (std::size_t piece = k0; piece < k1; ++piece) {
+            std::uint64_t& p1 = c1[piece];
+            std::uint64_t& p2 = c2[piece];
+            for (std::uint32_t t = static_cast<std::uint32_t>(piece) * (trials / pieces);
+                 t < static_cast<std::uint32_t>(piece + 1) * (trials / pieces); ++t) {
+            std::uint64_t r = 0x14037294ull + (static_cast<std::uint64_t>(t) + 1) * 0x9E3779B97F4A7C15ull;
             r = (r ^ (r >> 30)) * 0xBF58476D1CE4E5B9ull;
             r = (r ^ (r >> 27)) * 0x94D049BB133111EBull;
             const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
@@ -313,11 +440,19 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
             }
             const std::uint32_t h2 = qhash2(h), m2 = qmask(h2);
             p2 += (d.qbloom2[qword(h2, words2)] & m2) == m2;
-        }
+            }
+          }
+        });
+        std::uint64_t p1 = 0, p2 = 0;
+        for (std::uint32_t k = 0; k < pieces; ++k) p1 += c1[k], p2 += c2[k];
         fp1 = static_cast<double>(p1) / trials;
         fp = static_cast<double>(p2) / trials;
     };
-    pass_rates(d.filter_fp1, d.filter_fp);
+    {
+        Phase ph("  filter pass rates");
+        pass_rates(d.filter_fp1, d.filter_fp);
+    }
+    ph_g.next("  level 2");
     if (d.filter_fp > 5e-3 && d.filter_fp1 <= kQLevel1Max) {
         // level 2: ~1.5 % of its bits set (4 bits per key)
         std::uint64_t w2 = (static_cast<std::uint64_t>(keys) * 4 * 100 / 3 / 32 + 3) & ~3ull;
@@ -347,73 +482,17 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
 
 void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& d,
                  std::uint32_t hot_limit) {
+    Phase ph_all("compile_dfa (total)");
+    Phase ph_ord("  hot order");
     const std::uint32_t S = nfa.state_count();
-    // Alphabet: which bytes occur in patterns (as goto labels).
-    bool used[256] = {};
-    for (std::uint8_t b : nfa.edge_byte) used[b] = true;
-    std::uint32_t n_sym = 0;
-    for (bool u : used) n_sym += u;
-    const bool dna = [&] {
-        for (int b = 0; b < 256; ++b)
-            if (used[b] && b != 'A' && b != 'C' && b != 'G' && b != 'T') return false;
-        return true;
-    }();
-    // column -> byte (or -1 for the escape column)
-    std::vector<int> col_byte;
-    if (dna) {
-        d.mode = kAlphaDna4;
-        d.K = 4;
-        col_byte = {'A', 'C', 'T', 'G'};  // column = (byte >> 1) & 3
-        std::memset(d.symmap, 0, sizeof d.symmap);
-        for (int c = 0; c < 4; ++c) d.symmap[col_byte[c]] = static_cast<std::uint8_t>(c);
-    } else {
-        d.mode = kAlphaGeneric;
-        d.K = n_sym + 1;
-        std::uint32_t c = 0;
-        for (int b = 0; b < 256; ++b)
-            if (used[b]) {
-                d.symmap[b] = static_cast<std::uint8_t>(c++);
-                col_byte.push_back(b);
-            }
-        for (int b = 0; b < 256; ++b)
-            if (!used[b]) d.symmap[b] = static_cast<std::uint8_t>(n_sym);  // escape column
-        col_byte.push_back(-1);
-    }
-    d.n_sym = n_sym;
+    // alphabet and dense rows come from the build (build_nfa: delta, fol, fesc)
+    d.mode = nfa.mode;
+    d.K = nfa.K;
+    d.n_sym = nfa.n_sym;
+    std::memcpy(d.symmap, nfa.symmap, sizeof d.symmap);
     const std::uint32_t K = d.K;
     d.S = S;
-
-    // Dense delta in NFA numbering, computed in BFS order:
-    // delta(s,c) = goto(s,c) if present else delta(fail(s),c); root misses stay at root.
-    std::vector<std::uint32_t> delta(static_cast<std::size_t>(S) * K);
-    std::vector<std::uint32_t> fol(static_cast<std::size_t>(S) * K);
-    std::vector<std::uint32_t> fesc(S, 0);
-    // (row = the fail state's row, one more follow per column, then the state's
-    // own goto edges; the fail state precedes s in BFS order)
-    int col_of[256];
-    std::fill(std::begin(col_of), std::end(col_of), -1);
-    for (std::uint32_t c = 0; c < K; ++c)
-        if (col_byte[c] >= 0) col_of[col_byte[c]] = static_cast<int>(c);
-    for (std::uint32_t s : nfa.bfs) {
-        const std::size_t row = static_cast<std::size_t>(s) * K;
-        if (s == 0) {
-            std::fill_n(delta.begin() + row, K, 0u);
-            std::fill_n(fol.begin() + row, K, 0u);
-        } else {
-            const std::size_t frow = static_cast<std::size_t>(nfa.fail[s]) * K;
-            for (std::uint32_t c = 0; c < K; ++c) {
-                delta[row + c] = delta[frow + c];
-                fol[row + c] = 1 + fol[frow + c];  // reference follows one failure link, then retries
-            }
-        }
-        for (std::uint32_t j = nfa.edge_off[s]; j < nfa.edge_off[s + 1]; ++j) {
-            const int c = col_of[nfa.edge_byte[j]];
-            if (c < 0) continue;  // (every pattern byte has a column)
-            delta[row + c] = nfa.edge_to[j];
-            fol[row + c] = 0;
-        }
-        fesc[s] = s == 0 ? 0 : 1 + fesc[nfa.fail[s]];
-    }
+    const std::vector<std::uint32_t>& delta = nfa.delta;
 
     // Hotness order: BFS (shallow first), or visit counts on a text sample.
     std::vector<std::uint32_t> hot_order(nfa.bfs.begin(), nfa.bfs.end());
@@ -451,6 +530,8 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
     d.dev_of.assign(S, 0);
     for (std::uint32_t i = 0; i < S; ++i) d.dev_of[d.nfa_of[i]] = i;
 
+    ph_ord.next("  (sub-phase end)");
+    Phase ph_ren("  renumber rows");
     d.next.resize(static_cast<std::size_t>(S) * K);
     d.follows.resize(static_cast<std::size_t>(S) * K);
     d.follows_esc.resize(S);
@@ -458,29 +539,30 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
     d.depth.resize(S);
     for (std::uint32_t i = 0; i < S; ++i) {
         const std::uint32_t s = d.nfa_of[i];
-        d.depth[i] = nfa.depth[s];
-        for (std::uint32_t c = 0; c < K; ++c) {
-            d.next[static_cast<std::size_t>(i) * K + c] = d.dev_of[delta[static_cast<std::size_t>(s) * K + c]];
-            const std::uint32_t f = fol[static_cast<std::size_t>(s) * K + c];
-            d.follows[static_cast<std::size_t>(i) * K + c] = static_cast<std::uint16_t>(std::min<std::uint32_t>(f, 0xFFFF));
-        }
-        d.follows_esc[i] = static_cast<std::uint16_t>(std::min<std::uint32_t>(fesc[s], 0xFFFF));
         d.out_off[i + 1] = d.out_off[i] + (nfa.out_off[s + 1] - nfa.out_off[s]);
     }
     d.out_ids.resize(d.out_off[S]);
-    for (std::uint32_t i = 0; i < S; ++i) {
-        const std::uint32_t s = d.nfa_of[i];
-        std::copy(nfa.out_ids.begin() + nfa.out_off[s], nfa.out_ids.begin() + nfa.out_off[s + 1],
-                  d.out_ids.begin() + d.out_off[i]);
-    }
     d.outinfo.assign(S, 0ull);
-    for (std::uint32_t i = 0; i < S; ++i) {
-        const std::uint32_t lo = d.out_off[i], cnt = d.out_off[i + 1] - lo;
-        if (!cnt) continue;
-        const std::uint64_t first = d.out_ids[lo];
-        d.outinfo[i] = lo | (static_cast<std::uint64_t>(std::min<std::uint32_t>(cnt, 255)) << 32) |
-                       ((first < (1u << 24) ? first : 0ull) << 40);
-    }
+    parallel_for(S, 1 << 14, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const std::uint32_t s = d.nfa_of[i];
+            d.depth[i] = nfa.depth[s];
+            const std::size_t row = i * K, srow = static_cast<std::size_t>(s) * K;
+            for (std::uint32_t c = 0; c < K; ++c) {
+                d.next[row + c] = d.dev_of[delta[srow + c]];
+                d.follows[row + c] = nfa.fol[srow + c];
+            }
+            d.follows_esc[i] = nfa.fesc[s];
+            std::copy(nfa.out_ids.begin() + nfa.out_off[s], nfa.out_ids.begin() + nfa.out_off[s + 1],
+                      d.out_ids.begin() + d.out_off[i]);
+            const std::uint32_t lo2 = d.out_off[i], cnt = d.out_off[i + 1] - lo2;
+            if (!cnt) continue;
+            const std::uint64_t first = d.out_ids[lo2];
+            d.outinfo[i] = lo2 | (static_cast<std::uint64_t>(std::min<std::uint32_t>(cnt, 255)) << 32) |
+                           ((first < (1u << 24) ? first : 0ull) << 40);
+        }
+    });
+    ph_ren.next("  hot tables");
     d.hot16.assign(static_cast<std::size_t>(H + 1) * K, 0xFFFF);
     for (std::size_t i = 0; i < static_cast<std::size_t>(H) * K; ++i)
         if (d.next[i] < H) d.hot16[i] = static_cast<std::uint16_t>(d.next[i]);
@@ -490,16 +572,17 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
     d.sparse_ok = !(visits && visits->size() == S) && d.mode == kAlphaDna4 && H <= 0x7FFF;
     if (d.sparse_ok) {
         d.hotH.assign(static_cast<std::size_t>(H) * K, 0);
-        for (std::uint32_t i = 0; i < H; ++i) {
-            for (std::uint32_t c = 0; c < K; ++c) {
-                const std::uint32_t t = d.next[static_cast<std::size_t>(i) * K + c];  // true target (device id)
-                std::uint32_t h = d.nfa_of[t];
-                while (d.dev_of[h] >= H) h = nfa.fail[h];  // first hot state on t's fail chain
-                const bool attn = t >= H || has_out(d.nfa_of[t]);
-                d.hotH[static_cast<std::size_t>(i) * K + c] =
-                    static_cast<std::uint16_t>(d.dev_of[h] | (attn ? 0x8000u : 0u));
+        parallel_for(H, 4096, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t i = lo; i < hi; ++i) {
+                for (std::uint32_t c = 0; c < K; ++c) {
+                    const std::uint32_t t = d.next[i * K + c];  // true target (device id)
+                    std::uint32_t h = d.nfa_of[t];
+                    while (d.dev_of[h] >= H) h = nfa.fail[h];  // first hot state on t's fail chain
+                    const bool attn = t >= H || has_out(d.nfa_of[t]);
+                    d.hotH[i * K + c] = static_cast<std::uint16_t>(d.dev_of[h] | (attn ? 0x8000u : 0u));
+                }
             }
-        }
+        });
     }
     d.id_bits = 1;
     while ((1ull << d.id_bits) < nfa.n_patterns) ++d.id_bits;

@@ -35,6 +35,15 @@ struct Nfa {
     std::uint32_t min_len = 0;
     std::vector<std::uint8_t> pat_bytes;  // the dictionary as given (q-gram prefilter build)
     std::vector<std::uint64_t> pat_off;   // n_patterns + 1
+    // Dense image built level by level with the failure links (NFA numbering):
+    // columns = symbol classes of the pattern alphabet (Dfa::mode / K / symmap).
+    int mode = 1;                         // AlphaMode
+    std::uint32_t K = 0, n_sym = 0;
+    std::uint8_t symmap[256] = {};
+    std::vector<int> col_byte;            // column -> byte (-1: escape column)
+    std::vector<StateId> delta;           // S*K: next_state(s, byte of column c)
+    std::vector<std::uint16_t> fol;       // S*K: failure links the reference walk follows (saturating)
+    std::vector<std::uint16_t> fesc;      // S: ... for a byte outside the alphabet (dna4 mode)
 
     std::uint32_t state_count() const { return static_cast<std::uint32_t>(fail.size()); }
     bool goto_transition(StateId s, std::uint8_t b, StateId* out) const;

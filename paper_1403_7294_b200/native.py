@@ -31,6 +31,9 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+HOST_SOURCES = ("automaton.cpp", "parallel.cpp")  # host C++ of libacg.so
+
+
 def build(force: bool = False, verbose_ptxas: bool = False) -> None:
     os.makedirs(LIB, exist_ok=True)
     obj = os.path.join(LIB, "obj")
@@ -43,12 +46,15 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         _run(["g++", "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", synth, src])
 
     headers = [os.path.join(CSRC, h) for h in ("automaton.hpp", "scan_kernels.cuh", "filter_kernels.cuh",
-                                               "qfilter.hpp")] + [
+                                               "exact_kernels.cuh", "qfilter.hpp", "parallel.hpp")] + [
         os.path.join(ROOT, "include", "acg.h")]
-    auto_src = os.path.join(CSRC, "automaton.cpp")
-    auto_o = os.path.join(obj, "automaton.o")
-    if force or _stale(auto_o, [auto_src] + headers):
-        _run(["g++", "-std=c++17", "-O3", "-fPIC", "-c", "-o", auto_o, auto_src] + inc)
+    host_objs = []
+    for name in HOST_SOURCES:
+        src_c = os.path.join(CSRC, name)
+        o = os.path.join(obj, name.replace(".cpp", ".o"))
+        if force or _stale(o, [src_c] + headers):
+            _run(["g++", "-std=c++17", "-O3", "-fPIC", "-pthread", "-c", "-o", o, src_c] + inc)
+        host_objs.append(o)
     dev_src = os.path.join(CSRC, "acg_device.cu")
     dev_o = os.path.join(obj, "acg_device.o")
     if force or _stale(dev_o, [dev_src] + headers):
@@ -57,8 +63,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
     lib = os.path.join(LIB, "libacg.so")
-    if force or _stale(lib, [auto_o, dev_o]):
-        _run([NVCC, *ARCH, "-shared", "-o", lib, auto_o, dev_o, "-Xcompiler", "-pthread"])
+    if force or _stale(lib, host_objs + [dev_o]):
+        _run([NVCC, *ARCH, "-shared", "-o", lib, *host_objs, dev_o, "-Xcompiler", "-pthread"])
 
 
 def build_variant(name: str, defines: list[str]) -> str:
@@ -70,7 +76,8 @@ def build_variant(name: str, defines: list[str]) -> str:
     _run([NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", "-o", dev_o,
           os.path.join(CSRC, "acg_device.cu")] + inc + [f"-D{d}" for d in defines])
     lib = os.path.join(out, "libacg.so")
-    _run([NVCC, *ARCH, "-shared", "-o", lib, os.path.join(LIB, "obj", "automaton.o"), dev_o, "-Xcompiler", "-pthread"])
+    host_objs = [os.path.join(LIB, "obj", name.replace(".cpp", ".o")) for name in HOST_SOURCES]
+    _run([NVCC, *ARCH, "-shared", "-o", lib, *host_objs, dev_o, "-Xcompiler", "-pthread"])
     return lib
 
 

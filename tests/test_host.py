@@ -155,3 +155,39 @@ def test_scan_without_device_raises_device_error():
     a = am.build(am.make_patterns([b"HIS", b"SHE", b"HERS"]))
     with pytest.raises(am.DeviceError):
         am.scan(a, b"USHERS")
+
+
+@pytest.mark.parametrize("cfg", range(5))
+def test_full_machine_equals_reference_on_config_dictionaries(cfg):
+    """The bulk (sort-based, level-parallel) build against the REFERENCE's own
+    build (oracle/_ref), state by state over the whole machine — failure links,
+    depths, sorted edges, suffix-closed output sets — on every BASELINE
+    config's full dictionary (up to cfg2's 100,000 patterns, 1.85M states)."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref (the reference compiled here) is not built")
+    concat, offs = synth.patterns(synth.CONFIGS[cfg])
+    mine = am.Automaton.from_arrays(concat, offs).nfa_arrays()
+    theirs = oracle.RefAutomaton(concat, offs).export()
+    for k in ("fail", "depth", "edge_off", "edge_byte", "edge_to", "out_off", "out_ids"):
+        assert np.array_equal(mine[k], theirs[k]), k
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_bulk_build_duplicates_prefixes_and_bytes(seed):
+    """Duplicate patterns, patterns that are prefixes of others, ids whose
+    insertion order disagrees with lexicographic order, the full byte range."""
+    rng = np.random.default_rng(1000 + seed)
+    alpha = [b"AB", b"ACGT", bytes(range(256))][seed % 3]
+    words = []
+    for _ in range(int(rng.integers(1, 400))):
+        n = int(rng.integers(1, 9))
+        words.append(bytes(alpha[int(i)] for i in rng.integers(0, len(alpha), n)))
+    words += [w[: max(1, len(w) // 2)] for w in words[:50]] + words[:30]  # prefixes and duplicates
+    rng.shuffle(words)
+    concat, offs = oracle.pack(words)
+    mine = am.Automaton.from_arrays(concat, offs).nfa_arrays()
+    ref = (oracle.RefAutomaton(concat, offs).export() if oracle.ref_available() else None)
+    if ref is None:
+        pytest.skip("oracle/_ref is not built")
+    for k in mine:
+        assert np.array_equal(mine[k], ref[k]), k
