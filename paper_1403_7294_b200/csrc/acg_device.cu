@@ -916,7 +916,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     plan_geometry(s, owned);
     const bool prof = s->flags & ACG_SCAN_PROFILE;
 
-    const std::uint32_t n_out_states = (d.H - d.Hn) + (d.S - d.Cn);
+    const std::uint32_t n_out_states = d.Cn - d.Hn;  // [Hn, Cn)
     ACG_CUDA(s->chunk_counts.reserve(s->n_chunks, st));
     ACG_CUDA(s->chunk_offs.reserve(s->n_chunks + 1, st));
     ACG_CUDA(s->active_list.reserve(s->n_chunks, st));
@@ -1131,7 +1131,11 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         zero_later(s, s->scalars64.p + 8, sizeof(unsigned long long));
         ACG_CUDA(flush_zeros(s, st));
         s->ev_run = true;
-        ACG_CUDA(launch_event_walk(d.mode, s->U_run, a, s->eargs, s->grid, s->tpb_run, smem_bytes(dd), st));
+        // KE strides chunks over the CTAs (exact_kernels.cuh): a full one-per-SM grid
+        // whenever there are enough chunks, whatever the per-block rounding
+        const unsigned g_ev = static_cast<unsigned>(std::max<unsigned long long>(
+            s->grid, std::min<unsigned long long>(dd.num_sms, (s->n_chunks + s->U_run - 1) / s->U_run)));
+        ACG_CUDA(launch_event_walk(d.mode, s->U_run, a, s->eargs, g_ev, s->tpb_run, smem_bytes(dd), st));
         ++s->launches;
         if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
         const bool smem_bins = want_counts && static_cast<std::size_t>(n_out_states) * 4 <= kEventBinsMax;

@@ -523,10 +523,10 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
         if (has_out(hot_order[i])) d.nfa_of.push_back(hot_order[i]);
     d.H = static_cast<std::uint32_t>(H);
     for (std::size_t i = H; i < S; ++i)
-        if (!has_out(hot_order[i])) d.nfa_of.push_back(hot_order[i]);
+        if (has_out(hot_order[i])) d.nfa_of.push_back(hot_order[i]);
     d.Cn = static_cast<std::uint32_t>(d.nfa_of.size());
     for (std::size_t i = H; i < S; ++i)
-        if (has_out(hot_order[i])) d.nfa_of.push_back(hot_order[i]);
+        if (!has_out(hot_order[i])) d.nfa_of.push_back(hot_order[i]);
     d.dev_of.assign(S, 0);
     for (std::uint32_t i = 0; i < S; ++i) d.dev_of[d.nfa_of[i]] = i;
 

@@ -78,7 +78,8 @@ struct Dfa {
     std::uint32_t n_sym = 0;    // distinct pattern bytes
     std::uint8_t symmap[256];   // byte -> column (generic mode); escape = K-1
     std::uint32_t S = 0;
-    // device numbering: [0,Hn) hot non-output, [Hn,H) hot output, [H,Cn) cold non-output, [Cn,S) cold output
+    // device numbering: [0,Hn) hot non-output, [Hn,H) hot output, [H,Cn) cold output, [Cn,S) cold non-output
+    // (the output states [Hn,Cn) are contiguous: output rank = s - Hn)
     std::uint32_t H = 0, Hn = 0, Cn = 0;
     std::vector<std::uint32_t> dev_of;   // NFA id -> device id
     std::vector<std::uint32_t> nfa_of;   // device id -> NFA id

@@ -27,6 +27,8 @@
 //        chunk: the canonical (end, id) order of aho_corasick.hpp:38-41).
 #pragma once
 
+#include <type_traits>
+
 #include "scan_kernels.cuh"
 
 namespace acg {
@@ -85,60 +87,86 @@ __device__ __forceinline__ void ev_put(const EventArgs& e, std::uint32_t v, std:
 
 __device__ __forceinline__ std::uint32_t out_rank_of(std::uint32_t s, std::uint32_t H, std::uint32_t Hn,
                                                     std::uint32_t Cn) {
-    return s < H ? s - Hn : (H - Hn) + (s - Cn);
+    (void)H;
+    (void)Cn;
+    return s - Hn;  // output states [Hn, Cn) are contiguous
 }
 __device__ __forceinline__ std::uint32_t state_of_rank(std::uint32_t r, std::uint32_t H, std::uint32_t Hn,
                                                       std::uint32_t Cn) {
-    return r < H - Hn ? Hn + r : Cn + (r - (H - Hn));
+    (void)H;
+    (void)Cn;
+    return Hn + r;
 }
 
 // ===================================================================== KE ==
+// Chunk c of the stream (thread t, slot u) in CTA b: c = (t*U + u) * gridDim + b,
+// so every CTA of a one-per-SM grid gets the same number of chunks whatever the
+// chunk count's rounding.
+//
+// Per step and stream (fast path): the column from the 16-byte word (PRMT +
+// a shared-memory byte map, or 2-bit codes for DNA), t = s*K + col, the hot
+// row entry LDS [min(t, H*K)] (row H is all-escape), the L2 load of the cold
+// row entry only under the escape predicate, then the output test on the
+// contiguous output range [Hn, Cn) and a PREDICATED store of the event: no
+// per-event branch. Each owned 16-step block starts with >= 16 free slots in
+// the chunk's current region (else the region is closed with filler events
+// and continued in a pool block), so the stores need no bounds check.
+constexpr std::uint32_t kEvPad = 0xFFFFFFFFu;  // filler slot of a region closed early: expands to nothing
+
 template <int U, int MODE>
 __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_event_kernel(const ScanArgs a, const EventArgs e) {
     extern __shared__ __align__(16) std::uint8_t smem[];
-    const std::uint32_t hot_s = smem_u32(smem);
-    const std::uint8_t* smap = smem + a.smem_table_bytes;
-
-    const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (static_cast<long long>(blockIdx.x) * blockDim.x * U >= a.n_chunks) return;  // whole block idle
+    std::uint8_t* smap = smem + a.smem_table_bytes;  // byte -> column (MODE 1)
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.hot16);
         uint4* dst = reinterpret_cast<uint4*>(smem);
         for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
         if (MODE == 1)
-            for (std::uint32_t i = threadIdx.x; i < 256; i += blockDim.x) smem[a.smem_table_bytes + i] = a.symmap[i];
+            for (std::uint32_t i = threadIdx.x; i < 256; i += blockDim.x) smap[i] = a.symmap[i];
     }
     __syncthreads();
+    const std::uint32_t hot_s = smem_u32(smem);
 
-    bool act[U];
+    const long long G = gridDim.x;
+    long long cid[U];
+    bool act[U], live[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        cid[u] = (static_cast<long long>(threadIdx.x) * U + u) * G + blockIdx.x;
+        act[u] = cid[u] < a.n_chunks;
+        live[u] = act[u];
+    }
+    if (!act[0]) return;  // (cid ascends with u: no stream of this thread is active)
+    const std::uint32_t K = a.K, HK = a.H * a.K, Hn = a.Hn, nout = a.Cn - a.Hn, ob = e.ob;
+    const long long halo = a.halo, steps = a.halo + a.chunk, n = a.n;
+    const std::uint32_t* __restrict__ next = a.next;
+    std::uint32_t* __restrict__ ev = e.ev;
+
     std::uint32_t st[U], wr[U], lim[U], cnt[U];
     long long pos0[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const long long c = tid * U + u;
-        act[u] = c < a.n_chunks;
         st[u] = 0;
         cnt[u] = 0;
-        wr[u] = act[u] ? slab_start(e, c) : 0u;
-        lim[u] = act[u] ? slab_end(e, c) - 1u : 0u;  // last slot = link to a pool block
-        pos0[u] = a.emit_from + c * a.chunk - a.halo;
+        wr[u] = act[u] ? slab_start(e, cid[u]) : 0u;
+        lim[u] = act[u] ? slab_end(e, cid[u]) - 1u : 0u;  // last slot = link to a pool block
+        pos0[u] = a.emit_from + cid[u] * a.chunk - halo;
     }
-    if (!act[0]) return;
-    const std::uint32_t K = a.K, H = a.H, Hn = a.Hn, Cn = a.Cn, ob = e.ob;
-    const long long halo = a.halo, steps = a.halo + a.chunk;
 
     uint4 w[U];
     auto load = [&](long long off) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const long long p = pos0[u] + off;
-            w[u] = (act[u] && p >= 0 && p < a.n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
+            w[u] = (act[u] && p >= 0 && p < n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
         }
     };
-    // an owned step that entered output state s at chunk offset o
-    auto log = [&](int u, std::uint32_t s, long long o) {
-        ev_put(e, (static_cast<std::uint32_t>(o - halo) << ob) | out_rank_of(s, H, Hn, Cn), wr[u], lim[u]);
-        ++cnt[u];
+    // next-state lookup for the byte of column `col` (t = s*K + col)
+    auto step = [&](std::uint32_t s, std::uint32_t col) -> std::uint32_t {
+        const std::uint32_t t = s * K + col;
+        std::uint32_t v = lds_u16z(hot_s + 2u * min(t, HK));
+        if (v == kEsc16) v = __ldg(next + t);
+        return v;
     };
     load(0);
     for (long long off = 0; off < steps; off += 16) {
@@ -147,12 +175,26 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_event_kerne
         for (int u = 0; u < U; ++u) cur[u] = w[u];
         if (off + 16 < steps) load(off + 16);
         const bool owned_blk = off >= halo;  // halo is a multiple of 16: blocks are all-owned or all-warm-up
+        std::uint32_t wr0[U];
+        if (owned_blk) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (live[u] && lim[u] - wr[u] < 16u) {  // close the region, continue in a pool block
+                    for (; wr[u] < lim[u]; ++wr[u], ++cnt[u]) ev[wr[u]] = kEvPad;
+                    const uint2 g = ev_grow(ev, e.pool_used, e.pool_base, e.pool_blocks, lim[u]);
+                    wr[u] = g.x;
+                    lim[u] = g.y;
+                    if (g.y == 0u) live[u] = false;  // pool exhausted: the host replays the run
+                }
+                wr0[u] = wr[u];
+            }
+        }
         bool fast = true;
         std::uint32_t pk[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const long long p = pos0[u] + off;
-            const bool full = p >= 0 && p + 16 <= a.n;
+            const bool full = p >= 0 && p + 16 <= n;
             if (MODE == 0) {
                 std::uint32_t bad = 0;
                 pk[u] = dna4_pack(cur[u], bad);
@@ -162,53 +204,66 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_event_kerne
                 fast = fast && (!act[u] || full);
             }
         }
-        if (fast) {
+        // event word of step k: (offset in chunk << ob) + output rank
+        std::uint32_t kk = owned_blk ? static_cast<std::uint32_t>(off - halo) << ob : 0u;
+        const std::uint32_t kinc = 1u << ob;
+        // 16 steps of all U streams; LOG: owned block (events), else warm-up
+        auto fast_block = [&](auto log_tag) {
+            constexpr bool LOG = decltype(log_tag)::value;
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                std::uint32_t col[U], v[U];
+                std::uint32_t v[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
+                    std::uint32_t col;
                     if (MODE == 0) {
-                        col[u] = (pk[u] >> (2 * k)) & 3u;
+                        col = (pk[u] >> (2 * k)) & 3u;
                     } else {
                         const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
-                        col[u] = smap[(word >> ((k & 3) * 8)) & 0xFFu];
+                        col = smap[__byte_perm(word, 0u, 0x4440u + (k & 3))];
                     }
-                    v[u] = lds_u16(hot_s + 2u * (min(st[u], H) * K + col[u]));
+                    v[u] = step(st[u], col);
                 }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (v[u] == kEsc16) v[u] = __ldg(a.next + st[u] * K + col[u]);
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     st[u] = v[u];
-                    if (owned_blk && act[u] && ((st[u] >= Hn && st[u] < H) || st[u] >= Cn)) log(u, st[u], off + k);
+                    if (LOG) {
+                        const std::uint32_t r = v[u] - Hn;
+                        if (live[u] && r < nout) ev[wr[u]++] = kk + r;
+                    }
                 }
+                if (LOG) kk += kinc;
             }
+        };
+        if (fast) {
+            if (owned_blk) fast_block(std::true_type{});
+            else fast_block(std::false_type{});
         } else {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (!act[u]) continue;
+                std::uint32_t kq = kk;
 #pragma unroll 1
-                for (int k = 0; k < 16; ++k) {
+                for (int k = 0; k < 16; ++k, kq += kinc) {
                     const long long p = pos0[u] + off + k;
-                    const bool inside = p >= 0 && p < a.n;
+                    const bool inside = p >= 0 && p < n;
                     const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
                     const int c = inside ? column_of<MODE>((word >> (8 * (k & 3))) & 0xFFu, smap, a) : -1;
-                    std::uint32_t nx = 0;
-                    if (c >= 0) {
-                        nx = lds_u16(hot_s + 2u * (min(st[u], H) * K + c));
-                        if (nx == kEsc16) nx = __ldg(a.next + st[u] * K + c);
-                    }
+                    const std::uint32_t nx = c >= 0 ? step(st[u], static_cast<std::uint32_t>(c)) : 0u;
                     st[u] = nx;
-                    if (owned_blk && ((nx >= Hn && nx < H) || nx >= Cn)) log(u, nx, off + k);
+                    const std::uint32_t r = nx - Hn;
+                    if (owned_blk && live[u] && r < nout) ev[wr[u]++] = kq + r;
                 }
             }
+        }
+        if (owned_blk) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) cnt[u] += wr[u] - wr0[u];
         }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (act[u]) e.ev_count[tid * U + u] = cnt[u];
+        if (act[u]) e.ev_count[cid[u]] = cnt[u];
 }
 
 // Per-chunk slab sizes for the next run from this run's event counts:
@@ -275,7 +330,7 @@ __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, cons
         unsigned long long recs = 0;
         if (total) {
             for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t, std::uint32_t v, bool ok) {
-                if (!ok) return;
+                if (!ok || v == kEvPad) return;
                 const std::uint32_t r = v & rmask;
                 const std::uint32_t s = state_of_rank(r, H, Hn, Cn);
                 recs += n_out_of(s, __ldg(a.outinfo + s), a);
@@ -314,7 +369,7 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
         for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t nb, std::uint32_t v, bool ok) {
             std::uint32_t n = 0, lo = 0, first = 0;
             unsigned long long key = 0;
-            if (ok) {
+            if (ok && v != kEvPad) {
                 const std::uint32_t s = state_of_rank(v & rmask, H, Hn, Cn);
                 const unsigned long long info = __ldg(a.outinfo + s);
                 lo = static_cast<std::uint32_t>(info);

@@ -10,7 +10,8 @@
 // walks U chunks in lockstep (U independent dependent-load chains).
 //
 // Device numbering. [0,Hn) hot non-output, [Hn,H) hot output, [H,Cn) cold
-// non-output, [Cn,S) cold output; rows [0,H) are "hot" (shared memory).
+// output, [Cn,S) cold non-output; rows [0,H) are "hot" (shared memory); the
+// output states [Hn,Cn) are contiguous, output rank = s - Hn.
 //
 // Count-pass kernels:
 //
@@ -169,6 +170,13 @@ __device__ __forceinline__ std::uint32_t lds_u16(std::uint32_t saddr) {
     return v;
 }
 
+// u16 from shared memory, zero-extended into a 32-bit register
+__device__ __forceinline__ std::uint32_t lds_u16z(std::uint32_t saddr) {
+    std::uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(saddr));
+    return v;
+}
+
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -198,11 +206,11 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 }
 
 __device__ __forceinline__ std::uint32_t out_rank(std::uint32_t s, const ScanArgs& a) {
-    return s < a.H ? s - a.Hn : (a.H - a.Hn) + (s - a.Cn);
+    return s - a.Hn;
 }
 
 __device__ __forceinline__ bool has_out(std::uint32_t s, const ScanArgs& a) {
-    return (s >= a.Hn && s < a.H) || s >= a.Cn;
+    return s - a.Hn < a.Cn - a.Hn;
 }
 
 // Column of byte b (-1 = escape: every state goes to the root).
@@ -1199,10 +1207,11 @@ __global__ void __launch_bounds__(256) compact_active_kernel(const unsigned long
 __global__ void pattern_counts_kernel(const unsigned long long* visits, const std::uint32_t* out_off,
                                       const std::uint32_t* out_ids, std::uint32_t Hn, std::uint32_t H,
                                       std::uint32_t Cn, std::uint32_t S, unsigned long long* counts) {
-    const std::uint32_t n_hot_out = H - Hn;
-    const std::uint32_t n_out = n_hot_out + (S - Cn);
+    (void)H;
+    (void)S;
+    const std::uint32_t n_out = Cn - Hn;  // output states [Hn, Cn), rank = s - Hn
     for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_out; i += gridDim.x * blockDim.x) {
-        const std::uint32_t s = i < n_hot_out ? Hn + i : Cn + (i - n_hot_out);
+        const std::uint32_t s = Hn + i;
         const unsigned long long v = visits[i];
         if (!v) continue;
         for (std::uint32_t j = out_off[s]; j < out_off[s + 1]; ++j) atomicAdd(counts + out_ids[j], v);
