@@ -8,9 +8,10 @@ One step = one full pass of the hot path over the workload's text, producing
 the canonical (end, pattern id) match list and the per-pattern counts (+ an
 NCCL all-reduce of the counts when N > 1). `value` is text GB/s of the whole
 job with the text already resident in HBM, device-timed (CUDA events, max over
-ranks); `e2e` is the same metric through the public scanner API from pinned
-host memory (H2D of the text and D2H of the counts and the match list inside
-the timed region). The workload is BASELINE.json configs[1] (1 GiB iid ACGT,
+ranks); `e2e` is the same metric through the public pipelined host scan
+(acg_scan_pipelined) from pinned host memory: H2D of the text and D2H of the
+packed match list and the per-pattern counts inside the timed region, piece
+k+1's copy and scan overlapping piece k's read-back. The workload is BASELINE.json configs[1] (1 GiB iid ACGT,
 10,000 patterns of 16-64 bytes) unless --config says otherwise.
 
 Multi-GPU (one process per GPU): --scaling weak (default; cfg1) gives every
@@ -274,6 +275,7 @@ def main() -> None:
     ap.add_argument("--cpu-sample-mib", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-piece-mib", type=int, default=256, help="pipelined e2e scan: piece size (MiB)")
     ap.add_argument("--streams-per-thread", type=int, default=0)
     ap.add_argument("--threads-per-block", type=int, default=0)
     ap.add_argument("--chunk-bytes", type=int, default=0)
@@ -305,7 +307,10 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     scaling = scaling_of(args)
 
+    am.version()  # load libacg (and its CUDA driver init) outside the build timing
+    tb0 = time.perf_counter()
     a = am.Automaton.from_arrays(concat, offs)
+    build_ms = (time.perf_counter() - tb0) * 1e3  # host build: trie, failure links, dense DFA, filters
     halo_guess = ((int((offs[1:] - offs[:-1]).max()) + 15) // 16) * 16
     from dataclasses import replace
     if scaling == "weak":
@@ -419,22 +424,25 @@ def main() -> None:
     replayed_job = sum(p["replayed"] for p in parts)
     sc.__del__()  # release the timed scanner's workspace before the e2e scanner allocates its own
 
-    # e2e: the public scanner API from pinned host memory, H2D + D2H inside
-    sc_e2e = am.Scanner(a, local, am.SCAN_LIST | am.SCAN_COUNTS)
-    sc_e2e.set_mode(mode_req)
-    h_counts = np.empty(P, dtype=np.uint64)
-    sc_e2e.run_host_ptr(h_text.data_ptr(), sh.window)
-    sc_e2e.sync()
+    # e2e: the public pipelined host scan (acg_scan_pipelined) from pinned host
+    # memory: each step copies the shard's text H2D in pieces and reads the packed
+    # records and per-pattern counts back into pinned host memory (piece k+1's
+    # H2D and scan overlap piece k's D2H)
+    h_out = torch.empty(max(m_local + 1024, 1), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+    text_np = h_text.numpy()[: sh.window]
+    e2e_kw = dict(device=local, piece_bytes=args.e2e_piece_mib << 20, out=h_out, emit_from=sh.lo - sh.start,
+                  base_offset=sh.start)
+    am.scan_pipelined(a, text_np, **e2e_kw)  # warm-up (workspaces, adaptive sizes)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     d2h = 0
     for _ in range(args.e2e_steps):
-        sc_e2e.run_host_ptr(h_text.data_ptr(), sh.window)
-        packed, _bits = sc_e2e.packed_records()
-        h_counts[:] = sc_e2e.pattern_counts()
-        d2h = packed.nbytes + h_counts.nbytes
+        recs, _bits, h_counts, m_e2e, _ = am.scan_pipelined(a, text_np, **e2e_kw)
+        pieces = max(1, -(-owned // (args.e2e_piece_mib << 20)))
+        d2h = recs.nbytes + pieces * h_counts.nbytes
+    assert m_e2e == m_local, (m_e2e, m_local)
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
@@ -496,6 +504,8 @@ def main() -> None:
                      "host_enqueue_ms_per_step": round(host_ms, 4)},
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(sh.window),
                 "d2h_bytes_per_step": int(d2h)},
+        "build": {"ms": round(build_ms, 2), "host_threads": os.cpu_count(),
+                  "what": "acg_build: trie + failure links + dense DFA + filter tables (SURVEY 8(f) rank 1)"},
         "gpu_launches": int(geo["launches"]) * args.steps,
         "clocks": clk.summary(),
         "check": {"matches": m_job, "digest_sum": dsum_job, "digest_xor": dxor_job,
@@ -512,6 +522,10 @@ def main() -> None:
         single = cpu_reference_single(w, concat, offs, min(args.cpu_sample_mib, 16) << 20)
         if single:
             line["cpu_baseline"]["single_thread"] = {k: single[k] for k in ("value", "unit", "cores", "sample")}
+        import oracle
+        tr0 = time.perf_counter()
+        oracle.RefAutomaton(concat, offs)
+        line["build"]["reference_ms"] = round((time.perf_counter() - tr0) * 1e3, 2)  # acmatch::build, 1 thread
         if args.config == 0 and (os.cpu_count() or 1) != 16:  # BASELINE configs[0]: 1 and 16 threads
             c16 = cpu_reference(w, concat, offs, args.cpu_sample_mib << 20, 16, 1, 0)
             line["cpu_baseline"]["threads_16"] = {k: c16[k] for k in ("value", "unit", "cores", "sample")}

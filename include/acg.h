@@ -33,7 +33,8 @@ enum {
     ACG_ERR_INVALID_WORKER_COUNT = 4, /* acmatch::InvalidWorkerCountError (errors.hpp:27-30) */
     ACG_ERR_CUDA = 5,                 /* new: CUDA failure (acmatch::DeviceError) */
     ACG_ERR_OUT_OF_MEMORY = 6,        /* new: device allocation failure */
-    ACG_ERR_NO_DEVICE = 7             /* new: no usable sm_100 device */
+    ACG_ERR_NO_DEVICE = 7,            /* new: no usable sm_100 device */
+    ACG_ERR_IO = 9                    /* acmatch::IoError (errors.hpp; io.hpp:27-29, 71-76) */
 };
 
 /* scan flags */
@@ -110,8 +111,9 @@ int acg_scanner_create(const acg_automaton* a, int device, uint32_t flags, acg_s
 void acg_scanner_destroy(acg_scanner* s);
 int acg_scanner_run(acg_scanner* s, const uint8_t* d_text, uint64_t n, uint64_t emit_from, uint64_t base_offset,
                     void* stream);
-/* End-to-end: copy host text (pinned for full speed) to the device and scan it,
- * overlapping the copy with the scan piecewise. */
+/* End-to-end: copy host text (pinned for full speed) into the scanner's
+ * device buffer, then scan it (one copy, then the run, both on `stream`; for
+ * copy/scan overlap on large inputs see acg_scan_pipelined). */
 int acg_scanner_run_host(acg_scanner* s, const uint8_t* h_text, uint64_t n, void* stream);
 /* Waits for the last run; grows the record buffer and re-emits if it overflowed. */
 int acg_scanner_sync(acg_scanner* s);
@@ -172,6 +174,36 @@ int acg_automaton_filter_info(const acg_automaton* a, uint32_t* q, double* pass_
 /* Device layout of the automaton (diagnostics): states, hot rows in smem, columns. */
 int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* hot_rows, uint32_t* columns,
                          uint32_t* halo, int* alphabet_mode);
+
+/* ---- input path: replaces acmatch::load_input / load_patterns
+ * (proj/include/acmatch/io.hpp:25-31, :37-65) --------------------------------
+ * acg_load_input: the whole file as raw bytes in page-locked host memory
+ * (parallel reads; pageable if pinning fails), *n bytes; free with
+ * acg_host_free. Errors: ACG_ERR_IO ("cannot open <path>", "read failed"). */
+int acg_load_input(const char* path, uint8_t** data, uint64_t* n);
+/* acg_load_patterns: one pattern per line — LF split, one trailing CR
+ * stripped, empty lines skipped (*skipped_empty), repeated lines dropped
+ * keeping the first (*duplicates), dense ids in load order; the dictionary as
+ * acg_build takes it (*concat, *offsets[*count+1]; free both with
+ * acg_host_free). ACG_ERR_EMPTY_DICTIONARY when no line is left (io.hpp:62-63). */
+int acg_load_patterns(const char* path, uint8_t** concat, uint64_t** offsets, uint32_t* count, uint64_t* duplicates,
+                      uint64_t* skipped_empty);
+void acg_host_free(void* p);
+
+/* ---- pipelined host scan: acmatch::scan (aho_corasick.hpp:250-277) of a
+ * host text of any size, with the PCIe copies overlapped: the text is cut into
+ * pieces of piece_bytes (0 = 256 MiB) scanned as windows with maxlen-1 bytes
+ * of context on two scanners / two streams, so piece k+1's H2D copy and scan
+ * run while piece k's records come back. Outputs: *m_out matches; the first
+ * min(m, cap) packed records (end << *id_bits | id, canonical order) into
+ * h_packed (NULL: counts only); per-pattern counts into h_counts (NULL: none);
+ * ScanStats::failure_follows with ACG_SCAN_STATS in flags. Windows as
+ * acg_scanner_run: bytes [0, emit_from) are context only (a multiple of 16,
+ * >= the halo for shard exactness), ends are base_offset + position. Host
+ * buffers are best page-locked (acg_load_input); pageable text is staged. */
+int acg_scan_pipelined(const acg_automaton* a, int device, const uint8_t* h_text, uint64_t n, uint64_t emit_from,
+                       uint64_t base_offset, uint64_t piece_bytes, uint32_t flags, uint64_t* h_packed, uint64_t cap,
+                       uint64_t* h_counts, uint64_t* m_out, uint32_t* id_bits, uint64_t* failure_follows);
 
 /* Tuning knobs (diagnostics / benchmarks): streams per thread U in {1,2,4,8}
  * and threads per block; 0 = default. */

@@ -60,6 +60,7 @@ namespace detail {
         case ACG_ERR_CUDA:
         case ACG_ERR_OUT_OF_MEMORY:
         case ACG_ERR_NO_DEVICE: throw DeviceError(msg);
+        case ACG_ERR_IO: throw IoError(msg);
         default: throw Error(msg);
     }
 }

@@ -24,7 +24,7 @@ ACMATCH_DERIVED_ERROR(EmptyDictionaryError);     // ACG_ERR_EMPTY_DICTIONARY
 ACMATCH_DERIVED_ERROR(InvalidWorkerCountError);  // ACG_ERR_INVALID_WORKER_COUNT
 ACMATCH_DERIVED_ERROR(ZeroTimeError);            // reference bench API (out of scope here)
 ACMATCH_DERIVED_ERROR(InfeasiblePlantError);     // reference corpus API (out of scope here)
-ACMATCH_DERIVED_ERROR(IoError);                  // reference io API (out of scope here)
+ACMATCH_DERIVED_ERROR(IoError);                  // ACG_ERR_IO (io.hpp drop-in: acg_load_input / acg_load_patterns)
 ACMATCH_DERIVED_ERROR(DeviceError);              // ACG_ERR_CUDA / _OUT_OF_MEMORY / _NO_DEVICE
 
 #undef ACMATCH_DERIVED_ERROR

@@ -73,6 +73,8 @@ _REF_SYMS = {
     "ref_naive_find_all": (u64, [vp, vp, u32, vp, u64, vp, vp, u64]),
     "ref_hardware_concurrency": (C.c_uint, []),
     "ref_export": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ref_load_patterns": (C.c_int, [C.c_char_p, vp, vp, vp]),
+    "ref_load_input": (C.c_int, [C.c_char_p, C.POINTER(u64), vp]),
 }
 
 _libs: dict = {}
@@ -334,3 +336,27 @@ def ref_random_trial(seed: int, max_count: int = 50, min_len: int = 1, max_len: 
                                C.byref(tl))
     b = concat.tobytes()
     return [b[int(offs[i]):int(offs[i + 1])] for i in range(n)], text[: tl.value].tobytes()
+
+
+def ref_load_patterns(path: str):
+    """The reference's acmatch::load_patterns: (rc, words, duplicates, skipped_empty)."""
+    sizes = np.zeros(4, np.uint64)
+    rc = ref().ref_load_patterns(os.fsencode(path), _ptr(sizes), None, None)
+    if rc:
+        return rc, None, 0, 0
+    concat = np.zeros(max(int(sizes[1]), 1), np.uint8)
+    offs = np.zeros(int(sizes[0]) + 1, np.uint64)
+    ref().ref_load_patterns(os.fsencode(path), _ptr(sizes), _ptr(concat), _ptr(offs))
+    b = concat.tobytes()
+    return 0, [b[int(offs[i]):int(offs[i + 1])] for i in range(int(sizes[0]))], int(sizes[2]), int(sizes[3])
+
+
+def ref_load_input(path: str):
+    """The reference's acmatch::load_input: (rc, bytes)."""
+    n = u64()
+    rc = ref().ref_load_input(os.fsencode(path), C.byref(n), None)
+    if rc:
+        return rc, None
+    out = np.zeros(max(n.value, 1), np.uint8)
+    ref().ref_load_input(os.fsencode(path), C.byref(n), _ptr(out))
+    return 0, out[:n.value].tobytes()

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "acmatch/aho_corasick.hpp"
+#include "acmatch/io.hpp"
 #include "acmatch/partition.hpp"
 #include "support/oracle.hpp"
 
@@ -123,6 +124,48 @@ void ref_export(void* h, std::uint64_t* sizes, std::uint32_t* fail, std::uint32_
     }
     edge_off[S] = e;
     out_off[S] = o;
+}
+
+// acmatch::load_patterns (include/acmatch/io.hpp:37-65): 0 ok (sizes first with
+// null outputs), 9 IoError, 1 EmptyDictionaryError.
+int ref_load_patterns(const char* path, std::uint64_t* sizes, std::uint8_t* concat, std::uint64_t* offs) {
+    try {
+        const acmatch::PatternFile f = acmatch::load_patterns(path);
+        std::uint64_t total = 0;
+        for (const auto& p : f.patterns) total += p.bytes.size();
+        sizes[0] = f.patterns.size();
+        sizes[1] = total;
+        sizes[2] = f.duplicates;
+        sizes[3] = f.skipped_empty;
+        if (concat) {
+            std::uint64_t o = 0;
+            offs[0] = 0;
+            for (std::size_t i = 0; i < f.patterns.size(); ++i) {
+                std::memcpy(concat + o, f.patterns[i].bytes.data(), f.patterns[i].bytes.size());
+                o += f.patterns[i].bytes.size();
+                offs[i + 1] = o;
+            }
+        }
+        return 0;
+    } catch (const acmatch::IoError&) {
+        return 9;
+    } catch (const std::exception& e) {
+        return error_code(e);
+    }
+}
+
+// acmatch::load_input (include/acmatch/io.hpp:25-31): bytes copied when out is non-null.
+int ref_load_input(const char* path, std::uint64_t* n, std::uint8_t* out) {
+    try {
+        const std::string s = acmatch::load_input(path);
+        *n = s.size();
+        if (out) std::memcpy(out, s.data(), s.size());
+        return 0;
+    } catch (const acmatch::IoError&) {
+        return 9;
+    } catch (const std::exception& e) {
+        return error_code(e);
+    }
 }
 
 // acmatch::scan (include/acmatch/aho_corasick.hpp:250-272) over text[0, n).

@@ -11,6 +11,7 @@ used by the benchmark and the shard runner.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import NamedTuple, Optional, Sequence
 
@@ -43,8 +44,12 @@ class DeviceError(Error):
     """New in this build: CUDA failure or no usable device."""
 
 
+class IoError(Error):
+    """acmatch::IoError (reference errors.hpp; raised by the io.hpp loaders)."""
+
+
 _ERRORS = {1: EmptyDictionaryError, 2: EmptyPatternError, 3: Error, 4: InvalidWorkerCountError,
-           5: DeviceError, 6: DeviceError, 7: DeviceError}
+           5: DeviceError, 6: DeviceError, 7: DeviceError, 9: IoError}
 
 
 def _check(rc: int) -> None:
@@ -396,3 +401,74 @@ class Scanner:
         nc, cb, la = C.c_uint64(), C.c_uint64(), C.c_uint32()
         _check(_lib.acg().acg_scanner_last_geometry(self._h, C.byref(nc), C.byref(cb), C.byref(la)))
         return {"n_chunks": nc.value, "chunk_bytes": cb.value, "launches": la.value}
+
+
+# ---- input path (reference io.hpp:25-65) and the pipelined host scan ----------
+
+class PinnedInput:
+    """acmatch::load_input (io.hpp:25-31): the file's raw bytes, here in
+    page-locked host memory (acg_load_input). `.array` is a uint8 view."""
+
+    def __init__(self, path: str):
+        ptr, n = C.c_void_p(), C.c_uint64()
+        _check(_lib.acg().acg_load_input(os.fsencode(path), C.byref(ptr), C.byref(n)))
+        self._ptr, self.n = ptr, n.value
+        self.array = (np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(self.n,)) if self.n
+                      else np.zeros(0, np.uint8))
+
+    def __del__(self):
+        if getattr(self, "_ptr", None) and self._ptr.value and _lib is not None:
+            _lib.acg().acg_host_free(self._ptr)
+            self._ptr = C.c_void_p()
+
+
+def load_input(path: str) -> PinnedInput:
+    return PinnedInput(path)
+
+
+class PatternFile(NamedTuple):
+    """acmatch::PatternFile (io.hpp:17-22)."""
+    patterns: list
+    duplicates: int
+    skipped_empty: int
+
+
+def load_patterns(path: str) -> PatternFile:
+    """acmatch::load_patterns (io.hpp:37-65) through acg_load_patterns."""
+    cp, op, cnt = C.c_void_p(), C.c_void_p(), C.c_uint32()
+    dups, empty = C.c_uint64(), C.c_uint64()
+    _check(_lib.acg().acg_load_patterns(os.fsencode(path), C.byref(cp), C.byref(op), C.byref(cnt), C.byref(dups),
+                                        C.byref(empty)))
+    try:
+        P = cnt.value
+        offs = np.ctypeslib.as_array(C.cast(op, C.POINTER(C.c_uint64)), shape=(P + 1,)).copy()
+        total = int(offs[-1])
+        data = C.string_at(cp, total) if total else b""
+    finally:
+        _lib.acg().acg_host_free(cp)
+        _lib.acg().acg_host_free(op)
+    pats = [Pattern(i, data[int(offs[i]):int(offs[i + 1])]) for i in range(P)]
+    return PatternFile(pats, dups.value, empty.value)
+
+
+def scan_pipelined(a: Automaton, text, device: int = 0, piece_bytes: int = 0, list_cap: int | None = None,
+                   counts: bool = True, stats: bool = False, out: np.ndarray | None = None,
+                   emit_from: int = 0, base_offset: int = 0):
+    """acg_scan_pipelined: (packed records uint64[m] or None, id_bits, counts or
+    None, m, failure follows). `text` is a uint8 array (page-locked for full
+    speed: PinnedInput.array or a pinned torch tensor's numpy view) or a
+    PinnedInput; `out` an optional (pinned) uint64 buffer for the records."""
+    arr = text.array if isinstance(text, PinnedInput) else _as_u8(text)
+    P = a.pattern_count()
+    if out is None and list_cap is not None:
+        out = np.empty(max(list_cap, 1), np.uint64)
+    cnt = np.zeros(P, np.uint64) if counts else None
+    m, ib, fol = C.c_uint64(), C.c_uint32(), C.c_uint64()
+    cap = 0 if out is None else (out.size if list_cap is None else min(list_cap, out.size))
+    _check(_lib.acg().acg_scan_pipelined(a.handle, device, arr.ctypes.data_as(C.c_void_p) if arr.size else None,
+                                         arr.size, emit_from, base_offset, piece_bytes, SCAN_STATS if stats else 0,
+                                         out.ctypes.data_as(C.c_void_p) if out is not None else None, cap,
+                                         cnt.ctypes.data_as(C.c_void_p) if cnt is not None else None,
+                                         C.byref(m), C.byref(ib), C.byref(fol)))
+    recs = None if out is None else out[:min(m.value, cap)]
+    return recs, ib.value, cnt, m.value, fol.value

@@ -228,8 +228,6 @@ struct acg_scanner {
     std::uint32_t flags = 0;
     std::shared_ptr<DeviceDfa> dd;
     cudaStream_t stream = nullptr;       // own compute stream
-    cudaStream_t copy_stream = nullptr;  // H2D for run_host
-    std::vector<cudaEvent_t> piece_events;
     cudaStream_t last = nullptr;
     // workspace
     DevBuf<std::uint32_t> active_list, scalars32;
@@ -534,6 +532,7 @@ constexpr unsigned long long kSparseMaxWalk = 1ull << 17;
 constexpr unsigned long long kSparseMinChunk = 256 + 64;
 constexpr double kSparseMaxEventRate = 0.005;
 constexpr std::uint32_t kHistMaxPatterns = 56 * 1024;  // record histogram: u32 bins in shared memory  // AUTO: sparse mode below this event rate
+constexpr unsigned long long kEventBoundBudget = 16ull << 30;  // first-run event slabs at the 1-per-byte bound
 constexpr unsigned long long kScratchBudget = 64ull << 30;  // exact-mode single-pass slabs (bytes)
 
 // Slab budget: at most kScratchBudget and 60 % of the device memory free now
@@ -834,7 +833,14 @@ cudaError_t plan_events(acg_scanner* s, std::uint32_t n_out, cudaStream_t st) {
     } else {
         const double dens = known ? static_cast<double>(s->xev_total) / static_cast<double>(s->xev_n) : 1.0 / 16;
         unsigned long long cap = static_cast<unsigned long long>(1.25 * dens * static_cast<double>(s->chunk)) + 17;
-        if (!known) cap = s->chunk / 16 + 33;
+        // a chunk logs at most one event per owned byte (one state per step, owned
+        // blocks only): slabs of chunk + 1 slots never overflow. Without a density
+        // from an earlier run, take that bound when it fits the budget (a first
+        // run on dense output would otherwise chain thousands of pool blocks per
+        // chunk through one global counter)
+        if (!known) cap = (static_cast<double>(nc) * (s->chunk + 1) * 4.0 <= static_cast<double>(kEventBoundBudget))
+                              ? s->chunk + 1
+                              : s->chunk / 16 + 33;
         cap = std::min<unsigned long long>(cap, 0xFFFFFFFull);
         e.ecap = static_cast<std::uint32_t>(cap);
         prim = cap * nc;
@@ -899,8 +905,13 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if (mode == ACG_MODE_AUTO)
         // measured on the BASELINE configs: sparse wins at 8.5e-4 events per walked
         // byte (cfg0: 3x faster than exact) and loses badly at 0.025 (cfg4) and
-        // 0.0625 (cfg2: fix-up replay dominates)
-        mode = (s->last_event_rate < 0 || s->last_event_rate < kSparseMaxEventRate) ? ACG_MODE_SPARSE : ACG_MODE_EXACT;
+        // 0.0625 (cfg2: fix-up replay dominates). Without a measured rate, sparse
+        // only when every state is hot (no excursions at all: cfg0); a first run of
+        // sparse on a dense-output automaton (cfg4) is 19x slower than exact
+        mode = ((s->last_event_rate < 0 && d.S <= d.H) ||
+                (s->last_event_rate >= 0 && s->last_event_rate < kSparseMaxEventRate))
+                   ? ACG_MODE_SPARSE
+                   : ACG_MODE_EXACT;
     s->mode_run = mode;
     if (mode != ACG_MODE_EXACT) s->exact_chunks = 0;  // chunk_counts no longer hold an exact run's counts
     // default interleave: sparse 1; exact 4 on DNA, 2 on generic alphabets (cfg3
@@ -1404,7 +1415,6 @@ int make_scanner(const acg_automaton* a, int device, std::uint32_t flags, acg_sc
     if (const int rc = get_device_dfa(a, device, &s->dd)) return rc;
     ACG_CUDA(cudaSetDevice(device));
     ACG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    ACG_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     s->pinned = pinned_take();
     if (!s->pinned) return fail(ACG_ERR_OUT_OF_MEMORY, "pinned host allocation failed");
     ACG_CUDA(cudaEventCreateWithFlags(&s->order_ev, cudaEventDisableTiming));
@@ -1424,7 +1434,6 @@ void free_scanner(acg_scanner* s) {
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->last) cudaStreamSynchronize(s->last);
     if (s->stream) cudaStreamDestroy(s->stream);
-    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     if (s->pinned) pinned_give(s->pinned);
     if (s->order_ev) cudaEventDestroy(s->order_ev);
     for (auto& e : s->ev)
@@ -1533,6 +1542,22 @@ EagerDriverInit g_eager_driver_init;
 }  // namespace
 
 extern "C" {
+
+// Pooled scanners for the pipelined host scan (host_io.cpp); not part of include/acg.h.
+__attribute__((visibility("hidden"))) int acg_internal_scanner_take(const acg_automaton* a, int device,
+                                                                    std::uint32_t flags, acg_scanner** out) {
+    acg_scanner* s = pool_take(a, device, flags);
+    if (!s) {
+        if (const int rc = make_scanner(a, device, flags, &s)) return rc;
+    }
+    *out = s;
+    return ACG_OK;
+}
+__attribute__((visibility("hidden"))) void acg_internal_scanner_give(acg_scanner* s) { pool_give(s); }
+__attribute__((visibility("hidden"))) void* acg_internal_scanner_stream(acg_scanner* s) { return s->stream; }
+
+// (host_io.cpp reports its errors through this; not part of include/acg.h)
+__attribute__((visibility("hidden"))) int acg_internal_set_error(int code, const char* msg) { return fail(code, msg); }
 
 const char* acg_last_error(void) { return g_last_error.c_str(); }
 const char* acg_version(void) { return "acg 0.1 (sm_100a)"; }

@@ -31,7 +31,7 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-HOST_SOURCES = ("automaton.cpp", "parallel.cpp")  # host C++ of libacg.so
+HOST_SOURCES = ("automaton.cpp", "parallel.cpp", "host_io.cpp")  # host C++ of libacg.so
 
 
 def build(force: bool = False, verbose_ptxas: bool = False) -> None:
@@ -53,7 +53,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         src_c = os.path.join(CSRC, name)
         o = os.path.join(obj, name.replace(".cpp", ".o"))
         if force or _stale(o, [src_c] + headers):
-            _run(["g++", "-std=c++17", "-O3", "-fPIC", "-pthread", "-c", "-o", o, src_c] + inc)
+            _run(["g++", "-std=c++17", "-O3", "-fPIC", "-pthread", "-c", "-o", o, src_c] + inc +
+                 ["-I", os.path.join(os.path.dirname(NVCC), "..", "include")])
         host_objs.append(o)
     dev_src = os.path.join(CSRC, "acg_device.cu")
     dev_o = os.path.join(obj, "acg_device.o")
