@@ -175,6 +175,22 @@ int acg_automaton_filter_info(const acg_automaton* a, uint32_t* q, double* pass_
 int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* hot_rows, uint32_t* columns,
                          uint32_t* halo, int* alphabet_mode);
 
+/* ---- output step: replaces cmd_match's output loop (proj/include/acmatch/
+ * cli.hpp:58-76), formatted on the GPU from the device match list ----------
+ * ACG_FORMAT_TSV:  "<end>\t<pattern_id>\t<pattern bytes>\n" per record (:71-74)
+ * ACG_FORMAT_JSON: the nlohmann dump(-1) of [{"end":..,"pattern":"..",
+ *                  "pattern_id":..},...] plus "\n" (:63-69): compact, keys in
+ *                  order, strings escaped, invalid UTF-8 replaced by U+FFFD.
+ * acg_scanner_format: records [first, first+count) of the last run's list
+ * (JSON: "[" before record 0, "]\n" after the last, "," between); *bytes =
+ * the text size; host_out NULL = size query; cap < *bytes = ACG_ERR_INVALID.
+ * acg_scanner_write_matches: the whole list to a file descriptor, formatted
+ * in windows of 2^24 records (*bytes written). */
+enum { ACG_FORMAT_TSV = 0, ACG_FORMAT_JSON = 1 };
+int acg_scanner_format(acg_scanner* s, int format, uint64_t first, uint64_t count, uint8_t* host_out, uint64_t cap,
+                       uint64_t* bytes);
+int acg_scanner_write_matches(acg_scanner* s, int format, int fd, uint64_t* bytes);
+
 /* ---- input path: replaces acmatch::load_input / load_patterns
  * (proj/include/acmatch/io.hpp:25-31, :37-65) --------------------------------
  * acg_load_input: the whole file as raw bytes in page-locked host memory

@@ -75,6 +75,7 @@ _REF_SYMS = {
     "ref_export": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "ref_load_patterns": (C.c_int, [C.c_char_p, vp, vp, vp]),
     "ref_load_input": (C.c_int, [C.c_char_p, C.POINTER(u64), vp]),
+    "ref_match_tsv": (u64, [vp, vp, u64, vp, u64]),
 }
 
 _libs: dict = {}
@@ -285,6 +286,14 @@ class RefAutomaton:
         n = ref().ref_transitions(self._h, s, _ptr(bb), _ptr(tt), 256)
         return list(zip(bb[:n].tolist(), tt[:n].tolist()))
 
+    def match_tsv(self, text) -> bytes:
+        """The reference scan printed as `acmatch match` TSV (cli.hpp:71-74)."""
+        t = _u8(text)
+        n = ref().ref_match_tsv(self._h, _ptr(t), t.size, None, 0)
+        out = np.zeros(max(n, 1), np.uint8)
+        ref().ref_match_tsv(self._h, _ptr(t), t.size, _ptr(out), out.size)
+        return out[:n].tobytes()
+
     def export(self) -> dict:
         """The whole machine through the reference's public accessors, as CSR arrays."""
         sizes = np.zeros(3, np.uint64)
@@ -360,3 +369,46 @@ def ref_load_input(path: str):
     out = np.zeros(max(n.value, 1), np.uint8)
     ref().ref_load_input(os.fsencode(path), C.byref(n), _ptr(out))
     return 0, out[:n.value].tobytes()
+
+
+def json_escape(b: bytes) -> bytes:
+    """Restatement of nlohmann::json's string dump with error_handler replace and
+    ensure_ascii false (the reference's cmd_match JSON, cli.hpp:63-69): JSON
+    escapes for '"', backslash, \\b \\f \\n \\r \\t, \\u00xx for other bytes < 0x20,
+    valid UTF-8 as is, each invalid sequence -> U+FFFD. Parity of the invalid-UTF-8
+    rule is UNPINNED (nlohmann/json is not in this image); valid text is pinned
+    by Python's json module in the tests."""
+    out = bytearray()
+    i, n = 0, len(b)
+    esc = {0x22: b'\\"', 0x5C: b"\\\\", 0x08: b"\\b", 0x0C: b"\\f", 0x0A: b"\\n", 0x0D: b"\\r", 0x09: b"\\t"}
+    while i < n:
+        c = b[i]
+        if c < 0x80:
+            out += esc.get(c, b"\\u%04x" % c if c < 0x20 else bytes([c]))
+            i += 1
+            continue
+        need, lo, hi = 0, 0x80, 0xBF
+        if 0xC2 <= c <= 0xDF: need = 1
+        elif c == 0xE0: need, lo = 2, 0xA0
+        elif 0xE1 <= c <= 0xEC or c in (0xEE, 0xEF): need = 2
+        elif c == 0xED: need, hi = 2, 0x9F
+        elif c == 0xF0: need, lo = 3, 0x90
+        elif 0xF1 <= c <= 0xF3: need = 3
+        elif c == 0xF4: need, hi = 3, 0x8F
+        if need == 0:
+            out += b"\xef\xbf\xbd"
+            i += 1
+            continue
+        k = 1
+        while k <= need and i + k < n:
+            d = b[i + k]
+            if not ((lo <= d <= hi) if k == 1 else (0x80 <= d <= 0xBF)):
+                break
+            k += 1
+        if k == need + 1:
+            out += b[i:i + need + 1]
+            i += need + 1
+        else:
+            out += b"\xef\xbf\xbd"
+            i += k
+    return bytes(out)

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <exception>
 #include <random>
+#include <sstream>
 #include <string>
 #include <string_view>
 #include <thread>
@@ -166,6 +167,19 @@ int ref_load_input(const char* path, std::uint64_t* n, std::uint8_t* out) {
     } catch (const std::exception& e) {
         return error_code(e);
     }
+}
+
+// `acmatch match --output tsv` bytes for text[0, n): the reference scan, then
+// cmd_match's TSV loop restated (proj/include/acmatch/cli.hpp:71-74; cli.hpp
+// itself needs CLI11/nlohmann, absent here). Returns the size; copies when it fits.
+std::uint64_t ref_match_tsv(void* h, const std::uint8_t* text, std::uint64_t n, std::uint8_t* out, std::uint64_t cap) {
+    const Automaton& a = *static_cast<Automaton*>(h);
+    const auto recs = acmatch::scan(a, std::string_view(reinterpret_cast<const char*>(text), n));
+    std::ostringstream os;
+    for (const MatchRecord& r : recs) os << r.end << '\t' << r.pattern_id << '\t' << a.patterns()[r.pattern_id].bytes << '\n';
+    const std::string s = os.str();
+    if (out && s.size() <= cap) std::memcpy(out, s.data(), s.size());
+    return s.size();
 }
 
 // acmatch::scan (include/acmatch/aho_corasick.hpp:250-272) over text[0, n).

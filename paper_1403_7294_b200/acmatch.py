@@ -291,6 +291,9 @@ def match_count(records) -> int:
     return len(records)
 
 
+FORMAT_TSV, FORMAT_JSON = 0, 1
+
+
 class Scanner:
     """Device-resident scanning (acg_scanner_*): reusable workspace for one
     automaton on one device; `run` enqueues on a CUDA stream without host syncs."""
@@ -344,6 +347,30 @@ class Scanner:
         bits = C.c_uint32()
         _check(_lib.acg().acg_scanner_packed_records(self._h, out.ctypes.data_as(C.c_void_p), m, C.byref(bits)))
         return out, bits.value
+
+    def format(self, fmt: str = "tsv", first: int = 0, count: int | None = None) -> bytes:
+        """The match list (records [first, first+count)) as the reference's
+        `acmatch match` output, formatted on the GPU (acg_scanner_format)."""
+        f = {"tsv": FORMAT_TSV, "json": FORMAT_JSON}[fmt]
+        if count is None:
+            count = self.match_count() - first
+        nb = C.c_uint64()
+        _check(_lib.acg().acg_scanner_format(self._h, f, first, count, None, 0, C.byref(nb)))
+        buf = np.empty(max(nb.value, 1), np.uint8)
+        _check(_lib.acg().acg_scanner_format(self._h, f, first, count, buf.ctypes.data_as(C.c_void_p), buf.size,
+                                             C.byref(nb)))
+        return buf[:nb.value].tobytes()
+
+    def write_matches(self, path: str, fmt: str = "tsv") -> int:
+        """The whole match list to a file (acg_scanner_write_matches); bytes written."""
+        f = {"tsv": FORMAT_TSV, "json": FORMAT_JSON}[fmt]
+        nb = C.c_uint64()
+        fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+        try:
+            _check(_lib.acg().acg_scanner_write_matches(self._h, f, fd, C.byref(nb)))
+        finally:
+            os.close(fd)
+        return nb.value
 
     def copy_records(self, first: int, count: int) -> np.ndarray:
         """Packed records [first, first+count) of the list (acg_scanner_copy_records)."""

@@ -27,6 +27,7 @@
 #include "scan_kernels.cuh"
 #include "filter_kernels.cuh"
 #include "exact_kernels.cuh"
+#include "format_kernels.cuh"
 
 namespace {
 
@@ -187,6 +188,10 @@ struct DeviceDfa {
     DevBuf<std::uint32_t> qtab, qb_off, qb_ent, pat_off;  // filter mode: exact q-gram table, patterns
     DevBuf<std::uint8_t> pat_bytes;
     DevBuf<unsigned long long> pat_code;  // filter mode: 2-bit codes of each pattern's first 64 bytes
+    // output step (format_kernels.cuh): per pattern, its raw bytes [0] / JSON-escaped bytes [1]; built on first use
+    std::mutex fmt_mu;
+    DevBuf<std::uint8_t> fmt_str[2];
+    DevBuf<unsigned long long> fmt_off[2];
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
     std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
     int smem_optin = 0;
@@ -235,6 +240,8 @@ struct acg_scanner {
     DevBuf<unsigned long long> chunk_offs, visits, counts, records, scalars64;  // [0]=follows [1..3]=digest
     DevBuf<std::uint8_t> text;
     DevBuf<std::uint8_t> cub_tmp;
+    DevBuf<std::uint8_t> fmt_out;                 // output step: formatted bytes of one window
+    DevBuf<unsigned long long> fmt_tiles;         // per-tile byte sums, then offsets
     unsigned long long* pinned = nullptr;  // 8 host words
     cudaEvent_t order_ev = nullptr;        // orders a run on a new stream after the previous one
     // geometry of the last run
@@ -1539,6 +1546,144 @@ void warm_up_device(int device) {
 
 EagerDriverInit g_eager_driver_init;
 
+// JSON string body of pattern bytes as nlohmann::json::dump(-1, ' ', false,
+// error_handler_t::replace) writes it (the reference's cmd_match,
+// proj/include/acmatch/cli.hpp:63-69): '"' '\\' and \b \f \n \r \t escaped,
+// other bytes < 0x20 as \u00xx (lower-case hex), valid UTF-8 passed through,
+// each invalid UTF-8 sequence replaced by U+FFFD (the byte that broke a
+// sequence is read again as a possible start of the next one).
+void json_escape(const std::uint8_t* b, std::size_t n, std::vector<std::uint8_t>& out) {
+    auto fffd = [&] {
+        out.push_back(0xEF);
+        out.push_back(0xBF);
+        out.push_back(0xBD);
+    };
+    std::size_t i = 0;
+    while (i < n) {
+        const std::uint8_t c = b[i];
+        if (c < 0x80) {
+            switch (c) {
+                case '"': out.push_back('\\'); out.push_back('"'); break;
+                case '\\': out.push_back('\\'); out.push_back('\\'); break;
+                case '\b': out.push_back('\\'); out.push_back('b'); break;
+                case '\f': out.push_back('\\'); out.push_back('f'); break;
+                case '\n': out.push_back('\\'); out.push_back('n'); break;
+                case '\r': out.push_back('\\'); out.push_back('r'); break;
+                case '\t': out.push_back('\\'); out.push_back('t'); break;
+                default:
+                    if (c < 0x20) {
+                        static const char hex[] = "0123456789abcdef";
+                        const std::uint8_t esc[6] = {'\\', 'u', '0', '0', static_cast<std::uint8_t>(hex[c >> 4]),
+                                                     static_cast<std::uint8_t>(hex[c & 15])};
+                        out.insert(out.end(), esc, esc + 6);
+                    } else {
+                        out.push_back(c);
+                    }
+            }
+            ++i;
+            continue;
+        }
+        // UTF-8 sequence: lead byte ranges and the first continuation's range (RFC 3629)
+        std::size_t need = 0;
+        std::uint8_t lo = 0x80, hi = 0xBF;
+        if (c >= 0xC2 && c <= 0xDF) need = 1;
+        else if (c == 0xE0) need = 2, lo = 0xA0;
+        else if ((c >= 0xE1 && c <= 0xEC) || c == 0xEE || c == 0xEF) need = 2;
+        else if (c == 0xED) need = 2, hi = 0x9F;
+        else if (c == 0xF0) need = 3, lo = 0x90;
+        else if (c >= 0xF1 && c <= 0xF3) need = 3;
+        else if (c == 0xF4) need = 3, hi = 0x8F;
+        if (need == 0) {  // not a lead byte
+            fffd();
+            ++i;
+            continue;
+        }
+        std::size_t k = 1;
+        for (; k <= need && i + k < n; ++k) {
+            const std::uint8_t d = b[i + k];
+            const bool ok = k == 1 ? (d >= lo && d <= hi) : (d >= 0x80 && d <= 0xBF);
+            if (!ok) break;
+        }
+        if (k == need + 1) {
+            out.insert(out.end(), b + i, b + i + need + 1);
+            i += need + 1;
+        } else {
+            fffd();  // the valid prefix is dropped; the breaking byte (if any) starts over
+            i += k;
+        }
+    }
+}
+
+cudaError_t format_tables(const acg_automaton* a, DeviceDfa& dd, int json, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(dd.fmt_mu);
+    if (dd.fmt_off[json].p) return cudaSuccess;
+    const acg::Nfa& nfa = a->nfa;
+    std::vector<std::uint8_t> bytes;
+    std::vector<unsigned long long> offs(nfa.n_patterns + 1, 0);
+    for (std::uint32_t p = 0; p < nfa.n_patterns; ++p) {
+        const std::uint8_t* b = nfa.pat_bytes.data() + nfa.pat_off[p];
+        const std::size_t len = nfa.pat_off[p + 1] - nfa.pat_off[p];
+        if (json) json_escape(b, len, bytes);
+        else bytes.insert(bytes.end(), b, b + len);
+        offs[p + 1] = bytes.size();
+    }
+    if (bytes.empty()) bytes.push_back(0);
+    cudaError_t e = upload(dd.fmt_str[json], bytes.data(), bytes.size(), st);
+    if (e == cudaSuccess) e = upload(dd.fmt_off[json], offs.data(), offs.size(), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // (host vectors die here)
+    return e;
+}
+
+// Formats records [first, first + count) of the synced list into s->fmt_out
+// (device); *bytes = their text size.
+int format_window(acg_scanner* s, int json, std::uint64_t first, std::uint64_t count, std::uint64_t* bytes) {
+    using namespace acg::kern;
+    DeviceDfa& dd = *s->dd;
+    cudaStream_t st = s->last;
+    *bytes = 0;
+    if (json && s->m_total == 0) {  // "[]\n"
+        ACG_CUDA(s->fmt_out.reserve(3, st));
+        ACG_CUDA(cudaMemcpyAsync(s->fmt_out.p, "[]\n", 3, cudaMemcpyHostToDevice, st));
+        ACG_CUDA(cudaStreamSynchronize(st));
+        *bytes = 3;
+        return ACG_OK;
+    }
+    if (count == 0) return ACG_OK;
+    ACG_CUDA(format_tables(s->a, dd, json, st));
+    const std::uint64_t tiles = (count + kFmtTile - 1) / kFmtTile;
+    ACG_CUDA(s->fmt_tiles.reserve(2 * tiles + 1, st));
+    FmtArgs f{};
+    f.rec = s->records.p + first;
+    f.m = count;
+    f.id_bits = dd.dfa->id_bits;
+    f.str = dd.fmt_str[json].p;
+    f.str_off = dd.fmt_off[json].p;
+    f.json = json;
+    f.open = first == 0;
+    f.close = first + count == s->m_total;
+    f.tile_sum = s->fmt_tiles.p;
+    f.tile_off = s->fmt_tiles.p + tiles;
+    const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(tiles, 16ull * dd.num_sms));
+    format_len_kernel<<<g, kFmtTile, 0, st>>>(f);
+    ACG_CUDA(cudaGetLastError());
+    ACG_CUDA(cudaMemsetAsync(s->fmt_tiles.p + tiles, 0, sizeof(unsigned long long), st));
+    std::size_t tmp = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp, f.tile_sum, s->fmt_tiles.p + tiles + 1, static_cast<int>(tiles), st);
+    ACG_CUDA(s->cub_tmp.reserve(std::max(tmp, s->cub_tmp.n), st));
+    tmp = s->cub_tmp.n;
+    ACG_CUDA(cub::DeviceScan::InclusiveSum(s->cub_tmp.p, tmp, f.tile_sum, s->fmt_tiles.p + tiles + 1,
+                                           static_cast<int>(tiles), st));
+    unsigned long long total = 0;
+    ACG_CUDA(cudaMemcpyAsync(&total, s->fmt_tiles.p + 2 * tiles, sizeof total, cudaMemcpyDeviceToHost, st));
+    ACG_CUDA(cudaStreamSynchronize(st));
+    ACG_CUDA(s->fmt_out.reserve(std::max<std::uint64_t>(total, 1), st));
+    f.out = s->fmt_out.p;
+    format_write_kernel<<<g, kFmtTile, 0, st>>>(f);
+    ACG_CUDA(cudaGetLastError());
+    *bytes = total;
+    return ACG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1781,6 +1926,72 @@ int acg_scanner_copy_records(acg_scanner* s, std::uint64_t first, std::uint64_t 
         ACG_CUDA(cudaStreamSynchronize(s->last));
     }
     return ACG_OK;
+}
+
+int acg_scanner_format(acg_scanner* s, int format, std::uint64_t first, std::uint64_t count, std::uint8_t* host_out,
+                       std::uint64_t cap, std::uint64_t* bytes) {
+    if (!s || !bytes) return fail(ACG_ERR_INVALID, "null argument");
+    if (format != ACG_FORMAT_TSV && format != ACG_FORMAT_JSON) return fail(ACG_ERR_INVALID, "unknown output format");
+    if (!(s->flags & ACG_SCAN_LIST)) return fail(ACG_ERR_INVALID, "scanner was created without ACG_SCAN_LIST");
+    if (const int rc = scanner_sync(s)) return rc;
+    if (first > s->m_total || count > s->m_total - first) return fail(ACG_ERR_INVALID, "record range beyond the match list");
+    ACG_CUDA(cudaSetDevice(s->device));
+    if (const int rc = format_window(s, format == ACG_FORMAT_JSON, first, count, bytes)) return rc;
+    if (!host_out) return ACG_OK;
+    if (cap < *bytes) return fail(ACG_ERR_INVALID, "output buffer smaller than the formatted text");
+    if (*bytes) {
+        ACG_CUDA(cudaMemcpyAsync(host_out, s->fmt_out.p, *bytes, cudaMemcpyDeviceToHost, s->last));
+        ACG_CUDA(cudaStreamSynchronize(s->last));
+    }
+    return ACG_OK;
+}
+
+int acg_scanner_write_matches(acg_scanner* s, int format, int fd, std::uint64_t* bytes) {
+    if (!s) return fail(ACG_ERR_INVALID, "null scanner");
+    if (bytes) *bytes = 0;
+    if (const int rc = scanner_sync(s)) return rc;
+    constexpr std::uint64_t kWindow = 1ull << 24;  // records per formatted window
+    std::uint64_t total = 0;
+    unsigned char* stage = nullptr;
+    std::uint64_t stage_n = 0;
+    int rc = ACG_OK;
+    const std::uint64_t m = s->m_total;
+    const std::uint64_t windows = m ? (m + kWindow - 1) / kWindow : 1;
+    for (std::uint64_t w = 0; w < windows && !rc; ++w) {
+        const std::uint64_t first = w * kWindow, count = std::min(kWindow, m - std::min(m, first));
+        std::uint64_t nb = 0;
+        if ((rc = acg_scanner_format(s, format, first, count, nullptr, 0, &nb))) break;
+        if (nb > stage_n) {
+            if (stage) cudaFreeHost(stage);
+            stage_n = nb + nb / 8;
+            if (cudaHostAlloc(reinterpret_cast<void**>(&stage), stage_n, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                stage = nullptr;
+                rc = fail(ACG_ERR_OUT_OF_MEMORY, "pinned staging allocation failed");
+                break;
+            }
+        }
+        if (nb) {
+            if (cudaMemcpyAsync(stage, s->fmt_out.p, nb, cudaMemcpyDeviceToHost, s->last) != cudaSuccess ||
+                cudaStreamSynchronize(s->last) != cudaSuccess) {
+                rc = fail(ACG_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+                break;
+            }
+        }
+        for (std::uint64_t off = 0; off < nb;) {
+            const ssize_t k = ::write(fd, stage + off, nb - off);
+            if (k < 0 && errno == EINTR) continue;
+            if (k <= 0) {
+                rc = fail(ACG_ERR_IO, "write failed");
+                break;
+            }
+            off += static_cast<std::uint64_t>(k);
+        }
+        total += nb;
+    }
+    if (stage) cudaFreeHost(stage);
+    if (!rc && bytes) *bytes = total;
+    return rc;
 }
 
 int acg_scanner_records(acg_scanner* s, std::uint32_t* ids, std::uint64_t* ends, std::uint64_t cap) {
