@@ -175,6 +175,28 @@ int acg_automaton_filter_info(const acg_automaton* a, uint32_t* q, double* pass_
 int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* hot_rows, uint32_t* columns,
                          uint32_t* halo, int* alphabet_mode);
 
+/* ---- the paper's dictionary-partitioned run, GPU-native: replaces
+ * acmatch::run_partitioned + split_patterns + merge_matches
+ * (proj/include/acmatch/partition.hpp:29-170). Same split (contiguous chunks,
+ * sizes differ by at most one), one worker per non-empty chunk (machines built
+ * concurrently on host threads), the input copied to the device once and
+ * scanned by every worker on its own stream, the workers' lists merged ON THE
+ * DEVICE (global ids, merge-path rounds) and read back once. Errors:
+ * ACG_ERR_INVALID_WORKER_COUNT (worker_count < 1), ACG_ERR_EMPTY_DICTIONARY,
+ * else the lowest failing chunk's error. Timings: per launched worker the
+ * host build and scan seconds (the reference's fields) and the scan's device
+ * time; the whole call's wall time; device times of the H2D copy and merge. */
+typedef struct acg_partitioned acg_partitioned;
+int acg_run_partitioned(const uint8_t* concat, const uint64_t* offsets, uint32_t n_patterns, const uint8_t* text,
+                        uint64_t n, uint32_t worker_count, int device, acg_partitioned** out);
+uint64_t acg_partitioned_match_count(const acg_partitioned* r);
+const uint32_t* acg_partitioned_ids(const acg_partitioned* r);
+const uint64_t* acg_partitioned_ends(const acg_partitioned* r);
+int acg_partitioned_timings(const acg_partitioned* r, uint32_t* worker_count, uint32_t* workers_launched,
+                            const double** build_s, const double** scan_s, const double** gpu_scan_ms, double* total_s,
+                            double* h2d_ms, double* merge_ms, double* d2h_ms);
+void acg_partitioned_destroy(acg_partitioned* r);
+
 /* ---- output step: replaces cmd_match's output loop (proj/include/acmatch/
  * cli.hpp:58-76), formatted on the GPU from the device match list ----------
  * ACG_FORMAT_TSV:  "<end>\t<pattern_id>\t<pattern bytes>\n" per record (:71-74)

@@ -1,16 +1,17 @@
 // Drop-in for the reference's dictionary-partitioned run
 // (/root/reference/proj/include/acmatch/partition.hpp:29-170): same types,
-// split rule, error behaviour and timing fields. Each worker thread builds
-// the machine for its contiguous chunk of the dictionary and scans the whole
-// input on the GPU (workers' scans run concurrently, one scanner each); the
-// per-worker lists are merged into global (end, pattern_id) order.
+// split rule, error behaviour and timing fields (plus device-timed ones).
+// run_partitioned is the library's acg_run_partitioned: each worker builds the
+// machine for its contiguous chunk of the dictionary on a host thread and
+// scans the one device copy of the input; the lists are merged on the device.
+// merge_matches (the host merge of given lists) keeps the reference's API.
 #pragma once
 
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <functional>
-#include <future>
+#include <memory>
 #include <string_view>
 #include <thread>
 #include <vector>
@@ -79,64 +80,54 @@ struct PartitionedRun {
     double total_wall_s = 0.0;               // split + builds + scans + merge
     unsigned worker_count = 1;               // as requested
     unsigned workers_launched = 0;           // non-empty chunks
+    // new: device-timed columns (CUDA events)
+    std::vector<double> per_worker_gpu_scan_s;  // each worker's scan on the device
+    double h2d_gpu_s = 0.0;                      // the input's one copy to the device
+    double merge_gpu_s = 0.0;                    // the device-side merge of the workers' lists
+    double d2h_s = 0.0;                          // the merged list's read-back
 };
 
-namespace detail {
-
-struct WorkerOutcome {
-    std::vector<MatchRecord> found;  // global ids, (end, pattern_id) order
-    double build_s = 0, scan_s = 0;
-};
-
-// One worker: build the chunk's machine (local ids 0..k-1), scan the whole
-// input on the GPU, map local ids back to global (the map ascends, so the
-// order is kept).
-inline WorkerOutcome partition_worker(const std::vector<Pattern>& patterns, const std::vector<std::uint32_t>& ids,
-                                      std::string_view input) {
-    using clock = std::chrono::steady_clock;
-    const auto b0 = clock::now();
-    std::vector<Pattern> local;
-    local.reserve(ids.size());
-    for (const std::uint32_t g : ids) local.push_back(Pattern{static_cast<std::uint32_t>(local.size()), patterns[g].bytes});
-    const Automaton machine = build(std::move(local));
-    const auto s0 = clock::now();
-    WorkerOutcome out;
-    out.found = scan(machine, input);
-    const auto s1 = clock::now();
-    for (MatchRecord& r : out.found) r.pattern_id = ids[r.pattern_id];
-    out.build_s = std::chrono::duration<double>(s0 - b0).count();
-    out.scan_s = std::chrono::duration<double>(s1 - s0).count();
-    return out;
-}
-
-}  // namespace detail
-
-// The paper's scheme (:101-170): one worker per non-empty dictionary chunk,
-// all started at once; a failure in any worker fails the run (the lowest
-// chunk's error is rethrown, after every worker has finished).
+// The paper's scheme (:101-170), GPU-native (acg_run_partitioned): one worker
+// per non-empty chunk, machines built concurrently on host threads, the input
+// copied to the device once and scanned by every worker on its own stream,
+// the lists merged on the device; a failure in any worker fails the run (the
+// lowest chunk's error is rethrown).
 inline PartitionedRun run_partitioned(const std::vector<Pattern>& patterns, std::string_view input,
                                       unsigned worker_count) {
-    const auto t0 = std::chrono::steady_clock::now();
-    const PartitionPlan plan = split_patterns(patterns, worker_count);
-    std::vector<std::future<detail::WorkerOutcome>> pending;
-    for (const auto& chunk : plan.chunks)
-        if (!chunk.empty())
-            pending.push_back(std::async(std::launch::async, detail::partition_worker, std::cref(patterns),
-                                         std::cref(chunk), input));
-    for (auto& f : pending) f.wait();
-
-    PartitionedRun run;
-    run.worker_count = worker_count;
-    run.workers_launched = static_cast<unsigned>(pending.size());
-    std::vector<std::vector<MatchRecord>> lists;
-    for (auto& f : pending) {
-        detail::WorkerOutcome w = f.get();  // rethrows that worker's error
-        run.per_worker_build_s.push_back(w.build_s);
-        run.per_worker_scan_s.push_back(w.scan_s);
-        lists.push_back(std::move(w.found));
+    if (worker_count < 1) throw InvalidWorkerCountError("worker count must be >= 1");
+    if (patterns.empty()) throw EmptyDictionaryError("dictionary is empty");
+    std::vector<std::uint8_t> concat;
+    std::vector<std::uint64_t> offs{0};
+    for (std::size_t i = 0; i < patterns.size(); ++i) {  // global ids = positions (the split ignores .id)
+        concat.insert(concat.end(), patterns[i].bytes.begin(), patterns[i].bytes.end());
+        offs.push_back(concat.size());
     }
-    run.matches = merge_matches(lists);
-    run.total_wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    acg_partitioned* r = nullptr;
+    int device = 0;
+    detail::check(acg_run_partitioned(concat.data(), offs.data(), static_cast<std::uint32_t>(patterns.size()),
+                                      reinterpret_cast<const std::uint8_t*>(input.data()), input.size(), worker_count,
+                                      device, &r));
+    std::unique_ptr<acg_partitioned, void (*)(acg_partitioned*)> guard(r, acg_partitioned_destroy);
+    PartitionedRun run;
+    const std::uint64_t m = acg_partitioned_match_count(r);
+    const std::uint32_t* ids = acg_partitioned_ids(r);
+    const std::uint64_t* ends = acg_partitioned_ends(r);
+    run.matches.resize(m);
+    for (std::uint64_t i = 0; i < m; ++i) run.matches[i] = MatchRecord{ids[i], static_cast<std::size_t>(ends[i])};
+    std::uint32_t wc = 0, launched = 0;
+    const double *build_s = nullptr, *scan_s = nullptr, *gpu_ms = nullptr;
+    double total_s = 0, h2d_ms = 0, merge_ms = 0, d2h_ms = 0;
+    detail::check(acg_partitioned_timings(r, &wc, &launched, &build_s, &scan_s, &gpu_ms, &total_s, &h2d_ms, &merge_ms,
+                                          &d2h_ms));
+    run.worker_count = wc;
+    run.workers_launched = launched;
+    run.per_worker_build_s.assign(build_s, build_s + launched);
+    run.per_worker_scan_s.assign(scan_s, scan_s + launched);
+    for (std::uint32_t k = 0; k < launched; ++k) run.per_worker_gpu_scan_s.push_back(gpu_ms[k] * 1e-3);
+    run.h2d_gpu_s = h2d_ms * 1e-3;
+    run.merge_gpu_s = merge_ms * 1e-3;
+    run.d2h_s = d2h_ms * 1e-3;
+    run.total_wall_s = total_s;
     return run;
 }
 

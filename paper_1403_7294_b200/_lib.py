@@ -67,6 +67,14 @@ ACG_SYMBOLS = {
     "acg_automaton_layout": (C.c_int, [vp, u32p, u32p, u32p, u32p, C.POINTER(C.c_int)]),
     "acg_automaton_filter_info": (C.c_int, [vp, u32p, C.POINTER(C.c_double)]),
     "acg_scanner_set_geometry": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint64]),
+    "acg_run_partitioned": (C.c_int, [vp, vp, C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(vp)]),
+    "acg_partitioned_match_count": (C.c_uint64, [vp]),
+    "acg_partitioned_ids": (vp, [vp]),
+    "acg_partitioned_ends": (vp, [vp]),
+    "acg_partitioned_timings": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(vp),
+                                          C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "acg_partitioned_destroy": (None, [vp]),
     "acg_scanner_format": (C.c_int, [vp, C.c_int, C.c_uint64, C.c_uint64, vp, C.c_uint64, C.POINTER(C.c_uint64)]),
     "acg_scanner_write_matches": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "acg_load_input": (C.c_int, [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_uint64)]),

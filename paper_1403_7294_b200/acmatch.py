@@ -499,3 +499,61 @@ def scan_pipelined(a: Automaton, text, device: int = 0, piece_bytes: int = 0, li
                                          C.byref(m), C.byref(ib), C.byref(fol)))
     recs = None if out is None else out[:min(m.value, cap)]
     return recs, ib.value, cnt, m.value, fol.value
+
+
+# ---- the paper's dictionary-partitioned run (reference partition.hpp:29-170) ----
+
+@dataclass
+class PartitionedRun:
+    """acmatch::PartitionedRun (partition.hpp:92-99) plus device-timed fields."""
+    matches: list
+    per_worker_build_s: list
+    per_worker_scan_s: list
+    total_wall_s: float
+    worker_count: int
+    workers_launched: int
+    per_worker_gpu_scan_s: list = field(default_factory=list)
+    h2d_gpu_s: float = 0.0
+    merge_gpu_s: float = 0.0
+    d2h_s: float = 0.0
+    ids: np.ndarray | None = None
+    ends: np.ndarray | None = None
+
+
+def run_partitioned(patterns: Sequence[Pattern], input, worker_count: int, device: int = 0,
+                    records: bool = True) -> PartitionedRun:
+    """acg_run_partitioned: dictionary split into worker_count contiguous chunks,
+    one worker per non-empty chunk, the device-side merge. `records=False`
+    skips building the MatchRecord list (ids/ends arrays only)."""
+    if worker_count < 1:
+        raise InvalidWorkerCountError("worker count must be >= 1")
+    concat, offs = _pack(patterns)
+    text = _as_u8(input)
+    h = C.c_void_p()
+    _check(_lib.acg().acg_run_partitioned(concat.ctypes.data_as(C.c_void_p) if concat.size else None,
+                                          offs.ctypes.data_as(C.c_void_p), len(patterns),
+                                          text.ctypes.data_as(C.c_void_p) if text.size else None, text.size,
+                                          worker_count, device, C.byref(h)))
+    L = _lib.acg()
+    try:
+        m = L.acg_partitioned_match_count(h)
+        ids = np.ctypeslib.as_array(C.cast(L.acg_partitioned_ids(h), C.POINTER(C.c_uint32)), shape=(m,)).copy() \
+            if m else np.zeros(0, np.uint32)
+        ends = np.ctypeslib.as_array(C.cast(L.acg_partitioned_ends(h), C.POINTER(C.c_uint64)), shape=(m,)).copy() \
+            if m else np.zeros(0, np.uint64)
+        wc, launched = C.c_uint32(), C.c_uint32()
+        bp, sp, gp = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        tot, h2d, mg, d2h = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        _check(L.acg_partitioned_timings(h, C.byref(wc), C.byref(launched), C.byref(bp), C.byref(sp), C.byref(gp),
+                                         C.byref(tot), C.byref(h2d), C.byref(mg), C.byref(d2h)))
+        k = launched.value
+
+        def arr(p):
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(k,)).tolist() if k else []
+
+        recs = [MatchRecord(int(i), int(e)) for i, e in zip(ids.tolist(), ends.tolist())] if records else []
+        return PartitionedRun(recs, arr(bp), arr(sp), tot.value, wc.value, k,
+                              [x * 1e-3 for x in arr(gp)], h2d.value * 1e-3, mg.value * 1e-3, d2h.value * 1e-3,
+                              ids, ends)
+    finally:
+        L.acg_partitioned_destroy(h)

@@ -2153,3 +2153,6 @@ std::uint64_t acg_result_failure_follows(const acg_result* r) { return r ? r->fo
 void acg_result_destroy(acg_result* r) { delete r; }
 
 }  // extern "C"
+
+// the GPU-native dictionary-partitioned run (its own C-ABI entry points)
+#include "partition.cuh"

@@ -32,6 +32,7 @@ def _stale(target: str, sources: list[str]) -> bool:
 
 
 HOST_SOURCES = ("automaton.cpp", "parallel.cpp", "host_io.cpp")  # host C++ of libacg.so
+DEVICE_SOURCES = ("acg_device.cu",)  # CUDA translation units of libacg.so
 
 
 def build(force: bool = False, verbose_ptxas: bool = False) -> None:
@@ -46,7 +47,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         _run(["g++", "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", synth, src])
 
     headers = [os.path.join(CSRC, h) for h in ("automaton.hpp", "scan_kernels.cuh", "filter_kernels.cuh",
-                                               "exact_kernels.cuh", "qfilter.hpp", "parallel.hpp")] + [
+                                               "exact_kernels.cuh", "format_kernels.cuh", "partition.cuh", "qfilter.hpp", "parallel.hpp")] + [
         os.path.join(ROOT, "include", "acg.h")]
     host_objs = []
     for name in HOST_SOURCES:
@@ -56,16 +57,19 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
             _run(["g++", "-std=c++17", "-O3", "-fPIC", "-pthread", "-c", "-o", o, src_c] + inc +
                  ["-I", os.path.join(os.path.dirname(NVCC), "..", "include")])
         host_objs.append(o)
-    dev_src = os.path.join(CSRC, "acg_device.cu")
-    dev_o = os.path.join(obj, "acg_device.o")
-    if force or _stale(dev_o, [dev_src] + headers):
-        cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", "-o", dev_o, dev_src] + inc
-        if verbose_ptxas:
-            cmd.insert(1, "-Xptxas=-v")
-        _run(cmd)
+    dev_objs = []
+    for name in DEVICE_SOURCES:
+        dev_src = os.path.join(CSRC, name)
+        dev_o = os.path.join(obj, name.replace(".cu", ".o"))
+        if force or _stale(dev_o, [dev_src] + headers):
+            cmd = [NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-c", "-o", dev_o, dev_src] + inc
+            if verbose_ptxas:
+                cmd.insert(1, "-Xptxas=-v")
+            _run(cmd)
+        dev_objs.append(dev_o)
     lib = os.path.join(LIB, "libacg.so")
-    if force or _stale(lib, host_objs + [dev_o]):
-        _run([NVCC, *ARCH, "-shared", "-o", lib, *host_objs, dev_o, "-Xcompiler", "-pthread"])
+    if force or _stale(lib, host_objs + dev_objs):
+        _run([NVCC, *ARCH, "-shared", "-o", lib, *host_objs, *dev_objs, "-Xcompiler", "-pthread"])
 
 
 def build_variant(name: str, defines: list[str]) -> str:
@@ -78,7 +82,8 @@ def build_variant(name: str, defines: list[str]) -> str:
           os.path.join(CSRC, "acg_device.cu")] + inc + [f"-D{d}" for d in defines])
     lib = os.path.join(out, "libacg.so")
     host_objs = [os.path.join(LIB, "obj", name.replace(".cpp", ".o")) for name in HOST_SOURCES]
-    _run([NVCC, *ARCH, "-shared", "-o", lib, *host_objs, dev_o, "-Xcompiler", "-pthread"])
+    others = [os.path.join(LIB, "obj", name.replace(".cu", ".o")) for name in DEVICE_SOURCES if name != "acg_device.cu"]
+    _run([NVCC, *ARCH, "-shared", "-o", lib, *host_objs, dev_o, *others, "-Xcompiler", "-pthread"])
     return lib
 
 

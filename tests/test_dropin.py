@@ -74,3 +74,16 @@ def test_reference_acceptance_criterion_on_gpu(criterion):
     # 77 = the criterion skipped itself (criterion 7 below 4 hardware threads)
     assert p.returncode in (0, 77), _summary(p)
     assert ("PASS" in p.stdout) or ("SKIP" in p.stdout), _summary(p)
+
+
+EXT = os.path.join(ROOT, "oracle", "_ref", "dropin_ext_tests")
+
+
+@pytest.mark.gpu
+def test_dropin_extensions_on_gpu():
+    """This repo's C++ tests of the drop-in's extensions (tests/cpp/test_dropin_ext.cpp):
+    device-timed run_partitioned fields, GPU benchmark rows and CSV, pinned-input scan."""
+    _need(EXT)
+    p = _run([EXT], 600)
+    assert p.returncode == 0, _summary(p)
+    assert "0 failed" in p.stdout
