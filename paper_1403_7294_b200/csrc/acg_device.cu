@@ -592,11 +592,12 @@ cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
     using namespace acg::kern;
     const QKernelChoice c = qfilter_choice();
     const std::size_t bloom = static_cast<std::size_t>(a.qwords) * 4;
-    if (qfilter_fused(a)) {
+    if (qfilter_fused(a) && !a.qbm) {
         if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, true>, a, 32 * 17, bloom, sms, st);
         return launch_q(qfilter_ldg_kernel<16, 2, false, true>, a, 32 * 17, bloom, sms, st);
     }
     if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, false>, a, 32 * 16, bloom, sms, st);
+    if (a.qbm) return launch_q(qfilter_ldg_kernel<16, 2, false, false, true>, a, 32 * 16, bloom, sms, st);
     if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2, false, false>, a, 32 * 24, bloom, sms, st);
     if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3, false, false>, a, 32 * 16, bloom, sms, st);
     return launch_q(qfilter_ldg_kernel<16, 2, false, false>, a, 32 * 16, bloom, sms, st);
@@ -1041,6 +1042,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         a.qwarp_n = s->qwarp_n.p;
         a.qwarps = static_cast<std::uint32_t>(warps);
         a.qwords = static_cast<std::uint32_t>(d.qbloom.size());
+        a.qbm = d.qbm ? 1u : 0u;
         a.qbloom2 = d.qbloom2.empty() ? nullptr : dd.qbloom2.p;
         a.qwords2 = static_cast<std::uint32_t>(d.qbloom2.size());
         a.qcand_cap = static_cast<std::uint32_t>(cap);
@@ -1062,7 +1064,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             a.qreg = static_cast<long long>(s->chunk);
             a.reg_n = s->qreg_n.p;
             a.qscal = s->qscal.p;
-            if (qfilter_fused(a)) {  // V1 runs inside KQ: its region counters start at zero
+            if (qfilter_fused(a) && !a.qbm) {  // V1 runs inside KQ: its region counters start at zero
                 zero_later(s, s->qreg_n.p, W * sizeof(std::uint32_t));
                 ACG_CUDA(flush_zeros(s, st));
                 ACG_CUDA(launch_qfilter(a, dd.num_sms, st));

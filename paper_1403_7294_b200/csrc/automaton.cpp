@@ -347,6 +347,7 @@ namespace {
 void compile_qfilter(const Nfa& nfa, Dfa& d) {
     Phase ph_all("compile_qfilter");
     d.filter_ok = false;
+    d.qbm = false;
     d.qbloom.clear();
     d.qbloom2.clear();
     d.qtab.clear();
@@ -371,19 +372,38 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
     Phase ph_g("  grams sort+tables");
     parallel_sort(grams, [](const std::pair<std::uint32_t, std::uint32_t>& x, const std::pair<std::uint32_t, std::uint32_t>& y) { return x < y; });
     ph_g.next("  bloom level 1");
-    std::uint32_t words = kQWords;
+    std::uint32_t keys = 0;
+    for (std::size_t i = 0; i < grams.size(); ++i) keys += !i || grams[i].first != grams[i - 1].first;
+    // level 1: a bitmap of the keys' 10-gram prefixes for dictionaries it keeps
+    // selective (qfilter.hpp), with the Bloom filter of the full q-grams after it;
+    // else the Bloom filter alone in all of shared memory
+    // Off by default (ACG_QBITMAP=1 turns it on): on cfg1 it halves the
+    // survivors (V1 24.6 -> 18.5 us) but KQ runs 0.242 ms against 0.226 with the
+    // Bloom filter alone — the lanes' level-1 hits (3.8 % of samples) make the
+    // level-2 probes a divergent loop of dependent hash/LDS chains.
+    static const bool bm_on = [] {
+        const char* e = std::getenv("ACG_QBITMAP");
+        return e && e[0] == '1';
+    }();
+    d.qbm = bm_on && q >= 10 && keys <= kQBitmapMaxKeys;
+    std::uint32_t words = d.qbm ? kQWordsBM : kQWords;
     if (const char* e = std::getenv("ACG_QWORDS")) {  // experiments only (Bloom size sweeps)
         const long v = std::strtol(e, nullptr, 10);
-        if (v >= 1024 && v <= 57344) words = static_cast<std::uint32_t>(v) & ~3u;
+        if (!d.qbm && v >= 1024 && v <= 57344) words = static_cast<std::uint32_t>(v) & ~3u;
     }
-    d.qbloom.assign(words, 0u);
-    std::uint32_t keys = 0;
+    std::vector<std::uint32_t> bloom(words, 0u), bitmap(d.qbm ? kQBitmapWords : 0u, 0u);
     for (std::size_t i = 0; i < grams.size(); ++i) {
         if (i && grams[i].first == grams[i - 1].first) continue;
-        ++keys;
         const std::uint32_t h = qhash(qtop(grams[i].first, q));
-        d.qbloom[qword(h, words)] |= qmask(h);
+        bloom[qword(h, words)] |= qmask(h);
+        if (d.qbm) {
+            const std::uint32_t idx = grams[i].first & 0xFFFFFu;  // bases 0..9 (2 bits each)
+            bitmap[idx >> 5] |= 1u << (idx & 31);
+        }
     }
+    // the shared-memory image the KQ kernel stages: [bitmap | Bloom] or [Bloom]
+    d.qbloom = bitmap;
+    d.qbloom.insert(d.qbloom.end(), bloom.begin(), bloom.end());
     ph_g.next("  q-gram table");
     // load factor <= 1/4: a random (non-key) code ends its probe in ~1.4 slots
     d.qtab_bits = 10;
@@ -432,7 +452,14 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
             const std::uint32_t c = static_cast<std::uint32_t>(r ^ (r >> 31)) & qm;
             const std::uint32_t h = qhash(qtop(c, q));
             const std::uint32_t m = qmask(h);
-            if ((d.qbloom[qword(h, words)] & m) != m) continue;
+            if (d.qbm) {
+                const std::uint32_t idx = c & 0xFFFFFu;
+                if (!(bitmap[idx >> 5] >> (idx & 31) & 1u)) continue;
+                ++p1;
+                p2 += (bloom[qword(h, words)] & m) == m;
+                continue;
+            }
+            if ((bloom[qword(h, words)] & m) != m) continue;
             ++p1;
             if (!words2) {
                 ++p2;
@@ -453,7 +480,7 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         pass_rates(d.filter_fp1, d.filter_fp);
     }
     ph_g.next("  level 2");
-    if (d.filter_fp > 5e-3 && d.filter_fp1 <= kQLevel1Max) {
+    if (!d.qbm && d.filter_fp > 5e-3 && d.filter_fp1 <= kQLevel1Max) {
         // level 2: ~1.5 % of its bits set (4 bits per key)
         std::uint64_t w2 = (static_cast<std::uint64_t>(keys) * 4 * 100 / 3 / 32 + 3) & ~3ull;
         w2 = std::min<std::uint64_t>(std::max<std::uint64_t>(w2, 1024), 16ull << 20);
@@ -468,6 +495,7 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
     // worth it when few samples survive (each survivor costs an exact probe)
     d.filter_ok = d.filter_fp <= 5e-3;
     if (!d.filter_ok) {
+        d.qbm = false;
         d.pat_code.clear();
         d.qbloom2.clear();
         d.qbloom.clear();

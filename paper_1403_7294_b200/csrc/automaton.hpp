@@ -105,7 +105,11 @@ struct Dfa {
     // whose shortest pattern has at least kQMinQ + kQSample - 1 bytes.
     bool filter_ok = false;
     std::uint32_t q = 0;
-    std::vector<std::uint32_t> qbloom;   // blocked Bloom filter of the (pattern, offset) q-grams (kQWords words)
+    // shared-memory image of level 1: the blocked Bloom filter of the (pattern,
+    // offset) q-grams (kQWords words), or with qbm a 2^20-bit bitmap of their
+    // 10-gram prefixes followed by that Bloom filter (kQBitmapWords + kQWordsBM)
+    std::vector<std::uint32_t> qbloom;
+    bool qbm = false;
     std::uint32_t qtab_bits = 0;         // exact table: 2^qtab_bits slots of (code, bucket start | kQEmpty)
     std::vector<std::uint32_t> qtab;     // 2 * 2^qtab_bits
     std::vector<std::uint32_t> qb_off;   // bucket offsets (keys + 1)

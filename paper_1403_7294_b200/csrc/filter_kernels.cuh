@@ -145,7 +145,7 @@ __device__ __forceinline__ uint4 ldg_stream(const std::uint8_t* p) {
 
 __device__ __forceinline__ const std::uint32_t* tab_of() { return reinterpret_cast<const std::uint32_t*>(acg_hot_smem); }
 
-template <int NW, int R, bool L2F, bool FUSED>
+template <int NW, int R, bool L2F, bool FUSED, bool BM>
 __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::uint32_t* tab, std::uint32_t* wcnt,
                                                 std::uint32_t* pub, std::uint32_t* nfin) {
     constexpr long long kBlk = 2048;
@@ -215,10 +215,38 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
                     nb_[r] = __shfl_sync(0xFFFFFFFFu, s, (lane + 1) & 31);
                 }
                 std::uint32_t t[16];
+                std::uint32_t bm_hits = 0;  // BM: samples that pass both levels (bit 4r+o)
+                if (BM) {
+                    // level 1: bit (c & 0xFFFFF) of a 2^20-bit bitmap of the keys' 10-gram
+                    // prefixes; the word's bit is rotated to position k and merged into
+                    // the mask (SHF, LOP3, LDS, SHF.W, LOP3 per sample, no hashing)
+                    std::uint32_t hm = 0;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+#pragma unroll
+                        for (int o = 0; o < 4; ++o) {
+                            const std::uint32_t win = window(cur[r], nb_[r], o);
+                            const std::uint32_t wd = tab[(win >> 5) & (kQBitmapWords - 1)];
+                            hm |= __funnelshift_r(wd, wd, win - (4 * r + o)) & (1u << (4 * r + o));
+                        }
+                    // level 2, the lane's level-1 hits only: the blocked Bloom filter of
+                    // the full q-grams after the bitmap
+                    const std::uint32_t* bl = tab + kQBitmapWords;
+                    const std::uint32_t w2 = words - kQBitmapWords;
+                    for (std::uint32_t mm = hm; mm; mm &= mm - 1) {
+                        const int k = __ffs(mm) - 1, r = k >> 2, o = k & 3;
+                        const std::uint32_t lo = r == 0 ? cur[0] : r == 1 ? cur[1] : r == 2 ? cur[2] : cur[3];
+                        const std::uint32_t hi = r == 0 ? nb_[0] : r == 1 ? nb_[1] : r == 2 ? nb_[2] : nb_[3];
+                        const std::uint32_t h = (o == 0 ? lo : __funnelshift_r(lo, hi, 8 * o)) * qmul;
+                        const std::uint32_t m = qmask(h);
+                        if ((bl[qword(h, w2)] & m) == m) bm_hits |= 1u << k;
+                    }
+                } else {
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
 #pragma unroll
                     for (int o = 0; o < 4; ++o) t[4 * r + o] = probe(window(cur[r], nb_[r], o) * qmul);
+                }
                 if (L2F) {
                     // level 2 for the samples level 1 passed: predicated L2-resident
                     // probes, issued together (one L2 latency per block)
@@ -239,20 +267,29 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
 #pragma unroll
                     for (int i = 0; i < 16; ++i) t[i] |= m2[i] & ~v2[i];
                 }
-                std::uint32_t z = min(min(t[0], t[1]), t[2]);
-                z = min(min(z, t[3]), t[4]);
-                z = min(min(z, t[5]), t[6]);
-                z = min(min(z, t[7]), t[8]);
-                z = min(min(z, t[9]), t[10]);
-                z = min(min(z, t[11]), t[12]);
-                z = min(min(z, t[13]), t[14]);
-                z = min(z, t[15]);
-                const bool hit = z == 0u;
+                bool hit;
+                if (BM) {
+                    hit = bm_hits != 0u;
+                } else {
+                    std::uint32_t z = min(min(t[0], t[1]), t[2]);
+                    z = min(min(z, t[3]), t[4]);
+                    z = min(min(z, t[5]), t[6]);
+                    z = min(min(z, t[7]), t[8]);
+                    z = min(min(z, t[9]), t[10]);
+                    z = min(min(z, t[11]), t[12]);
+                    z = min(min(z, t[13]), t[14]);
+                    z = min(z, t[15]);
+                    hit = z == 0u;
+                }
                 const bool anyhit = __any_sync(0xFFFFFFFFu, hit);
                 if (anyhit && hit) {
                     std::uint32_t pm = 0;
+                    if (BM) {
+                        pm = bm_hits;
+                    } else {
 #pragma unroll
-                    for (int o = 0; o < 16; ++o) pm |= (t[o] == 0u ? 1u : 0u) << o;
+                        for (int o = 0; o < 16; ++o) pm |= (t[o] == 0u ? 1u : 0u) << o;
+                    }
                     const long long P = b * kBlk + 16 * lane;
                     if (b >= nfull) {  // the text's partial last block: samples past its end are not survivors
 #pragma unroll
@@ -369,7 +406,7 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
 }
 
 
-template <int NW, int R, bool L2F, bool FUSED>
+template <int NW, int R, bool L2F, bool FUSED, bool BM = false>
 __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_kernel(const ScanArgs a) {
     __shared__ std::uint32_t wcnt[NW], pub[NW], done_sh[NW], nfin;
     {
@@ -383,7 +420,7 @@ __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_ke
     if (FUSED && (threadIdx.x >> 5) == NW) {  // the consumer warp
         qfilter_consume<NW>(a, pub, done_sh, &nfin);
     } else {
-        qfilter_produce<NW, R, L2F, FUSED>(a, tab_of(), wcnt, pub, &nfin);
+        qfilter_produce<NW, R, L2F, FUSED, BM>(a, tab_of(), wcnt, pub, &nfin);
     }
     if (FUSED) {
         __syncthreads();

@@ -34,6 +34,12 @@ constexpr std::uint32_t kQMinQ = 10;    // below this the filter is not selectiv
 constexpr std::uint32_t kQBlock = 64;   // dirty-block size (bytes)
 constexpr std::uint32_t kQChunkBlocks = 128;  // blocks per output chunk (8 KiB)
 constexpr std::uint32_t kQWords = 57344;      // Bloom words (224 KiB: all of the opt-in shared memory but 3 KiB)
+// Bitmap level 1 (dictionaries of at most kQBitmapMaxKeys keys): a 2^20-bit
+// bitmap of the keys' 10-gram prefixes (128 KiB, direct index: no hash),
+// then a blocked Bloom filter of the full q-grams in the rest of shared memory.
+constexpr std::uint32_t kQBitmapWords = 1u << 15;
+constexpr std::uint32_t kQWordsBM = 24576;      // level-2 Bloom words beside the bitmap (96 KiB)
+constexpr std::uint32_t kQBitmapMaxKeys = 60000;  // bitmap density <= 5.7 %
 constexpr std::uint32_t kQMul0 = 0x9E3779B1u, kQMul1 = 0x85EBCA77u, kQMul2 = 0xC2B2AE3Du;
 constexpr std::uint32_t kQEmpty = 0xFFFFFFFFu;  // exact-table slot marker
 constexpr std::uint32_t kQSingle = 0x80000000u;  // slot payload = kQSingle | the bucket's only entry

@@ -113,7 +113,8 @@ struct ScanArgs {
     const std::uint32_t* qb_ent;            // pattern id << 2 | offset
     const std::uint8_t* pat_bytes;          // the dictionary
     const std::uint32_t* pat_off;           // n_patterns + 1
-    std::uint32_t qwords;                   // Bloom words
+    std::uint32_t qwords;                   // words of the staged level-1 image (Bloom, or bitmap + Bloom)
+    std::uint32_t qbm;                      // 1: level 1 = 10-gram bitmap, then the Bloom filter (qfilter.hpp)
     const std::uint32_t* qbloom2;           // level-2 Bloom filter (L2-resident; null = single level)
     std::uint32_t qwords2;
     unsigned long long* qcands;             // KQ survivors (sample offsets): one region of qcand_cap per KQ warp
