@@ -573,6 +573,18 @@ unsigned qfilter_warps() { return static_cast<unsigned>(qfilter_choice().nw); }
 // V1 launch): region pipeline, 16x2 geometry; ACG_QFUSED=1 turns it on. Off by
 // default: measured 0.294 ms against 0.226 + 0.028 (V1) unfused on cfg1 — the
 // producers lose registers (96 at 544 threads) and the consumer issue slots.
+// V1 inside KQ after the streaming loop (each CTA confirms its own warps'
+// survivors): ACG_QPOST=1 (experiment).
+bool qfilter_post(const ScanArgs& a) {
+    static const bool on = [] {
+        // off by default: measured 0.2558 ms/step on cfg1 against 0.2483 with the
+        // separate V1 launch (512 threads per SM hide the confirmations' L2 latency
+        // worse than V1's 2048, and the CTAs' streaming ends nearly together)
+        const char* e = std::getenv("ACG_QPOST");
+        return e && e[0] == '1';
+    }();
+    return on && a.reg_n;
+}
 bool qfilter_fused(const ScanArgs& a) {
     static const bool on = [] {
         const char* e = std::getenv("ACG_QFUSED");
@@ -581,6 +593,33 @@ bool qfilter_fused(const ScanArgs& a) {
     const QKernelChoice c = qfilter_choice();
     return on && a.reg_n && c.nw == 16 && c.r == 2;
 }
+// Programmatic dependent launch: the kernel may be scheduled while the previous
+// kernel on the stream drains (it waits for that grid's results with
+// griddepcontrol.wait before reading them): hides launch latency between the
+// filter pipeline's stages. ACG_PDL=0 launches plainly.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned threads, cudaStream_t st, Args&&... args) {
+    static const bool on = [] {
+        const char* e = std::getenv("ACG_PDL");
+        return !(e && e[0] == '0');
+    }();
+    if (!on) {
+        k<<<grid, threads, 0, st>>>(std::forward<Args>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 template <typename Kern>
 cudaError_t launch_q(Kern k, const ScanArgs& a, unsigned threads, std::size_t smem, int sms, cudaStream_t st) {
     cudaError_t e = prepare_smem(k, smem);
@@ -595,6 +634,11 @@ cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
     if (qfilter_fused(a) && !a.qbm) {
         if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, true>, a, 32 * 17, bloom, sms, st);
         return launch_q(qfilter_ldg_kernel<16, 2, false, true>, a, 32 * 17, bloom, sms, st);
+    }
+    if (qfilter_post(a)) {
+        if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, false, false, true>, a, 32 * 16, bloom, sms, st);
+        if (a.qbm) return launch_q(qfilter_ldg_kernel<16, 2, false, false, true, true>, a, 32 * 16, bloom, sms, st);
+        return launch_q(qfilter_ldg_kernel<16, 2, false, false, false, true>, a, 32 * 16, bloom, sms, st);
     }
     if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, false>, a, 32 * 16, bloom, sms, st);
     if (a.qbm) return launch_q(qfilter_ldg_kernel<16, 2, false, false, true>, a, 32 * 16, bloom, sms, st);
@@ -1064,7 +1108,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             a.qreg = static_cast<long long>(s->chunk);
             a.reg_n = s->qreg_n.p;
             a.qscal = s->qscal.p;
-            if (qfilter_fused(a) && !a.qbm) {  // V1 runs inside KQ: its region counters start at zero
+            if ((qfilter_fused(a) && !a.qbm) || qfilter_post(a)) {  // V1 runs inside KQ: its region counters start at zero
                 zero_later(s, s->qreg_n.p, W * sizeof(std::uint32_t));
                 ACG_CUDA(flush_zeros(s, st));
                 ACG_CUDA(launch_qfilter(a, dd.num_sms, st));
@@ -1078,15 +1122,14 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
                     const int v = e ? std::atoi(e) : 0;
                     return v > 0 && v <= 64 ? static_cast<unsigned>(v) : 8u;
                 }();
-                qconfirm_region_kernel<<<v1_ctas * dd.num_sms, 256, 0, st>>>(a);
-                ACG_CUDA(cudaGetLastError());
+                ACG_CUDA(launch_pdl(qconfirm_region_kernel, v1_ctas * dd.num_sms, 256, st, a));
             }
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[2], st));
             ScanArgs oa = a;
             oa.records = want_list ? s->records.p : nullptr;
             oa.rec_cap = want_list ? s->records.n : 0;
-            qorder_region_kernel<<<(W + kQOrderWarps - 1) / kQOrderWarps, 32 * kQOrderWarps, 0, st>>>(oa, s->chunk_offs.p);
-            ACG_CUDA(cudaGetLastError());
+            ACG_CUDA(launch_pdl(qorder_region_kernel, (W + kQOrderWarps - 1) / kQOrderWarps, 32 * kQOrderWarps, st, oa,
+                                s->chunk_offs.p));
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[5], st));
             s->ev_mask = 0x27;  // events 0, 1, 2, 5 (stages KQ, V1, ORDER)
             s->launches += 3;

@@ -143,9 +143,13 @@ __device__ __forceinline__ uint4 ldg_stream(const std::uint8_t* p) {
     return v;
 }
 
+// programmatic dependent launch (sm_90+): wait for / release the stream's neighbouring grids
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ const std::uint32_t* tab_of() { return reinterpret_cast<const std::uint32_t*>(acg_hot_smem); }
 
-template <int NW, int R, bool L2F, bool FUSED, bool BM>
+template <int NW, int R, bool L2F, bool FUSED, bool BM, bool POST>
 __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::uint32_t* tab, std::uint32_t* wcnt,
                                                 std::uint32_t* pub, std::uint32_t* nfin) {
     constexpr long long kBlk = 2048;
@@ -326,7 +330,8 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
     if (lane == 0) {
         const std::uint32_t found = *static_cast<volatile std::uint32_t*>(&wcnt[warp]);
         a.qwarp_n[gw] = found;
-        if (!FUSED && a.reg_n && gw < a.n_chunks) a.reg_n[gw] = 0u;  // V1's per-region counters (one per chunk)
+        // V1's per-region counters (one per chunk; zeroed by the host when V1 runs inside KQ)
+        if (!FUSED && !POST && a.reg_n && gw < a.n_chunks) a.reg_n[gw] = 0u;
         atomicAdd(a.qcand_n, found);
         atomicMax(a.qcand_max, static_cast<unsigned long long>(found));
         if (FUSED) {
@@ -406,7 +411,9 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
 }
 
 
-template <int NW, int R, bool L2F, bool FUSED, bool BM = false>
+// POST: the CTA confirms its own warps' survivors right after streaming (V1
+// inside KQ, overlapping the other CTAs' streaming tails; no V1 launch).
+template <int NW, int R, bool L2F, bool FUSED, bool BM = false, bool POST = false>
 __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_kernel(const ScanArgs a) {
     __shared__ std::uint32_t wcnt[NW], pub[NW], done_sh[NW], nfin;
     {
@@ -420,7 +427,19 @@ __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_ke
     if (FUSED && (threadIdx.x >> 5) == NW) {  // the consumer warp
         qfilter_consume<NW>(a, pub, done_sh, &nfin);
     } else {
-        qfilter_produce<NW, R, L2F, FUSED, BM>(a, tab_of(), wcnt, pub, &nfin);
+        qfilter_produce<NW, R, L2F, FUSED, BM, POST>(a, tab_of(), wcnt, pub, &nfin);
+    }
+    if (!POST && !FUSED) pdl_trigger();  // V1 may be scheduled (it waits for this grid's results)
+    if (POST) {
+        __syncthreads();  // this CTA's survivors and their counts are written
+        const unsigned long long cap = a.qcand_cap;
+        const unsigned long long t0 = static_cast<unsigned long long>(blockIdx.x) * NW * cap;
+        for (unsigned long long t = t0 + threadIdx.x; t < t0 + NW * cap; t += blockDim.x) {
+            const long long w = static_cast<long long>(t / cap);
+            if (t - static_cast<unsigned long long>(w) * cap < min(wcnt[w - static_cast<long long>(blockIdx.x) * NW],
+                                                                   a.qcand_cap))
+                qconfirm_slot(a, w, t);
+        }
     }
     if (FUSED) {
         __syncthreads();
@@ -435,7 +454,9 @@ __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_ke
 // capacity), so every slab holds exactly its region's matches whatever the
 // pattern length.
 __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) {
+    pdl_wait();  // (launched programmatically after KQ: its survivors are complete past this point)
     const long long total = static_cast<long long>(a.qwarps) * a.qcand_cap;
+    pdl_trigger();  // ORDER may be scheduled (it waits for this grid's results)
     for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long w = t / a.qcand_cap;
@@ -454,6 +475,7 @@ constexpr int kQOrderMax = 1024;
 constexpr int kQOrderWarps = 4;
 
 __global__ void __launch_bounds__(32 * kQOrderWarps) qorder_region_kernel(const ScanArgs a, unsigned long long* offs) {
+    pdl_wait();  // (after V1: its slabs and region counts are complete past this point)
     static_assert(kQOrderWarps == 4, "the CTA prefix below reads whole uint4 groups of regions");
     __shared__ unsigned long long buf[kQOrderWarps][kQOrderMax];
     __shared__ unsigned long long part[kQOrderWarps];
@@ -528,6 +550,7 @@ template <int PASS>
 __global__ void __launch_bounds__(256) qconfirm_kernel(const ScanArgs a) {
     const std::uint32_t tmask = (1u << a.qtab_bits) - 1u;
     const long long total = static_cast<long long>(a.qwarps) * a.qcand_cap;
+    pdl_trigger();  // ORDER may be scheduled (it waits for this grid's results)
     for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         if (static_cast<std::uint32_t>(t % a.qcand_cap) >= a.qwarp_n[t / a.qcand_cap]) continue;
