@@ -976,6 +976,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     s->tpb_run = mode == ACG_MODE_SPARSE                ? sparse_tpb(s->U_run)
                  : (s->tpb_set || s->U_run > 2 || stats) ? s->tpb
                                                         : 2 * acg::kern::kTPB;
+    if (mode != ACG_MODE_SPARSE && (s->U_run > 2 || stats))  // those kernels are bounded at kTPB threads
+        s->tpb_run = std::min<std::uint32_t>(s->tpb_run, acg::kern::kTPB);
     plan_geometry(s, owned);
     const bool prof = s->flags & ACG_SCAN_PROFILE;
 
@@ -1913,8 +1915,8 @@ int acg_scanner_set_geometry(acg_scanner* s, std::uint32_t streams_per_thread, s
         s->U = streams_per_thread;
     }
     if (threads_per_block) {
-        if (threads_per_block % 32 || threads_per_block > static_cast<std::uint32_t>(acg::kern::kTPB))
-            return fail(ACG_ERR_INVALID, "threads per block must be a multiple of 32, at most 512");
+        if (threads_per_block % 32 || threads_per_block > 2u * acg::kern::kTPB)
+            return fail(ACG_ERR_INVALID, "threads per block must be a multiple of 32, at most 1024 (512 above 2 streams per thread)");
         s->tpb = threads_per_block;
         s->tpb_set = true;
     }
