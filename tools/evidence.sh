@@ -1,0 +1,28 @@
+#!/bin/bash
+# One gpurun call of round evidence: GPU tests, smoke, bench lines, the ncu
+# launch list of the default bench command and one --set full capture of the
+# EXACT walk (KE) on cfg3 (CSV exports; the .ncu-rep stays on the box).
+cd "$(dirname "$0")/.."
+O=gpurun_out/evidence; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $O/nvidia-smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+BENCH=${BENCH:-"--steps 20;--config 0 --steps 20;--config 2 --steps 10 --no-cpu-baseline;--config 3 --steps 5 --no-cpu-baseline --profile-layout;--config 3 --steps 5 --no-cpu-baseline;--config 4 --text-mib 256 --steps 3 --no-cpu-baseline;--mode exact --steps 10 --no-cpu-baseline;--mode sparse --steps 10 --no-cpu-baseline"}
+IFS=';' read -ra RUNS <<< "$BENCH"
+for r in "${RUNS[@]}"; do
+  echo "== $r" >> $O/bench.log
+  timeout 900 python bench.py $r >> $O/bench.log 2>> $O/bench.err
+done
+timeout 600 python bench.py --steps 20 --impl reference > $O/bench_reference.json 2>> $O/bench.err
+if [ -z "$NO_NCU" ]; then
+  timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg1.csv \
+      python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_launch.log 2>&1
+  C3="python tools/exact_probe.py 3 256 exact both profile 2 1024"
+  timeout 300 $C3 > $O/plain_ke3.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"exact_event_kernel|event_count|event_expand" \
+      -s 12 -c 3 -o /tmp/ke3 -f $C3 > $O/ncu_ke3.log 2>&1
+  ncu -i /tmp/ke3.ncu-rep --page raw --csv > $O/ncu_ke3_raw.csv 2>/dev/null
+  ncu -i /tmp/ke3.ncu-rep --page details --csv > $O/ncu_ke3_details.csv 2>/dev/null
+fi
+echo done
