@@ -194,6 +194,8 @@ struct DeviceDfa {
     DevBuf<unsigned long long> fmt_off[2];
     std::uint32_t hot_bytes = 0;   // exact table image: (H+1)*K u16, padded to 16
     std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
+    DevBuf<std::uint16_t> hotG;    // generic alphabets: SPARSE-G truncated automaton (exact_kernels.cuh)
+    std::uint32_t hotG_bytes = 0;
     int smem_optin = 0;
     int num_sms = 0;
 };
@@ -300,6 +302,9 @@ struct acg_scanner {
     // event counts, per-chunk slab offsets, pool counter; the last event run's
     // geometry and totals size the next one's slabs
     DevBuf<std::uint32_t> xev, xev_count, xev_slab, xev_pool;
+    DevBuf<std::uint32_t> gfin, gfin_count, gfin_pool;  // SPARSE-G: the fix-up's final events (chunk + 1 slots per chunk)
+    bool g_run = false;                                  // the last run walked SPARSE-G
+    std::uint32_t walk_pool_blocks = 0;                  // pool blocks of the last walk's event slabs
     acg::kern::EventArgs eargs{};
     bool ev_run = false;
     unsigned long long xev_chunk = 0, xev_chunks = 0, xev_total = 0, xev_n = 0;
@@ -374,6 +379,12 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
         std::vector<std::uint16_t> hh(dd->hotH_bytes / 2, 0);
         std::copy(d.hotH.begin(), d.hotH.end(), hh.begin());
         ACG_CUDA(upload(dd->hotH, hh.data(), hh.size(), up));
+    }
+    if (!d.hotG.empty()) {
+        dd->hotG_bytes = static_cast<std::uint32_t>((d.hotG.size() * 2 + 15) & ~std::size_t(15));
+        std::vector<std::uint16_t> hg(dd->hotG_bytes / 2, 0);
+        std::copy(d.hotG.begin(), d.hotG.end(), hg.begin());
+        ACG_CUDA(upload(dd->hotG, hg.data(), hg.size(), up));
     }
     if (d.filter_ok) {
         ACG_CUDA(upload(dd->qbloom, d.qbloom.data(), d.qbloom.size(), up));
@@ -851,6 +862,39 @@ bool event_slots_ok(const acg_scanner* s, std::uint32_t n_out, bool stats) {
     return on && !stats && n_out > 0 && bits_for(n_out) + bits_for(s->chunk) <= 32;
 }
 
+// SPARSE-G (generic alphabets, BFS hot set): ACG_SPARSEG=1 turns it on.
+// Off by default: exact, but measured 3.32 ms per 256 MiB of cfg3 against 1.38
+// for the KE walk — the walk logs an excursion event at ~every cold entry and
+// the one-thread-per-chunk replay (XG) is a long dependent chain of text and
+// L2 table loads (XG + E1 1.84 ms).
+bool sparseg_ok(const acg_scanner* s, std::uint32_t n_out) {
+    static const bool on = [] {
+        const char* e = std::getenv("ACG_SPARSEG");
+        return e && e[0] == '1';
+    }();
+    const DeviceDfa& dd = *s->dd;
+    const acg::Dfa& d = *dd.dfa;
+    return on && dd.hotG.p && dd.hotG_bytes + 256 <= static_cast<std::uint32_t>(dd.smem_optin) &&
+           bits_for(n_out + d.H) + bits_for(s->chunk + d.halo) <= 32;
+}
+
+template <int U>
+cudaError_t launch_sparseg(const ScanArgs& a, const acg::kern::EventArgs& e, std::uint32_t n_out, unsigned grid,
+                           unsigned tpb, std::size_t smem, cudaStream_t st) {
+    auto k = acg::kern::sparseg_walk_kernel<U>;
+    if (cudaError_t err = prepare_smem(k, smem)) return err;
+    k<<<grid, tpb, smem, st>>>(a, e, n_out);
+    return cudaGetLastError();
+}
+cudaError_t launch_sparseg_walk(std::uint32_t U, const ScanArgs& a, const acg::kern::EventArgs& e, std::uint32_t n_out,
+                                unsigned grid, unsigned tpb, std::size_t smem, cudaStream_t st) {
+    switch (U) {
+        case 1: return launch_sparseg<1>(a, e, n_out, grid, tpb, smem, st);
+        case 4: return launch_sparseg<4>(a, e, n_out, std::min(grid, grid), std::min(tpb, 512u), smem, st);
+        default: return launch_sparseg<2>(a, e, n_out, grid, tpb, smem, st);
+    }
+}
+
 // Event slabs for this run: per chunk from the previous event run's counts
 // when the geometry repeats (exact + 1/8 + 17 slots), else uniform from its
 // density (x 1.25 + 17; chunk/16 + 33 without history); overflow goes to the
@@ -935,6 +979,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     s->zeros.clear();
     s->scratch_run = false;
     s->ev_run = false;
+    s->g_run = false;
     s->synced = false;
     s->last = st;
     s->run_text = d_text;
@@ -1191,18 +1236,54 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     } else if (event_slots_ok(s, n_out_states, stats)) {
         // event pipeline (exact_kernels.cuh): KE walk logs output visits, E1
         // counts records per chunk + visits, K2 prefix, E2 expands (enqueue_write)
-        ACG_CUDA(plan_events(s, n_out_states, st));
+        s->g_run = sparseg_ok(s, n_out_states);
+        ACG_CUDA(plan_events(s, s->g_run ? n_out_states + d.H : n_out_states, st));
+        s->walk_pool_blocks = s->eargs.pool_blocks;
         zero_later(s, s->xev_pool.p, sizeof(std::uint32_t));
         zero_later(s, s->scalars64.p + 8, sizeof(unsigned long long));
-        ACG_CUDA(flush_zeros(s, st));
-        s->ev_run = true;
+        zero_later(s, s->scalars64.p + 9, sizeof(unsigned long long));
         // KE strides chunks over the CTAs (exact_kernels.cuh): a full one-per-SM grid
         // whenever there are enough chunks, whatever the per-block rounding
         const unsigned g_ev = static_cast<unsigned>(std::max<unsigned long long>(
             s->grid, std::min<unsigned long long>(dd.num_sms, (s->n_chunks + s->U_run - 1) / s->U_run)));
-        ACG_CUDA(launch_event_walk(d.mode, s->U_run, a, s->eargs, g_ev, s->tpb_run, smem_bytes(dd), st));
-        ++s->launches;
-        if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+        if (s->g_run) {
+            // SPARSE-G: walk the truncated automaton (shared memory only), then replay
+            // the excursions exactly into the final events E1/E2 take
+            const unsigned long long ecap = s->chunk + 1;
+            ACG_CUDA(s->gfin.reserve(ecap * s->n_chunks, st));
+            ACG_CUDA(s->gfin_count.reserve(s->n_chunks, st));
+            ACG_CUDA(s->gfin_pool.reserve(1, st));
+            zero_later(s, s->gfin_pool.p, sizeof(std::uint32_t));
+            ACG_CUDA(flush_zeros(s, st));
+            acg::kern::EventArgs ew = s->eargs;
+            acg::kern::EventArgs ef{};
+            ef.ev = s->gfin.p;
+            ef.ecap = static_cast<std::uint32_t>(ecap);
+            ef.ev_count = s->gfin_count.p;
+            ef.pool_used = s->gfin_pool.p;
+            ef.pool_base = static_cast<std::uint32_t>(ecap * s->n_chunks);
+            ef.pool_blocks = 0;
+            ef.ob = bits_for(n_out_states);
+            ef.n_out = n_out_states;
+            ef.ev_total = s->scalars64.p + 9;
+            ScanArgs ga = a;
+            ga.hotH = dd.hotG.p;
+            ga.smem_table_bytes = dd.hotG_bytes;
+            ACG_CUDA(launch_sparseg_walk(s->U_run, ga, ew, n_out_states, g_ev, s->tpb_run, dd.hotG_bytes + 256, st));
+            if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+            const unsigned gx = static_cast<unsigned>(
+                std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 255) / 256, 64ull * dd.num_sms)));
+            acg::kern::sparseg_fix_kernel<<<gx, 256, 0, st>>>(ga, ew, ef, n_out_states);
+            ACG_CUDA(cudaGetLastError());
+            s->eargs = ef;  // E1 / E2 (and a regrowth's re-expansion) read the final events
+            s->launches += 2;
+        } else {
+            ACG_CUDA(flush_zeros(s, st));
+            ACG_CUDA(launch_event_walk(d.mode, s->U_run, a, s->eargs, g_ev, s->tpb_run, smem_bytes(dd), st));
+            ++s->launches;
+            if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
+        }
+        s->ev_run = true;
         const bool smem_bins = want_counts && static_cast<std::size_t>(n_out_states) * 4 <= kEventBinsMax;
         const unsigned g1 = static_cast<unsigned>(
             std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 15) / 16, 2ull * dd.num_sms)));
@@ -1400,7 +1481,7 @@ int scanner_sync(acg_scanner* s) {
         ACG_CUDA(cudaMemcpyAsync(s->pinned + 2, s->scalars64.p + 8, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         ACG_CUDA(cudaStreamSynchronize(st));
         const std::uint32_t used = static_cast<std::uint32_t>(s->pinned[1]);
-        if (used > s->eargs.pool_blocks) {  // the event pool overflowed: grow it and run again
+        if (used > s->walk_pool_blocks) {  // the walk's event pool overflowed: grow it and run again
             s->xev_min_pool = used + used / 4 + 1024;
             s->xev_n = 0;  // (no valid counts from this run: uniform slabs)
             ++s->replays;

@@ -612,6 +612,23 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
             }
         });
     }
+    // Truncated automaton for generic alphabets (SPARSE-G, exact_kernels.cuh):
+    // hotG = longest hot suffix of the target | 0x8000 when the true target is
+    // cold (BFS-ordered hot set only: closed under longest hot suffix).
+    d.hotG.clear();
+    if (d.mode == kAlphaGeneric && !(visits && visits->size() == S) && H <= 0x7FFF && H < S) {
+        d.hotG.assign(static_cast<std::size_t>(H) * K, 0);
+        parallel_for(H, 4096, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t i = lo; i < hi; ++i) {
+                for (std::uint32_t c = 0; c < K; ++c) {
+                    const std::uint32_t t = d.next[i * K + c];
+                    std::uint32_t h = d.nfa_of[t];
+                    while (d.dev_of[h] >= H) h = nfa.fail[h];
+                    d.hotG[i * K + c] = static_cast<std::uint16_t>(d.dev_of[h] | (t >= H ? 0x8000u : 0u));
+                }
+            }
+        });
+    }
     d.id_bits = 1;
     while ((1ull << d.id_bits) < nfa.n_patterns) ++d.id_bits;
     d.halo = (nfa.max_len + 15u) & ~15u;

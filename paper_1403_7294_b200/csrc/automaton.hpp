@@ -90,6 +90,9 @@ struct Dfa {
     // true target is cold or has outputs (the step must be replayed exactly).
     std::vector<std::uint16_t> hotH;     // H*K
     bool sparse_ok = false;
+    // Generic alphabets (SPARSE-G walk): H*K u16 = longest hot suffix of the
+    // target | 0x8000 when the true target is cold (empty = not available).
+    std::vector<std::uint16_t> hotG;
     std::vector<std::uint32_t> depth;    // S, device order
     std::vector<std::uint32_t> out_off;  // S+1 in device order
     std::vector<std::uint32_t> out_ids;  // ascending per state

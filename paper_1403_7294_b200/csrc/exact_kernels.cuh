@@ -266,6 +266,192 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_event_kerne
         if (act[u]) e.ev_count[cid[u]] = cnt[u];
 }
 
+// ====================================================== SPARSE-G (generic) ==
+// EXACT mode for generic alphabets without L2 lookups in the lockstep walk.
+// hotG[s*K + c] (s hot) = the longest suffix of s.c in the hot set H (a BFS
+// prefix, closed under "longest hot suffix") | kGCold when the TRUE target is
+// cold. Walking hotG from the root gives, at every position, the longest hot
+// suffix of the text, which IS the true state whenever the true state is hot.
+//  * KG sparseg_walk_kernel: the walk, all in shared memory. Logs, per chunk in
+//    position order: an output event for each owned step whose (hot) state has
+//    outputs, and an excursion event (walk offset, source state) for each step
+//    whose true target is cold (also in the halo: an excursion can run into
+//    the owned part).
+//  * XG sparseg_fix_kernel: one thread per chunk replays the chunk's events in
+//    order: an excursion walks the true DFA (L2) from its source state until
+//    the state is hot again, emitting the cold states' outputs; events inside
+//    an excursion (proxy outputs, spurious excursions) are dropped; the rest
+//    are exact. The result is the chunk's final event list in the format E1/E2
+//    take (owned offset << ob | output rank), in slabs of chunk + 1 slots
+//    (one event per owned byte at most).
+constexpr std::uint32_t kGCold = 0x8000u;
+
+template <int U>
+__global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) sparseg_walk_kernel(const ScanArgs a, const EventArgs e,
+                                                                                   std::uint32_t n_out) {
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    std::uint8_t* smap = smem + a.smem_table_bytes;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.hotH);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < a.smem_table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        for (std::uint32_t i = threadIdx.x; i < 256; i += blockDim.x) smap[i] = a.symmap[i];
+    }
+    __syncthreads();
+    const std::uint32_t hot_s = smem_u32(smem);
+    const long long G = gridDim.x;
+    long long cid[U];
+    bool act[U], live[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        cid[u] = (static_cast<long long>(threadIdx.x) * U + u) * G + blockIdx.x;
+        act[u] = cid[u] < a.n_chunks;
+        live[u] = act[u];
+    }
+    if (!act[0]) return;
+    const std::uint32_t K = a.K, Hn = a.Hn, nhot = a.H - a.Hn, ob = e.ob;
+    const long long halo = a.halo, steps = a.halo + a.chunk, n = a.n;
+    std::uint32_t* __restrict__ ev = e.ev;
+    std::uint32_t st[U], wr[U], lim[U], cnt[U];
+    long long pos0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        st[u] = 0;
+        cnt[u] = 0;
+        wr[u] = act[u] ? slab_start(e, cid[u]) : 0u;
+        lim[u] = act[u] ? slab_end(e, cid[u]) - 1u : 0u;
+        pos0[u] = a.emit_from + cid[u] * a.chunk - halo;
+    }
+    uint4 w[U];
+    auto load = [&](long long off) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = pos0[u] + off;
+            w[u] = (act[u] && p >= 0 && p < n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    const std::uint32_t kinc = 1u << ob;
+    load(0);
+    for (long long off = 0; off < steps; off += 16) {
+        uint4 cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = w[u];
+        if (off + 16 < steps) load(off + 16);
+        const bool owned_blk = off >= halo;
+        std::uint32_t wr0[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {  // two events per step at most: 32 free slots per block
+            if (live[u] && lim[u] - wr[u] < 32u) {
+                for (; wr[u] < lim[u]; ++wr[u], ++cnt[u]) ev[wr[u]] = kEvPad;
+                const uint2 g = ev_grow(ev, e.pool_used, e.pool_base, e.pool_blocks, lim[u]);
+                wr[u] = g.x;
+                lim[u] = g.y;
+                if (g.y == 0u) live[u] = false;
+            }
+            wr0[u] = wr[u];
+        }
+        bool fast = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = pos0[u] + off;
+            fast = fast && (!act[u] || (p >= 0 && p + 16 <= n));
+        }
+        std::uint32_t kk = static_cast<std::uint32_t>(off) << ob;
+        if (fast) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
+                    const std::uint32_t col = smap[__byte_perm(word, 0u, 0x4440u + (k & 3))];
+                    const std::uint32_t v = lds_u16z(hot_s + 2u * (st[u] * K + col));
+                    const std::uint32_t nx = v & 0x7FFFu, r = nx - Hn;
+                    if (live[u] && (v & kGCold)) ev[wr[u]++] = kk + n_out + st[u];
+                    if (owned_blk && live[u] && r < nhot) ev[wr[u]++] = kk + r;
+                    st[u] = nx;
+                }
+                kk += kinc;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!act[u]) continue;
+                std::uint32_t kq = kk;
+#pragma unroll 1
+                for (int k = 0; k < 16; ++k, kq += kinc) {
+                    const long long p = pos0[u] + off + k;
+                    const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
+                    const int c = (p >= 0 && p < n) ? column_of<1>((word >> (8 * (k & 3))) & 0xFFu, smap, a) : -1;
+                    std::uint32_t nx = 0;
+                    if (c >= 0) {
+                        const std::uint32_t v = lds_u16z(hot_s + 2u * (st[u] * K + static_cast<std::uint32_t>(c)));
+                        nx = v & 0x7FFFu;
+                        if (live[u] && (v & kGCold)) ev[wr[u]++] = kq + n_out + st[u];
+                    }
+                    const std::uint32_t r = nx - Hn;
+                    if (owned_blk && live[u] && r < nhot) ev[wr[u]++] = kq + r;
+                    st[u] = nx;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) cnt[u] += wr[u] - wr0[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (act[u]) e.ev_count[cid[u]] = cnt[u];
+}
+
+// XG: ew = the walk's events (walk offsets, payload < n_out: hot output rank;
+// >= n_out: excursion from hot state payload - n_out); ef = the final events.
+__global__ void __launch_bounds__(256) sparseg_fix_kernel(const ScanArgs a, const EventArgs ew, const EventArgs ef,
+                                                          std::uint32_t n_out) {
+    if (!ev_pool_ok(ew)) return;  // the walk's pool overflowed: the host replays the run
+    const std::uint32_t K = a.K, H = a.H, Hn = a.Hn, wob = ew.ob, fob = ef.ob;
+    const std::uint32_t wmask = (1u << wob) - 1u;
+    const long long halo = a.halo, steps = a.halo + a.chunk, n = a.n;
+    unsigned long long seen = 0;
+    for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; c < a.n_chunks;
+         c += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const std::uint32_t total = ew.ev_count[c];
+        seen += total;
+        const long long pos0 = a.emit_from + c * a.chunk - halo;
+        std::uint32_t p = slab_start(ew, c), lim = slab_end(ew, c) - 1u;
+        std::uint32_t out = static_cast<std::uint32_t>(c) * ef.ecap, o0 = out;
+        long long p_end = 0;  // walk offsets below this lie inside a replayed excursion
+        for (std::uint32_t i = 0; i < total; ++i) {
+            if (p == lim) {
+                p = ew.ev[lim];
+                lim = p + kEvBlock - 1;
+            }
+            const std::uint32_t v = __ldcs(ew.ev + p++);
+            if (v == kEvPad) continue;
+            const long long off = v >> wob;
+            if (off < p_end) continue;
+            const std::uint32_t pay = v & wmask;
+            if (pay < n_out) {  // a hot output state (exact: not inside an excursion)
+                ef.ev[out++] = (static_cast<std::uint32_t>(off - halo) << fob) | pay;
+                continue;
+            }
+            // excursion: the true DFA from the hot source state until the state is hot again
+            std::uint32_t x = pay - n_out;
+            long long o = off;
+            for (;;) {
+                const long long tp = pos0 + o;
+                const int col = (tp >= 0 && tp < n) ? column_of<1>(__ldg(a.text + tp), nullptr, a) : -1;
+                x = col < 0 ? 0u : __ldg(a.next + x * K + static_cast<std::uint32_t>(col));
+                if (x < H) break;  // hot again at o: the walk's events from o on are exact
+                if (o >= halo && x - Hn < a.Cn - Hn)
+                    ef.ev[out++] = (static_cast<std::uint32_t>(o - halo) << fob) | (x - Hn);
+                if (++o >= steps) break;
+            }
+            p_end = o;
+        }
+        ef.ev_count[c] = out - o0;
+    }
+    if (seen) atomicAdd(ew.ev_total, seen);  // the walk's events (size its next run's slabs)
+}
+
 // Per-chunk slab sizes for the next run from this run's event counts:
 // sizes[c] = cnt + cnt/8 + 17 (incl. the link slot); offs[0] = 0 (CUB prefixes
 // sizes into offs[1..]).
