@@ -213,6 +213,18 @@ int acg_scanner_format(acg_scanner* s, int format, uint64_t first, uint64_t coun
                        uint64_t* bytes);
 int acg_scanner_write_matches(acg_scanner* s, int format, int fd, uint64_t* bytes);
 
+/* ---- streamed host scan: the match list of a host text of any size handed
+ * to a callback window by window, in canonical order, while the next pieces
+ * are copied and scanned — for lists larger than host or device memory
+ * (cfg4: ~1.7e10 records per 4 GiB). format -1: packed records (count =
+ * records, end << *id_bits | id); ACG_FORMAT_TSV / _JSON: cmd_match's output
+ * (cli.hpp:58-76) formatted on the GPU (count = bytes; JSON framed across
+ * windows). The sink returns 0 to go on; anything else stops the scan
+ * (ACG_ERR_INVALID). Per-pattern counts into h_counts (NULL: none). */
+typedef int (*acg_sink)(void* user, const void* data, uint64_t count);
+int acg_scan_stream(const acg_automaton* a, int device, const uint8_t* h_text, uint64_t n, uint64_t piece_bytes,
+                    int format, acg_sink sink, void* user, uint64_t* h_counts, uint64_t* m_out, uint32_t* id_bits);
+
 /* ---- input path: replaces acmatch::load_input / load_patterns
  * (proj/include/acmatch/io.hpp:25-31, :37-65) --------------------------------
  * acg_load_input: the whole file as raw bytes in page-locked host memory

@@ -77,6 +77,8 @@ ACG_SYMBOLS = {
     "acg_partitioned_destroy": (None, [vp]),
     "acg_scanner_format": (C.c_int, [vp, C.c_int, C.c_uint64, C.c_uint64, vp, C.c_uint64, C.POINTER(C.c_uint64)]),
     "acg_scanner_write_matches": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
+    "acg_scan_stream": (C.c_int, [vp, C.c_int, vp, C.c_uint64, C.c_uint64, C.c_int, vp, vp, vp,
+                                  C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]),
     "acg_load_input": (C.c_int, [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_uint64)]),
     "acg_load_patterns": (C.c_int, [C.c_char_p, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_uint32),
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -557,3 +557,41 @@ def run_partitioned(patterns: Sequence[Pattern], input, worker_count: int, devic
                               ids, ends)
     finally:
         L.acg_partitioned_destroy(h)
+
+
+_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+def scan_stream(a: Automaton, text, consume, fmt: str | None = None, device: int = 0, piece_bytes: int = 0,
+                counts: bool = False):
+    """acg_scan_stream: the match list handed window by window to `consume`
+    (packed uint64 records and id_bits when fmt is None, else the TSV / JSON
+    bytes of cmd_match's output); consume returns a truthy value to stop.
+    Returns (m, per-pattern counts or None)."""
+    arr = text.array if isinstance(text, PinnedInput) else _as_u8(text)
+    f = {None: -1, "tsv": FORMAT_TSV, "json": FORMAT_JSON}[fmt]
+    ib_holder = [a.pattern_count()]
+    ib = 1
+    while (1 << ib) < ib_holder[0]:
+        ib += 1
+
+    def sink(_user, data, count):
+        try:
+            if f < 0:
+                view = np.ctypeslib.as_array(C.cast(data, C.POINTER(C.c_uint64)), shape=(count,)) if count else \
+                    np.zeros(0, np.uint64)
+                stop = consume(view, ib)
+            else:
+                stop = consume(C.string_at(data, count))
+            return 1 if stop else 0
+        except Exception:
+            return 1
+
+    cb = _SINK(sink)
+    cnt = np.zeros(a.pattern_count(), np.uint64) if counts else None
+    m, idb = C.c_uint64(), C.c_uint32()
+    _check(_lib.acg().acg_scan_stream(a.handle, device, arr.ctypes.data_as(C.c_void_p) if arr.size else None, arr.size,
+                                      piece_bytes, f, C.cast(cb, C.c_void_p), None,
+                                      cnt.ctypes.data_as(C.c_void_p) if cnt is not None else None,
+                                      C.byref(m), C.byref(idb)))
+    return m.value, cnt

@@ -1763,13 +1763,16 @@ cudaError_t format_tables(const acg_automaton* a, DeviceDfa& dd, int json, cudaS
 }
 
 // Formats records [first, first + count) of the synced list into s->fmt_out
-// (device); *bytes = their text size.
-int format_window(acg_scanner* s, int json, std::uint64_t first, std::uint64_t count, std::uint64_t* bytes) {
+// (device); *bytes = their text size. JSON framing: "[" before the window's
+// first record when open, "]\n" after its last when close (else ","); by
+// default (open/close < 0) the window's place in this scanner's list decides.
+int format_window(acg_scanner* s, int json, std::uint64_t first, std::uint64_t count, std::uint64_t* bytes,
+                  int open = -1, int close = -1) {
     using namespace acg::kern;
     DeviceDfa& dd = *s->dd;
     cudaStream_t st = s->last;
     *bytes = 0;
-    if (json && s->m_total == 0) {  // "[]\n"
+    if (json && s->m_total == 0 && open < 0) {
         ACG_CUDA(s->fmt_out.reserve(3, st));
         ACG_CUDA(cudaMemcpyAsync(s->fmt_out.p, "[]\n", 3, cudaMemcpyHostToDevice, st));
         ACG_CUDA(cudaStreamSynchronize(st));
@@ -1787,8 +1790,8 @@ int format_window(acg_scanner* s, int json, std::uint64_t first, std::uint64_t c
     f.str = dd.fmt_str[json].p;
     f.str_off = dd.fmt_off[json].p;
     f.json = json;
-    f.open = first == 0;
-    f.close = first + count == s->m_total;
+    f.open = open >= 0 ? open : first == 0;
+    f.close = close >= 0 ? close : first + count == s->m_total;
     f.tile_sum = s->fmt_tiles.p;
     f.tile_off = s->fmt_tiles.p + tiles;
     const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(tiles, 16ull * dd.num_sms));
@@ -1828,6 +1831,31 @@ __attribute__((visibility("hidden"))) int acg_internal_scanner_take(const acg_au
 }
 __attribute__((visibility("hidden"))) void acg_internal_scanner_give(acg_scanner* s) { pool_give(s); }
 __attribute__((visibility("hidden"))) void* acg_internal_scanner_stream(acg_scanner* s) { return s->stream; }
+// records [first, first+count) of the synced list formatted with explicit JSON
+// framing, copied to host (host_io.cpp's streamed scan)
+__attribute__((visibility("hidden"))) int acg_internal_format(acg_scanner* s, int json, std::uint64_t first,
+                                                              std::uint64_t count, int open, int close,
+                                                              std::uint8_t* host, std::uint64_t cap,
+                                                              std::uint64_t* bytes) {
+    if (const int rc = scanner_sync(s)) return rc;
+    if (const int rc = format_window(s, json, first, count, bytes, open, close)) return rc;
+    if (!host) return ACG_OK;  // the text stays in the scanner's output buffer (acg_internal_fetch)
+    if (*bytes > cap) return fail(ACG_ERR_INVALID, "output staging smaller than the formatted window");
+    if (*bytes) {
+        ACG_CUDA(cudaMemcpyAsync(host, s->fmt_out.p, *bytes, cudaMemcpyDeviceToHost, s->last));
+        ACG_CUDA(cudaStreamSynchronize(s->last));
+    }
+    return ACG_OK;
+}
+// the last acg_internal_format's text (bytes of it) to host
+__attribute__((visibility("hidden"))) int acg_internal_fetch(acg_scanner* s, std::uint8_t* host, std::uint64_t bytes) {
+    if (bytes > s->fmt_out.n) return fail(ACG_ERR_INVALID, "nothing formatted");
+    if (bytes) {
+        ACG_CUDA(cudaMemcpyAsync(host, s->fmt_out.p, bytes, cudaMemcpyDeviceToHost, s->last));
+        ACG_CUDA(cudaStreamSynchronize(s->last));
+    }
+    return ACG_OK;
+}
 
 // (host_io.cpp reports its errors through this; not part of include/acg.h)
 __attribute__((visibility("hidden"))) int acg_internal_set_error(int code, const char* msg) { return fail(code, msg); }

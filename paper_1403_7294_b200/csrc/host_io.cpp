@@ -26,6 +26,7 @@
 #include <cerrno>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <string_view>
 #include <thread>
@@ -39,6 +40,11 @@ extern "C" __attribute__((visibility("hidden"))) int acg_internal_scanner_take(c
                                                                                uint32_t flags, acg_scanner** out);
 extern "C" __attribute__((visibility("hidden"))) void acg_internal_scanner_give(acg_scanner* s);
 extern "C" __attribute__((visibility("hidden"))) void* acg_internal_scanner_stream(acg_scanner* s);  // its own stream
+// GPU-formatted window with explicit JSON framing, copied to host (acg_device.cu)
+extern "C" __attribute__((visibility("hidden"))) int acg_internal_format(acg_scanner* s, int json, uint64_t first,
+                                                                         uint64_t count, int open, int close,
+                                                                         uint8_t* host, uint64_t cap, uint64_t* bytes);
+extern "C" __attribute__((visibility("hidden"))) int acg_internal_fetch(acg_scanner* s, uint8_t* host, uint64_t bytes);
 constexpr uint32_t kPipelineTag = 0x100u;  // pool key bit: pipeline lanes keep their own adaptive state
 
 namespace {
@@ -190,14 +196,21 @@ int acg_load_patterns(const char* path, uint8_t** concat, uint64_t** offsets, ui
     return ACG_OK;
 }
 
-int acg_scan_pipelined(const acg_automaton* a, int device, const uint8_t* h_text, uint64_t n, uint64_t emit_from,
-                       uint64_t base_offset, uint64_t piece_bytes, uint32_t flags, uint64_t* h_packed, uint64_t cap,
-                       uint64_t* h_counts, uint64_t* m_out, uint32_t* id_bits, uint64_t* failure_follows) {
+}  // extern "C"
+
+namespace {
+
+// The pipeline of acg_scan_pipelined / acg_scan_stream: pieces alternate
+// between two pooled scanners; on_piece(scanner, piece matches, matches
+// before the piece) consumes each synced piece in text order.
+int run_pipeline(const acg_automaton* a, int device, const uint8_t* h_text, uint64_t n, uint64_t emit_from,
+                 uint64_t base_offset, uint64_t piece_bytes, uint32_t flags, bool want_list, uint64_t* h_counts,
+                 uint64_t* failure_follows, const std::function<int(acg_scanner*, uint64_t, uint64_t)>& on_piece,
+                 uint64_t* m_out) {
     if (!a || (!h_text && n) || !m_out) return acg_internal_set_error(ACG_ERR_INVALID, "null argument");
     if (emit_from > n || (emit_from & 15)) return acg_internal_set_error(ACG_ERR_INVALID, "emit_from must be a multiple of 16 inside the text");
     *m_out = 0;
     if (failure_follows) *failure_follows = 0;
-    const bool want_list = h_packed != nullptr;
     const std::uint32_t P = acg_pattern_count(a);
     if (h_counts) std::fill(h_counts, h_counts + P, 0ull);
     std::uint32_t halo = 0;
@@ -219,7 +232,6 @@ int acg_scan_pipelined(const acg_automaton* a, int device, const uint8_t* h_text
         std::uint8_t* d = nullptr;
         std::uint8_t* stage = nullptr;  // pinned staging (pageable input)
         std::uint64_t lo = 0, hi = 0;   // owned text range of the piece in flight
-        bool busy = false;
     } lane[2];
     std::vector<std::uint64_t> piece_counts(h_counts ? P : 0);
     std::uint64_t m = 0;
@@ -268,24 +280,19 @@ int acg_scan_pipelined(const acg_automaton* a, int device, const uint8_t* h_text
             src = l.stage;
         }
         if (cudaError_t e = cudaMemcpyAsync(l.d, src, len, cudaMemcpyHostToDevice, l.st)) return cuda_fail(e);
-        l.busy = true;
         return acg_scanner_run(l.s, l.d, len, ctx, base_offset + (l.lo - ctx), l.st);
     };
-    // drain piece held by lane i: its records to h_packed[m..], counts, follows
+    // drain the piece a lane holds: its records (on_piece), counts, follows
     auto drain = [&](Lane& l) -> int {
         if (int r = acg_scanner_sync(l.s)) return r;
         const std::uint64_t pm = acg_scanner_match_count(l.s);
-        if (want_list && m < cap && pm) {
-            const std::uint64_t take = std::min(pm, cap - m);
-            if (int r = acg_scanner_copy_records(l.s, 0, take, h_packed + m)) return r;
-        }
+        if (int r = on_piece(l.s, pm, m)) return r;
         if (h_counts) {
             if (int r = acg_scanner_pattern_counts(l.s, piece_counts.data())) return r;
             for (std::uint32_t p = 0; p < P; ++p) h_counts[p] += piece_counts[p];
         }
         if (failure_follows && (flags & ACG_SCAN_STATS)) *failure_follows += acg_scanner_failure_follows(l.s);
         m += pm;
-        l.busy = false;
         if (!pinned) cudaStreamSynchronize(l.st);  // the staging buffer is free again
         return ACG_OK;
     };
@@ -294,14 +301,111 @@ int acg_scan_pipelined(const acg_automaton* a, int device, const uint8_t* h_text
         rc = drain(lane[k % 2]);
         if (!rc && k + 2 < pieces) rc = enqueue(k + 2);
     }
-    if (!rc && id_bits) {  // id bits of the packed records (automaton.cpp: compile_dfa)
-        std::uint32_t ib = 1;
-        while ((1ull << ib) < P) ++ib;
-        *id_bits = ib;
-    }
     cleanup();
     if (!rc) *m_out = m;
     return rc;
+}
+
+std::uint32_t id_bits_of(const acg_automaton* a) {  // (automaton.cpp: compile_dfa)
+    const std::uint32_t P = acg_pattern_count(a);
+    std::uint32_t ib = 1;
+    while ((1ull << ib) < P) ++ib;
+    return ib;
+}
+
+}  // namespace
+
+extern "C" {
+
+int acg_scan_pipelined(const acg_automaton* a, int device, const uint8_t* h_text, uint64_t n, uint64_t emit_from,
+                       uint64_t base_offset, uint64_t piece_bytes, uint32_t flags, uint64_t* h_packed, uint64_t cap,
+                       uint64_t* h_counts, uint64_t* m_out, uint32_t* id_bits, uint64_t* failure_follows) {
+    const bool want_list = h_packed != nullptr;
+    const int rc = run_pipeline(
+        a, device, h_text, n, emit_from, base_offset, piece_bytes, flags, want_list, h_counts, failure_follows,
+        [&](acg_scanner* s, std::uint64_t pm, std::uint64_t m) -> int {
+            if (!want_list || m >= cap || !pm) return ACG_OK;
+            return acg_scanner_copy_records(s, 0, std::min(pm, cap - m), h_packed + m);
+        },
+        m_out);
+    if (!rc && id_bits) *id_bits = id_bits_of(a);
+    return rc;
+}
+
+int acg_scan_stream(const acg_automaton* a, int device, const uint8_t* h_text, uint64_t n, uint64_t piece_bytes,
+                    int format, acg_sink sink, void* user, uint64_t* h_counts, uint64_t* m_out, uint32_t* id_bits) {
+    if (!sink) return acg_internal_set_error(ACG_ERR_INVALID, "null sink");
+    if (format != -1 && format != ACG_FORMAT_TSV && format != ACG_FORMAT_JSON)
+        return acg_internal_set_error(ACG_ERR_INVALID, "unknown output format");
+    constexpr std::uint64_t kWindow = 1ull << 24;  // records per window handed to the sink
+    const bool json = format == ACG_FORMAT_JSON;
+    // page-locked staging: two windows (JSON holds the last one back: its final
+    // "," becomes "]" once the stream's end is known)
+    std::uint8_t* buf[2] = {nullptr, nullptr};
+    std::uint64_t cap[2] = {0, 0}, held = 0;
+    int hb = -1;  // buffer holding a window not yet handed over (JSON)
+    auto grow = [&](int i, std::uint64_t need) -> int {
+        if (need <= cap[i]) return ACG_OK;
+        if (buf[i]) cudaFreeHost(buf[i]);
+        cap[i] = need + need / 8;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&buf[i]), cap[i], cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            buf[i] = nullptr;
+            cap[i] = 0;
+            return acg_internal_set_error(ACG_ERR_OUT_OF_MEMORY, "pinned staging allocation failed");
+        }
+        return ACG_OK;
+    };
+    int next = 0;
+    const int rc = run_pipeline(
+        a, device, h_text, n, 0, 0, piece_bytes, 0, true, h_counts, nullptr,
+        [&](acg_scanner* s, std::uint64_t pm, std::uint64_t m) -> int {
+            for (std::uint64_t first = 0; first < pm; first += kWindow) {
+                const std::uint64_t count = std::min(kWindow, pm - first);
+                if (format < 0) {
+                    if (int r = grow(0, count * 8)) return r;
+                    if (int r = acg_scanner_copy_records(s, first, count, reinterpret_cast<std::uint64_t*>(buf[0])))
+                        return r;
+                    if (sink(user, buf[0], count)) return acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
+                    continue;
+                }
+                std::uint64_t nb = 0;
+                const int open = json && m + first == 0;
+                if (int r = acg_internal_format(s, json, first, count, open, 0, nullptr, 0, &nb)) return r;
+                if (int r = grow(next, nb)) return r;
+                if (int r = acg_internal_fetch(s, buf[next], nb)) return r;
+                if (!json) {
+                    if (nb && sink(user, buf[next], nb)) return acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
+                    continue;
+                }
+                if (hb >= 0 && sink(user, buf[hb], held)) return acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
+                hb = next;
+                held = nb;
+                next ^= 1;
+            }
+            return ACG_OK;
+        },
+        m_out);
+    int out = rc;
+    if (!out && json) {
+        if (hb < 0) {
+            static const std::uint8_t empty[] = {'[', ']', '\n'};
+            if (sink(user, empty, 3)) out = acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
+        } else {
+            // the last record's "," closes the list
+            if (grow(hb, held + 1) == ACG_OK) {
+                buf[hb][held - 1] = ']';
+                buf[hb][held] = '\n';
+                if (sink(user, buf[hb], held + 1)) out = acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
+            } else {
+                out = ACG_ERR_OUT_OF_MEMORY;
+            }
+        }
+    }
+    for (auto* b : buf)
+        if (b) cudaFreeHost(b);
+    if (!out && id_bits) *id_bits = id_bits_of(a);
+    return out;
 }
 
 }  // extern "C"

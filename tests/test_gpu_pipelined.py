@@ -82,3 +82,38 @@ def test_file_loaders_feed_the_pipelined_scan(tmp_path):
     oi, oe, _, cnt = oracle.OracleAutomaton(concat, offs).scan(text, counts=True)
     ids, ends = unpack(recs, ib)
     assert np.array_equal(ends, oe) and np.array_equal(ids, oi) and np.array_equal(counts, cnt)
+
+
+@pytest.mark.parametrize("fmt", [None, "tsv", "json"])
+@pytest.mark.parametrize("piece", [1 << 16, 0])
+def test_streamed_scan_equals_the_whole_list(fmt, piece):
+    """acg_scan_stream: windows handed to a callback in canonical order; their
+    concatenation is the whole list (packed records) or the whole cmd_match
+    output (TSV / JSON framed across windows), for any piece size."""
+    w = synth.CONFIGS[3].scaled(1 << 20, 400)
+    text = synth.text(w)
+    concat, offs = synth.patterns(w)
+    a = am.Automaton.from_arrays(concat, offs)
+    got = []
+    m, counts = am.scan_stream(a, text, lambda *x: got.append(x[0].copy() if fmt is None else x[0]) and False,
+                               fmt=fmt, piece_bytes=piece, counts=True)
+    s = am.Scanner(a, 0, am.SCAN_LIST | am.SCAN_COUNTS)
+    s.run_host(text)
+    assert m == s.match_count() and np.array_equal(counts, s.pattern_counts())
+    if fmt is None:
+        packed, _ = s.packed_records()
+        assert np.array_equal(np.concatenate(got) if got else np.zeros(0, np.uint64), packed)
+    else:
+        assert b"".join(got) == s.format(fmt)
+
+
+def test_streamed_scan_empty_list_and_stop():
+    concat, offs = synth.pack_patterns([b"ZZZZ"])
+    a = am.Automaton.from_arrays(concat, offs)
+    got = []
+    m, _ = am.scan_stream(a, b"ACGT" * 1000, lambda b: got.append(b) and False, fmt="json")
+    assert m == 0 and b"".join(got) == b"[]\n"
+    w = synth.CONFIGS[3].scaled(1 << 20, 400)
+    a2 = am.Automaton.from_arrays(*synth.patterns(w))
+    with pytest.raises(am.Error):
+        am.scan_stream(a2, synth.text(w), lambda *x: True, piece_bytes=1 << 16)  # the sink stops the scan
