@@ -257,8 +257,11 @@ class RefAutomaton:
         return cls(*pack(words))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            ref().ref_free(self._h)
+        try:
+            if getattr(self, "_h", None):
+                ref().ref_free(self._h)
+        except TypeError:  # interpreter shutdown: module globals already torn down
+            pass
 
     def state_count(self) -> int:
         return ref().ref_state_count(self._h)
