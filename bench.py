@@ -276,6 +276,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-piece-mib", type=int, default=256, help="pipelined e2e scan: piece size (MiB)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="tests only: gloo runs the N-rank logic with ranks sharing GPUs")
     ap.add_argument("--streams-per-thread", type=int, default=0)
     ap.add_argument("--threads-per-block", type=int, default=0)
     ap.add_argument("--chunk-bytes", type=int, default=0)
@@ -302,9 +304,14 @@ def main() -> None:
     from paper_1403_7294_b200 import shards
 
     rank, world, local = dist_env()
+    if args.dist_backend == "gloo":  # logic test of the N-rank path on fewer GPUs (tests only; never a bench line)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     scaling = scaling_of(args)
 
     am.version()  # load libacg (and its CUDA driver init) outside the build timing

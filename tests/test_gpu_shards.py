@@ -104,3 +104,28 @@ def test_two_ranks_one_gpu_cfg0_full_golden(tmp_path):
         dsum = int(np.sum(z, dtype=np.uint64))
     dxor = int(np.bitwise_xor.reduce(z))
     assert (dsum, dxor) == (case["dsum"], case["dxor"])
+
+
+def test_bench_two_ranks_strong_split_on_one_gpu():
+    """bench.py's N-rank path (shards, counts all-reduced inside the timed step,
+    max-over-ranks timing, the whole job's count/digest/order checks, the
+    pipelined e2e leg per shard) with 2 ranks over gloo sharing cuda:0: a
+    strong split of cfg2 at 64 MiB must give the same job result as 1 rank."""
+    import subprocess
+    import sys
+    base = [sys.executable, "bench.py", "--config", "2", "--text-mib", "64", "--steps", "2", "--warmup", "3",
+            "--no-cpu-baseline", "--e2e-steps", "1"]
+    one = subprocess.run(base, capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert one.returncode == 0, one.stderr[-3000:]
+    port = _free_port()
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port)] + base[1:] +
+                         ["--gpus", "2", "--dist-backend", "gloo"], capture_output=True, text=True, cwd=ROOT,
+                         timeout=900)
+    assert two.returncode == 0, two.stderr[-3000:]
+    j1 = json.loads(one.stdout.strip().splitlines()[-1])
+    j2 = json.loads(two.stdout.strip().splitlines()[-1])
+    assert j2["n_gpus"] == 2 and j2["scaling"] == "strong"
+    for k in ("matches", "digest_sum", "digest_xor", "count_sum"):
+        assert j2["check"][k] == j1["check"][k], k
+    assert j2["check"]["unsorted_pairs"] == 0 and j2["check"]["timed_runs_replayed"] == 0
