@@ -347,7 +347,7 @@ int acg_scan_stream(const acg_automaton* a, int device, const uint8_t* h_text, u
     auto grow = [&](int i, std::uint64_t need) -> int {
         if (need <= cap[i]) return ACG_OK;
         if (buf[i]) cudaFreeHost(buf[i]);
-        cap[i] = need + need / 8;
+        cap[i] = need + need / 8 + 16;  // (+16: the held JSON window's closing "]\n" always fits in place)
         if (cudaHostAlloc(reinterpret_cast<void**>(&buf[i]), cap[i], cudaHostAllocDefault) != cudaSuccess) {
             cudaGetLastError();
             buf[i] = nullptr;
@@ -392,14 +392,10 @@ int acg_scan_stream(const acg_automaton* a, int device, const uint8_t* h_text, u
             static const std::uint8_t empty[] = {'[', ']', '\n'};
             if (sink(user, empty, 3)) out = acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
         } else {
-            // the last record's "," closes the list
-            if (grow(hb, held + 1) == ACG_OK) {
-                buf[hb][held - 1] = ']';
-                buf[hb][held] = '\n';
-                if (sink(user, buf[hb], held + 1)) out = acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
-            } else {
-                out = ACG_ERR_OUT_OF_MEMORY;
-            }
+            // the last record's "," closes the list (cap >= held + 16: room for the "\n")
+            buf[hb][held - 1] = ']';
+            buf[hb][held] = '\n';
+            if (sink(user, buf[hb], held + 1)) out = acg_internal_set_error(ACG_ERR_INVALID, "sink stopped the scan");
         }
     }
     for (auto* b : buf)
