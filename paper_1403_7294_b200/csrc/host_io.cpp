@@ -45,6 +45,9 @@ extern "C" __attribute__((visibility("hidden"))) int acg_internal_format(acg_sca
                                                                          uint64_t count, int open, int close,
                                                                          uint8_t* host, uint64_t cap, uint64_t* bytes);
 extern "C" __attribute__((visibility("hidden"))) int acg_internal_fetch(acg_scanner* s, uint8_t* host, uint64_t bytes);
+// profile-guided hot rows from the text on a generic-alphabet automaton's first scan (acg_device.cu)
+extern "C" __attribute__((visibility("hidden"))) void acg_internal_auto_layout(acg_automaton* a, const uint8_t* text,
+                                                                               uint64_t n);
 constexpr uint32_t kPipelineTag = 0x100u;  // pool key bit: pipeline lanes keep their own adaptive state
 
 namespace {
@@ -225,6 +228,7 @@ int run_pipeline(const acg_automaton* a, int device, const uint8_t* h_text, uint
     int rc = cudaSetDevice(device) == cudaSuccess ? ACG_OK : acg_internal_set_error(ACG_ERR_NO_DEVICE, "bad device");
     if (rc) return rc;
     const bool pinned = owned && is_pinned(h_text);
+    acg_internal_auto_layout(const_cast<acg_automaton*>(a), h_text + emit_from, owned);
 
     struct Lane {
         acg_scanner* s = nullptr;

@@ -188,6 +188,7 @@ int acg_run_partitioned(const uint8_t* concat, const uint64_t* offsets, uint32_t
         w.rc = acg_build(concat ? concat + offsets[w.start] : nullptr, loff.data(), w.len, &w.a);
         const auto s0 = clock::now();
         w.build_s = std::chrono::duration<double>(s0 - b0).count();
+        if (!w.rc) acg_internal_auto_layout(w.a, text, n);
         if (!w.rc) w.rc = cudaSetDevice(device) == cudaSuccess ? ACG_OK : ACG_ERR_CUDA;
         if (!w.rc) w.rc = acg_scanner_create(w.a, device, ACG_SCAN_LIST, &w.s);
         if (!w.rc && (cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking) != cudaSuccess ||
