@@ -1284,16 +1284,21 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
         }
         s->ev_run = true;
-        const bool smem_bins = want_counts && static_cast<std::size_t>(n_out_states) * 4 <= kEventBinsMax;
+        const std::size_t nb4 = static_cast<std::size_t>(n_out_states) * 4, nb1 = (n_out_states + 15u) & ~15u;
+        const bool smem_bins = want_counts && nb4 <= kEventBinsMax;
+        const bool smem_nout = (smem_bins ? nb4 : 0) + nb1 <= kEventBinsMax;
+        const std::size_t e1_smem = (smem_bins ? nb4 : 0) + (smem_nout ? nb1 : 0);
         const unsigned g1 = static_cast<unsigned>(
             std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 15) / 16, 2ull * dd.num_sms)));
-        if (smem_bins) {
-            auto k = acg::kern::event_count_kernel<true>;
-            ACG_CUDA(prepare_smem(k, static_cast<std::size_t>(n_out_states) * 4));
-            k<<<g1, 512, static_cast<std::size_t>(n_out_states) * 4, st>>>(a, s->eargs);
-        } else {
-            acg::kern::event_count_kernel<false><<<g1, 512, 0, st>>>(a, s->eargs);
-        }
+        auto e1 = [&](auto k) -> cudaError_t {
+            if (cudaError_t err = prepare_smem(k, e1_smem)) return err;
+            k<<<g1, 512, e1_smem, st>>>(a, s->eargs);
+            return cudaGetLastError();
+        };
+        if (smem_bins && smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<true, true>));
+        else if (smem_bins) ACG_CUDA(e1(acg::kern::event_count_kernel<true, false>));
+        else if (smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<false, true>));
+        else ACG_CUDA(e1(acg::kern::event_count_kernel<false, false>));
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
     } else {

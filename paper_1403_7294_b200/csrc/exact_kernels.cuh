@@ -496,13 +496,18 @@ __device__ __forceinline__ std::uint32_t n_out_of(std::uint32_t s, unsigned long
 // ===================================================================== E1 ==
 // One warp per chunk: records per chunk (-> chunk_counts, u64 for the CUB
 // prefix) and visits per output rank (shared-memory bins when they fit).
-template <bool SMEM_BINS>
+// (SMEM_NOUT: each output state's output count, as a byte (255 = look it up),
+// staged after the bins: the events' record counts need no L2 lookups)
+template <bool SMEM_BINS, bool SMEM_NOUT>
 __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, const EventArgs e) {
     extern __shared__ std::uint32_t bins[];
-    if (SMEM_BINS) {
+    std::uint8_t* nout8 = reinterpret_cast<std::uint8_t*>(bins + (SMEM_BINS ? e.n_out : 0u));
+    if (SMEM_BINS)
         for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x) bins[i] = 0;
-        __syncthreads();
-    }
+    if (SMEM_NOUT)
+        for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x)
+            nout8[i] = static_cast<std::uint8_t>(__ldg(a.outinfo + a.Hn + i) >> 32);
+    if (SMEM_BINS || SMEM_NOUT) __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long wpb = blockDim.x >> 5;
     const long long warps = static_cast<long long>(gridDim.x) * wpb;
@@ -519,7 +524,9 @@ __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, cons
                 if (!ok || v == kEvPad) return;
                 const std::uint32_t r = v & rmask;
                 const std::uint32_t s = state_of_rank(r, H, Hn, Cn);
-                recs += n_out_of(s, __ldg(a.outinfo + s), a);
+                std::uint32_t no = SMEM_NOUT ? nout8[r] : 255u;
+                if (no == 255u) no = n_out_of(s, __ldg(a.outinfo + s), a);
+                recs += no;
                 if (visits) {
                     if (SMEM_BINS) atomicAdd(&bins[r], 1u);
                     else atomicAdd(a.visits + r, 1ull);
