@@ -609,19 +609,20 @@ bool qfilter_fused(const ScanArgs& a) {
 // griddepcontrol.wait before reading them): hides launch latency between the
 // filter pipeline's stages. ACG_PDL=0 launches plainly.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned threads, cudaStream_t st, Args&&... args) {
+cudaError_t launch_pdl_smem(void (*k)(KArgs...), unsigned grid, unsigned threads, std::size_t smem, cudaStream_t st,
+                            Args&&... args) {
     static const bool on = [] {
         const char* e = std::getenv("ACG_PDL");
         return !(e && e[0] == '0');
     }();
     if (!on) {
-        k<<<grid, threads, 0, st>>>(std::forward<Args>(args)...);
+        k<<<grid, threads, smem, st>>>(std::forward<Args>(args)...);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -630,13 +631,17 @@ cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned threads, cud
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned threads, cudaStream_t st, Args&&... args) {
+    return launch_pdl_smem(k, grid, threads, 0, st, std::forward<Args>(args)...);
+}
 
 template <typename Kern>
 cudaError_t launch_q(Kern k, const ScanArgs& a, unsigned threads, std::size_t smem, int sms, cudaStream_t st) {
     cudaError_t e = prepare_smem(k, smem);
     if (e != cudaSuccess) return e;
-    k<<<sms, threads, smem, st>>>(a);
-    return cudaGetLastError();
+    // programmatic: KQ stages its Bloom filter while the previous kernel drains
+    return launch_pdl_smem(k, static_cast<unsigned>(sms), threads, smem, st, a);
 }
 cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
     using namespace acg::kern;
@@ -819,14 +824,16 @@ cudaError_t flush_zeros(acg_scanner* s, cudaStream_t st) {
         zl.words[i] = z.second / 4;
         if (++i == acg::kern::ZeroList::kMax) {
             zl.n = static_cast<int>(i);
-            acg::kern::zero_regions_kernel<<<128, 256, 0, st>>>(zl);
+            e = launch_pdl(acg::kern::zero_regions_kernel, 128, 256, st, zl);
+            if (e != cudaSuccess) return e;
             ++s->launches;
             i = 0;
         }
     }
     if (e == cudaSuccess && i) {
         zl.n = static_cast<int>(i);
-        acg::kern::zero_regions_kernel<<<128, 256, 0, st>>>(zl);
+        e = launch_pdl(acg::kern::zero_regions_kernel, 128, 256, st, zl);
+        if (e != cudaSuccess) return e;
         ++s->launches;
     }
     s->zeros.clear();

@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_ke
         if (threadIdx.x < NW) wcnt[threadIdx.x] = pub[threadIdx.x] = 0;
         if (threadIdx.x == 0) nfin = 0;
     }
+    pdl_wait();  // (launched programmatically: the filter is staged; the workspace is ours from here)
     __syncthreads();
     if (FUSED && (threadIdx.x >> 5) == NW) {  // the consumer warp
         qfilter_consume<NW>(a, pub, done_sh, &nfin);

@@ -1309,6 +1309,8 @@ struct ZeroList {
     int n;
 };
 __global__ void __launch_bounds__(256) zero_regions_kernel(const ZeroList zl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // (may be launched programmatically)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * 256;
     for (int r = 0; r < zl.n; ++r)
         for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * 256 + threadIdx.x; i < zl.words[r];
