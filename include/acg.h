@@ -155,6 +155,10 @@ int acg_scanner_set_mode(acg_scanner* s, int mode);
  * rate: sparse, excursion events per walked byte; filter, passing samples per
  * text byte (-1 before the first sync of that mode). */
 int acg_scanner_last_mode(acg_scanner* s, double* event_rate);
+/* Which walk kernel the last EXACT run used (diagnostics): 0 = the dense hot
+ * rows (KE, or the inline-emission walk), 1 = the compressed hot automaton
+ * (KC, csrc/ctab.hpp), 2 = SPARSE-G; -1 for a null scanner. */
+int acg_scanner_last_walk(const acg_scanner* s);
 /* Copies the P per-pattern counts (u64) into a caller device buffer, enqueued
  * on `stream` (NULL = the stream of the last run) — e.g. for an NCCL all-reduce.
  * Enqueued without a host wait: if the run is later replayed at sync (an
@@ -174,6 +178,17 @@ int acg_automaton_filter_info(const acg_automaton* a, uint32_t* q, double* pass_
 /* Device layout of the automaton (diagnostics): states, hot rows in smem, columns. */
 int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* hot_rows, uint32_t* columns,
                          uint32_t* halo, int* alphabet_mode);
+
+/* Compressed hot automaton of the EXACT walk (diagnostics; host only, no
+ * device needed): info = {slots, default depth D, hot states, exception
+ * entries}; when `text` is given, walks it on the host both with the dense
+ * transition table and with the compressed tables exactly as the device walk
+ * (KC) does, and returns in *mismatches the positions where the two states
+ * differ (0 = the compressed automaton is exact on this text) and in
+ * *cold_steps the steps taken from cold state words. Returns 1 when the
+ * automaton has a compressed table, 0 when the scheme does not apply. */
+int acg_automaton_ctab_check(const acg_automaton* a, const uint8_t* text, uint64_t n, uint32_t* info,
+                             uint64_t* mismatches, uint64_t* cold_steps);
 
 /* ---- the paper's dictionary-partitioned run, GPU-native: replaces
  * acmatch::run_partitioned + split_patterns + merge_matches

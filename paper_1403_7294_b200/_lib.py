@@ -64,8 +64,10 @@ ACG_SYMBOLS = {
     "acg_scanner_set_mode": (C.c_int, [vp, C.c_int]),
     "acg_scanner_set_profiling": (C.c_int, [vp, C.c_int]),
     "acg_scanner_last_mode": (C.c_int, [vp, C.POINTER(C.c_double)]),
+    "acg_scanner_last_walk": (C.c_int, [vp]),
     "acg_automaton_layout": (C.c_int, [vp, u32p, u32p, u32p, u32p, C.POINTER(C.c_int)]),
     "acg_automaton_filter_info": (C.c_int, [vp, u32p, C.POINTER(C.c_double)]),
+    "acg_automaton_ctab_check": (C.c_int, [vp, vp, C.c_uint64, u32p, u64p, u64p]),
     "acg_scanner_set_geometry": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint64]),
     "acg_run_partitioned": (C.c_int, [vp, vp, C.c_uint32, vp, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(vp)]),
     "acg_partitioned_match_count": (C.c_uint64, [vp]),

@@ -202,6 +202,17 @@ class Automaton:
         ok = _lib.acg().acg_automaton_filter_info(self._h, C.byref(q), C.byref(fp))
         return {"eligible": bool(ok), "q": q.value, "pass_rate": fp.value}
 
+    def ctab_check(self, text=None) -> dict:
+        """Compressed hot automaton (csrc/ctab.hpp): its geometry and, with a
+        text, the host replay of the device walk against the dense table."""
+        info = (C.c_uint32 * 4)()
+        mis, cold = C.c_uint64(), C.c_uint64()
+        arr = None if text is None else _as_u8(text)
+        ok = _lib.acg().acg_automaton_ctab_check(self._h, None if arr is None else arr.ctypes.data_as(C.c_void_p),
+                                                 0 if arr is None else arr.size, info, C.byref(mis), C.byref(cold))
+        return {"available": bool(ok), "slots": info[0], "default_depth": info[1], "hot_states": info[2],
+                "entries": info[3], "mismatches": mis.value, "cold_steps": cold.value}
+
     def layout(self) -> dict:
         v = [C.c_uint32() for _ in range(4)]
         mode = C.c_int()
@@ -416,6 +427,11 @@ class Scanner:
         rate = C.c_double()
         m = _lib.acg().acg_scanner_last_mode(self._h, C.byref(rate))
         return {MODE_SPARSE: "sparse", MODE_EXACT: "exact", MODE_FILTER: "filter"}.get(m, "none"), rate.value
+
+    def last_walk(self) -> str:
+        """The walk kernel of the last EXACT run: dense hot rows (KE) or the
+        compressed hot automaton (KC, csrc/ctab.hpp)."""
+        return {0: "dense", 1: "ctab", 2: "sparseg"}.get(_lib.acg().acg_scanner_last_walk(self._h), "none")
 
     def copy_pattern_counts(self, d_dst_ptr: int, stream: int = 0) -> None:
         _check(_lib.acg().acg_scanner_copy_pattern_counts(self._h, C.c_void_p(d_dst_ptr), C.c_void_p(stream or None)))

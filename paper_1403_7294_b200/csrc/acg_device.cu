@@ -24,6 +24,7 @@
 
 #include "../../include/acg.h"
 #include "automaton.hpp"
+#include "ctab.hpp"
 #include "scan_kernels.cuh"
 #include "filter_kernels.cuh"
 #include "exact_kernels.cuh"
@@ -196,6 +197,10 @@ struct DeviceDfa {
     std::uint32_t hotH_bytes = 0;  // truncated automaton: H*K u16, padded to 16 (sparse mode)
     DevBuf<std::uint16_t> hotG;    // generic alphabets: SPARSE-G truncated automaton (exact_kernels.cuh)
     std::uint32_t hotG_bytes = 0;
+    // compressed hot automaton (ctab.hpp): shared-memory image, state words, id -> rank
+    DevBuf<std::uint32_t> ctab, ct_next;
+    DevBuf<std::uint16_t> ct_rank;
+    std::uint32_t ctab_bytes = 0;
     int smem_optin = 0;
     int num_sms = 0;
 };
@@ -304,6 +309,8 @@ struct acg_scanner {
     DevBuf<std::uint32_t> xev, xev_count, xev_slab, xev_pool;
     DevBuf<std::uint32_t> gfin, gfin_count, gfin_pool;  // SPARSE-G: the fix-up's final events (chunk + 1 slots per chunk)
     bool g_run = false;                                  // the last run walked SPARSE-G
+    bool c_run = false;                                  // the last run walked the compressed hot automaton (KC)
+    bool kc_geom = false;                                // ... and its geometry (short chunks walked in rounds)
     std::uint32_t walk_pool_blocks = 0;                  // pool blocks of the last walk's event slabs
     acg::kern::EventArgs eargs{};
     bool ev_run = false;
@@ -330,10 +337,11 @@ constexpr int kSm100SmemOptin = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOp
 // The automaton's host DFA for a device's shared-memory budget (a->mu held).
 std::shared_ptr<acg::Dfa> host_dfa_locked(const acg_automaton* a, int smem_optin) {
     std::size_t budget = hot_budget(smem_optin);
+    const std::size_t full_budget = budget;
     if (a->hot_limit) budget = std::min<std::size_t>(budget, (a->hot_limit + 1ull) * 2ull * 256ull);
     if (!a->dfa || a->dfa_budget != budget) {
         auto dfa = std::make_shared<acg::Dfa>();
-        acg::compile_dfa(a->nfa, budget, a->profile.empty() ? nullptr : &a->profile, *dfa, a->hot_limit);
+        acg::compile_dfa(a->nfa, budget, a->profile.empty() ? nullptr : &a->profile, *dfa, a->hot_limit, full_budget);
         a->dfa = std::move(dfa);
         a->dfa_budget = budget;
     }
@@ -379,6 +387,14 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
         std::vector<std::uint16_t> hh(dd->hotH_bytes / 2, 0);
         std::copy(d.hotH.begin(), d.hotH.end(), hh.begin());
         ACG_CUDA(upload(dd->hotH, hh.data(), hh.size(), up));
+    }
+    if (!d.ctab.empty()) {
+        dd->ctab_bytes = static_cast<std::uint32_t>((d.ctab.size() * 4 + 15) & ~std::size_t(15));
+        std::vector<std::uint32_t> img(dd->ctab_bytes / 4, 0);
+        std::copy(d.ctab.begin(), d.ctab.end(), img.begin());
+        ACG_CUDA(upload(dd->ctab, img.data(), img.size(), up));
+        ACG_CUDA(upload(dd->ct_next, d.ct_next.data(), d.ct_next.size(), up));
+        ACG_CUDA(upload(dd->ct_rank, d.ct_rank.data(), d.ct_rank.size(), up));
     }
     if (!d.hotG.empty()) {
         dd->hotG_bytes = static_cast<std::uint32_t>((d.hotG.size() * 2 + 15) & ~std::size_t(15));
@@ -767,6 +783,8 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
 
 // Chunk geometry for owned bytes [emit_from, n): one chunk per stream, all
 // streams of a full grid (one CTA per SM: the hot table takes the SM's smem).
+constexpr unsigned long long kCtabChunk = 2048;  // KC: owned bytes per chunk (upper bound)
+
 void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     const DeviceDfa& dd = *s->dd;
     const unsigned long long streams = static_cast<unsigned long long>(dd.num_sms) * s->tpb_run * s->U_run;
@@ -787,7 +805,12 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     }
     unsigned long long chunk = s->chunk_override;
     if (!chunk) {
-        chunk = (owned + streams - 1) / streams;
+        // KC walks short chunks in rounds (neighbouring lanes on neighbouring chunks):
+        // the fewest full rounds with chunks of at most kCtabChunk bytes
+        const unsigned long long kc_chunk = std::max<unsigned long long>(kCtabChunk, 32 * halo);  // warm-up <= 3 %
+        const unsigned long long rounds =
+            s->kc_geom ? std::max<unsigned long long>(1, (owned + streams * kc_chunk - 1) / (streams * kc_chunk)) : 1;
+        chunk = (owned + streams * rounds - 1) / (streams * rounds);
         chunk = std::max<unsigned long long>(chunk, std::max<unsigned long long>(256, 2 * halo));
     }
     chunk = (chunk + 15) & ~15ull;
@@ -883,6 +906,46 @@ bool sparseg_ok(const acg_scanner* s, std::uint32_t n_out) {
     const acg::Dfa& d = *dd.dfa;
     return on && dd.hotG.p && dd.hotG_bytes + 256 <= static_cast<std::uint32_t>(dd.smem_optin) &&
            bits_for(n_out + d.H) + bits_for(s->chunk + d.halo) <= 32;
+}
+
+// KC (ctab.hpp): the compressed hot automaton walk; ACG_CTAB=0 keeps KE.
+bool ctab_built(const acg_scanner* s) {
+    static const bool on = [] {
+        const char* e = std::getenv("ACG_CTAB");
+        return !(e && e[0] == '0');
+    }();
+    const DeviceDfa& dd = *s->dd;
+    return on && dd.ctab.p && dd.dfa->ct_slots && dd.ctab_bytes + 256 <= static_cast<std::uint32_t>(dd.smem_optin);
+}
+bool ctab_ok(const acg_scanner* s, std::uint32_t n_out) {
+    return ctab_built(s) && bits_for(s->dd->dfa->ct_slots + n_out) + bits_for(s->chunk) <= 32;
+}
+
+template <int U, int D>
+cudaError_t launch_ctab(const ScanArgs& a, const acg::kern::EventArgs& e, const acg::kern::CtabArgs& ct, unsigned grid,
+                        unsigned tpb, std::size_t smem, cudaStream_t st) {
+    auto k = acg::kern::ctab_event_kernel<U, D>;
+    if (cudaError_t err = prepare_smem(k, smem)) return err;
+    k<<<grid, tpb, smem, st>>>(a, e, ct);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ctab_walk(std::uint32_t U, std::uint32_t D, const ScanArgs& a, const acg::kern::EventArgs& e,
+                             const acg::kern::CtabArgs& ct, unsigned grid, unsigned tpb, std::size_t smem,
+                             cudaStream_t st) {
+    const unsigned t2 = std::min(tpb, 512u);  // (one stream per thread: up to 1024 threads; 512 above)
+    if (D == 3) {
+        switch (U) {
+            case 1: return launch_ctab<1, 3>(a, e, ct, grid, tpb, smem, st);
+            case 4: return launch_ctab<4, 3>(a, e, ct, grid, t2, smem, st);
+            default: return launch_ctab<2, 3>(a, e, ct, grid, t2, smem, st);
+        }
+    }
+    switch (U) {
+        case 1: return launch_ctab<1, 2>(a, e, ct, grid, tpb, smem, st);
+        case 4: return launch_ctab<4, 2>(a, e, ct, grid, t2, smem, st);
+        default: return launch_ctab<2, 2>(a, e, ct, grid, t2, smem, st);
+    }
 }
 
 template <int U>
@@ -987,6 +1050,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     s->scratch_run = false;
     s->ev_run = false;
     s->g_run = false;
+    s->c_run = false;
     s->synced = false;
     s->last = st;
     s->run_text = d_text;
@@ -1020,8 +1084,11 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
     if (mode != ACG_MODE_EXACT) s->exact_chunks = 0;  // chunk_counts no longer hold an exact run's counts
     // default interleave: sparse 1; exact 4 on DNA, 2 on generic alphabets (cfg3
     // at 512 MiB: U=1 5.70 ms, U=2 4.87 ms, U=4 6.77 ms — cold-row L2 waits grow with U)
+    // (the compressed-automaton walk KC is issue-bound, not latency-bound: one stream per thread)
+    const bool kc_likely = mode == ACG_MODE_EXACT && !stats && ctab_built(s);
     s->U_run = stats ? 2u
-                     : (s->U ? s->U : (mode == ACG_MODE_SPARSE ? 1u : (d.mode == acg::kAlphaDna4 ? 4u : 2u)));
+                     : (s->U ? s->U
+                             : (mode == ACG_MODE_SPARSE ? 1u : (d.mode == acg::kAlphaDna4 ? 4u : (kc_likely ? 1u : 2u))));
     if (mode == ACG_MODE_SPARSE && s->U_run > 4) s->U_run = 4;
     // exact mode at interleave <= 2 runs 1024 threads per SM (twice the warps to
     // hide cold-row L2 latency) unless the caller fixed the block size
@@ -1030,6 +1097,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
                                                         : 2 * acg::kern::kTPB;
     if (mode != ACG_MODE_SPARSE && (s->U_run > 2 || stats))  // those kernels are bounded at kTPB threads
         s->tpb_run = std::min<std::uint32_t>(s->tpb_run, acg::kern::kTPB);
+    s->kc_geom = kc_likely;
+    if (kc_likely && s->U_run > 1) s->tpb_run = std::min<std::uint32_t>(s->tpb_run, acg::kern::kTPB);  // KC: 1024 threads at U = 1 only
     plan_geometry(s, owned);
     const bool prof = s->flags & ACG_SCAN_PROFILE;
 
@@ -1244,7 +1313,17 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         // event pipeline (exact_kernels.cuh): KE walk logs output visits, E1
         // counts records per chunk + visits, K2 prefix, E2 expands (enqueue_write)
         s->g_run = sparseg_ok(s, n_out_states);
+        s->c_run = !s->g_run && ctab_ok(s, n_out_states);
         ACG_CUDA(plan_events(s, s->g_run ? n_out_states + d.H : n_out_states, st));
+        acg::kern::CtabArgs ct{};
+        if (s->c_run) {  // event payloads are state-word values: ids, or slots + rank
+            s->eargs.ob = bits_for(d.ct_slots + n_out_states);
+            ct.image = dd.ctab.p;
+            ct.image_bytes = dd.ctab_bytes;
+            ct.slots = d.ct_slots;
+            ct.next = dd.ct_next.p;
+            ct.rank = dd.ct_rank.p;
+        }
         s->walk_pool_blocks = s->eargs.pool_blocks;
         zero_later(s, s->xev_pool.p, sizeof(std::uint32_t));
         zero_later(s, s->scalars64.p + 8, sizeof(unsigned long long));
@@ -1284,6 +1363,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             ACG_CUDA(cudaGetLastError());
             s->eargs = ef;  // E1 / E2 (and a regrowth's re-expansion) read the final events
             s->launches += 2;
+        } else if (s->c_run) {
+            ACG_CUDA(flush_zeros(s, st));
+            const unsigned g_kc = static_cast<unsigned>(std::min<unsigned long long>(dd.num_sms, s->grid));  // rounds
+            ACG_CUDA(launch_ctab_walk(s->U_run, d.ct_D, a, s->eargs, ct, g_kc, s->tpb_run, dd.ctab_bytes + 256, st));
+            ++s->launches;
+            if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
         } else {
             ACG_CUDA(flush_zeros(s, st));
             ACG_CUDA(launch_event_walk(d.mode, s->U_run, a, s->eargs, g_ev, s->tpb_run, smem_bytes(dd), st));
@@ -1294,18 +1379,27 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         const std::size_t nb4 = static_cast<std::size_t>(n_out_states) * 4, nb1 = (n_out_states + 15u) & ~15u;
         const bool smem_bins = want_counts && nb4 <= kEventBinsMax;
         const bool smem_nout = (smem_bins ? nb4 : 0) + nb1 <= kEventBinsMax;
-        const std::size_t e1_smem = (smem_bins ? nb4 : 0) + (smem_nout ? nb1 : 0);
+        const std::size_t xl_bytes = s->c_run ? static_cast<std::size_t>(d.ct_slots) * 2 : 0;
+        // (the id -> rank table in shared memory only while two blocks still fit an SM;
+        // otherwise through L1: it is read-only and mostly resident)
+        const bool xl_smem = s->c_run && smem_nout && (smem_bins ? nb4 : 0) + nb1 + xl_bytes <= 100 * 1024;
+        const std::size_t e1_smem = (smem_bins ? nb4 : 0) + (smem_nout ? nb1 : 0) + (xl_smem ? xl_bytes : 0);
         const unsigned g1 = static_cast<unsigned>(
             std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 15) / 16, 2ull * dd.num_sms)));
         auto e1 = [&](auto k) -> cudaError_t {
             if (cudaError_t err = prepare_smem(k, e1_smem)) return err;
-            k<<<g1, 512, e1_smem, st>>>(a, s->eargs);
+            k<<<g1, 512, e1_smem, st>>>(a, s->eargs, ct, xl_smem);
             return cudaGetLastError();
         };
-        if (smem_bins && smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<true, true>));
-        else if (smem_bins) ACG_CUDA(e1(acg::kern::event_count_kernel<true, false>));
-        else if (smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<false, true>));
-        else ACG_CUDA(e1(acg::kern::event_count_kernel<false, false>));
+        if (s->c_run) {
+            if (smem_bins && smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<true, true, true>));
+            else if (smem_bins) ACG_CUDA(e1(acg::kern::event_count_kernel<true, false, true>));
+            else if (smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<false, true, true>));
+            else ACG_CUDA(e1(acg::kern::event_count_kernel<false, false, true>));
+        } else if (smem_bins && smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<true, true, false>));
+        else if (smem_bins) ACG_CUDA(e1(acg::kern::event_count_kernel<true, false, false>));
+        else if (smem_nout) ACG_CUDA(e1(acg::kern::event_count_kernel<false, true, false>));
+        else ACG_CUDA(e1(acg::kern::event_count_kernel<false, false, false>));
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
     } else {
@@ -2035,6 +2129,64 @@ int acg_automaton_filter_info(const acg_automaton* a, std::uint32_t* q, double* 
     return dfa->filter_ok ? 1 : 0;
 }
 
+int acg_automaton_ctab_check(const acg_automaton* a, const std::uint8_t* text, std::uint64_t n, std::uint32_t* info,
+                             std::uint64_t* mismatches, std::uint64_t* cold_steps) {
+    using namespace acg;
+    if (info) info[0] = info[1] = info[2] = info[3] = 0;
+    if (mismatches) *mismatches = 0;
+    if (cold_steps) *cold_steps = 0;
+    if (!a) return 0;
+    std::shared_ptr<const acg::Dfa> dfa;
+    {
+        std::lock_guard<std::mutex> lock(a->mu);
+        if (a->dev.empty()) dfa = host_dfa_locked(a, kSm100SmemOptin);
+        else dfa = a->dev.begin()->second->dfa;
+    }
+    const acg::Dfa& d = *dfa;
+    if (d.ctab.empty()) return 0;
+    const std::uint32_t K = d.K, slots = d.ct_slots, D = d.ct_D, esc = K - 1;
+    if (info) {
+        info[0] = slots;
+        info[1] = D;
+        info[2] = d.ct_hot;
+        std::uint32_t ents = 0;
+        for (std::uint32_t i = 0; i < slots; ++i) ents += d.ctab[i] != kCtEmpty;
+        info[3] = ents;
+    }
+    if (!text) return 1;
+    // the device walk (exact_kernels.cuh: ctab_event_kernel), step for step
+    std::uint64_t bad = 0, cold = 0;
+    std::uint32_t c1 = esc, c2 = esc, s_dev = 0;
+    std::uint32_t sw = d.ctab[slots + (D == 3 ? (K * K + K + 1) : (K + 1)) * esc];
+    for (std::uint64_t i = 0; i < n; ++i) {
+        const std::uint32_t c = d.symmap[text[i]];
+        const std::uint32_t idx = D == 3 ? (c2 * K + c1) * K + c : c1 * K + c;
+        const std::uint32_t x = d.ctab[slots + idx];
+        c2 = c1;
+        c1 = c;
+        std::uint32_t nx;
+        if (sw & kCtCold) {
+            ++cold;
+            const std::uint32_t v = sw & kCtValMask;
+            const std::uint32_t s = (sw & kCtOut) ? v - slots + d.Hn : v;
+            nx = d.ct_next[static_cast<std::size_t>(s) * K + c];
+        } else {
+            const std::uint32_t ent = d.ctab[(sw & kCtValMask) + c];
+            const std::uint32_t diff = ent ^ (c << kCtColShift);
+            nx = (diff & kCtColMask) ? x : diff;
+        }
+        sw = nx;
+        s_dev = d.next[static_cast<std::size_t>(s_dev) * K + c];
+        if (sw != d.ct_sw[s_dev]) {
+            ++bad;
+            sw = d.ct_sw[s_dev];
+        }
+    }
+    if (mismatches) *mismatches = bad;
+    if (cold_steps) *cold_steps = cold;
+    return 1;
+}
+
 int acg_automaton_layout(const acg_automaton* a, std::uint32_t* n_states, std::uint32_t* hot_rows,
                          std::uint32_t* columns, std::uint32_t* halo, int* alphabet_mode) {
     if (!a) return fail(ACG_ERR_INVALID, "null automaton");
@@ -2293,6 +2445,11 @@ int acg_scanner_last_mode(acg_scanner* s, double* event_rate) {
     if (!s) return -1;
     if (event_rate) *event_rate = s->mode_run == ACG_MODE_FILTER ? s->last_filter_rate : s->last_event_rate;
     return s->mode_run;
+}
+
+int acg_scanner_last_walk(const acg_scanner* s) {
+    if (!s) return -1;
+    return s->c_run ? 1 : s->g_run ? 2 : 0;
 }
 
 int acg_scanner_copy_pattern_counts(acg_scanner* s, void* d_dst, void* stream) {

@@ -1,6 +1,7 @@
 // Host automaton build (reference algorithm) and dense-DFA compilation.
 #include "automaton.hpp"
 #include "parallel.hpp"
+#include "ctab.hpp"
 #include "qfilter.hpp"
 
 #include <algorithm>
@@ -508,8 +509,150 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
 }  // namespace
 
 
+// Compressed hot automaton (ctab.hpp): T_D default table + row-displaced
+// exception entries of the hottest states, sized for `budget` bytes of shared
+// memory. Leaves d.ctab empty when the scheme does not apply.
+static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_order, std::size_t budget, Dfa& d,
+                         std::uint32_t hot_limit) {
+    d.ctab.clear();
+    d.ct_rank.clear();
+    d.ct_sw.clear();
+    d.ct_next.clear();
+    d.ct_slots = d.ct_D = d.ct_hot = 0;
+    const std::uint32_t S = d.S, K = d.K;
+    const std::uint32_t n_out = d.Cn - d.Hn;
+    if (d.mode != kAlphaGeneric || K > kCtMaxK || K < 2 || S <= d.H) return;  // (all states in the dense hot rows: KE has no cold steps)
+    if (S >= kCtValMask || n_out >= kCtNoRank) return;
+    const std::uint32_t D = (static_cast<std::uint64_t>(K) * K * K * 4 <= kCtDefaultMaxBytes) ? 3u : 2u;
+    std::uint32_t nd = 1;
+    for (std::uint32_t i = 0; i < D; ++i) nd *= K;
+    if (budget < static_cast<std::size_t>(nd) * 4 + 64 * K * 4) return;
+    const std::uint32_t slots =
+        static_cast<std::uint32_t>(std::min<std::size_t>((budget - static_cast<std::size_t>(nd) * 4) / 4 & ~std::size_t(3), 0xFFF0u));
+    if (slots + n_out >= kCtValMask) return;
+    const std::vector<std::uint32_t>& delta = nfa.delta;
+    auto has_out = [&](std::uint32_t s) { return nfa.out_off[s + 1] > nfa.out_off[s]; };
+    // exception columns of state s as a bit mask
+    auto exc_mask = [&](std::uint32_t s) {
+        std::uint32_t m = 0;
+        const std::size_t row = static_cast<std::size_t>(s) * K;
+        for (std::uint32_t c = 0; c < K; ++c)
+            if (nfa.depth[delta[row + c]] > D) m |= 1u << c;
+        return m;
+    };
+    // candidate prefix of the hot order: rows whose exceptions fill at most `fill` of the slots
+    std::vector<std::uint32_t> masks;
+    masks.reserve(std::min<std::size_t>(S, slots));
+    const std::uint32_t max_ids = slots - K + 1;
+    auto try_place = [&](std::size_t n_hot, std::vector<std::uint32_t>& id_of) -> bool {
+        // first-fit row displacement, largest rows first (occupancy and id bitsets)
+        std::vector<std::uint64_t> occ((slots + 64 + 63) / 64 + 1, 0), idu((slots + 63) / 64 + 1, 0);
+        std::vector<std::uint32_t> order(n_hot);
+        for (std::size_t i = 0; i < n_hot; ++i) order[i] = static_cast<std::uint32_t>(i);
+        std::stable_sort(order.begin(), order.end(), [&](std::uint32_t x, std::uint32_t y) {
+            return __builtin_popcount(masks[x]) > __builtin_popcount(masks[y]);
+        });
+        id_of.assign(n_hot, 0xFFFFFFFFu);
+        std::uint32_t lo = 0;  // every slot below lo is occupied
+        for (std::uint32_t i : order) {
+            const std::uint32_t m = masks[i];
+            if (!m) break;  // (sorted: the rest have no exceptions)
+            const std::uint32_t c0 = static_cast<std::uint32_t>(__builtin_ctz(m));
+            std::uint32_t b = lo > c0 ? lo - c0 : 0;
+            bool placed = false;
+            for (; b < max_ids; ++b) {
+                const std::uint32_t w = b >> 6, sh = b & 63;
+                const std::uint64_t win = sh ? (occ[w] >> sh) | (occ[w + 1] << (64 - sh)) : occ[w];
+                if ((win & m) == 0 && !((idu[w] >> sh) & 1)) {
+                    placed = true;
+                    break;
+                }
+            }
+            if (!placed) return false;
+            id_of[i] = b;
+            idu[b >> 6] |= 1ull << (b & 63);
+            for (std::uint32_t mm = m; mm; mm &= mm - 1) {
+                const std::uint32_t t = b + static_cast<std::uint32_t>(__builtin_ctz(mm));
+                occ[t >> 6] |= 1ull << (t & 63);
+            }
+            while (lo < slots && ((occ[lo >> 6] >> (lo & 63)) & 1)) ++lo;
+        }
+        // states without exceptions: any id no row uses
+        std::uint32_t b = 0;
+        for (std::uint32_t i : order) {
+            if (masks[i]) continue;
+            while (b < max_ids && ((idu[b >> 6] >> (b & 63)) & 1)) ++b;
+            if (b >= max_ids) return false;
+            id_of[i] = b;
+            idu[b >> 6] |= 1ull << (b & 63);
+        }
+        return true;
+    };
+    std::size_t n_hot = 0;
+    std::vector<std::uint32_t> id_of;
+    for (double fill = 0.94; fill > 0.3; fill -= 0.06) {
+        const std::uint64_t cap = static_cast<std::uint64_t>(fill * slots);
+        std::uint64_t used = 0;
+        n_hot = 0;
+        masks.clear();
+        while (n_hot < S && n_hot < max_ids && (!hot_limit || n_hot < hot_limit)) {  // (hot_limit: diagnostics, cold paths)
+            const std::uint32_t m = exc_mask(hot_order[n_hot]);
+            const std::uint32_t k = static_cast<std::uint32_t>(__builtin_popcount(m));
+            if (used + k > cap) break;
+            used += k;
+            masks.push_back(m);
+            ++n_hot;
+        }
+        if (n_hot && try_place(n_hot, id_of)) break;
+        n_hot = 0;
+    }
+    if (!n_hot) return;
+    // state words (device order) and the id -> rank table
+    d.ct_sw.assign(S, 0);
+    d.ct_rank.assign(slots, static_cast<std::uint16_t>(kCtNoRank));
+    std::vector<std::uint32_t> sw_nfa(S);
+    std::vector<std::uint8_t> is_hot(S, 0);
+    for (std::size_t i = 0; i < n_hot; ++i) {
+        const std::uint32_t s = hot_order[i];
+        is_hot[s] = 1;
+        sw_nfa[s] = id_of[i] | (has_out(s) ? kCtOut : 0u);
+        if (has_out(s)) d.ct_rank[id_of[i]] = static_cast<std::uint16_t>(d.dev_of[s] - d.Hn);
+    }
+    for (std::uint32_t s = 0; s < S; ++s) {
+        if (!is_hot[s]) sw_nfa[s] = kCtCold | (has_out(s) ? kCtOut | (slots + d.dev_of[s] - d.Hn) : d.dev_of[s]);
+        d.ct_sw[d.dev_of[s]] = sw_nfa[s];
+    }
+    d.ctab.assign(static_cast<std::size_t>(slots) + nd, kCtEmpty);
+    for (std::size_t i = 0; i < n_hot; ++i) {
+        const std::uint32_t s = hot_order[i];
+        const std::size_t row = static_cast<std::size_t>(s) * K;
+        for (std::uint32_t mm = masks[i]; mm; mm &= mm - 1) {
+            const std::uint32_t c = static_cast<std::uint32_t>(__builtin_ctz(mm));
+            d.ctab[id_of[i] + c] = sw_nfa[delta[row + c]] | (c << kCtColShift);
+        }
+    }
+    // T_D: index = sum_j col_{i-j} * K^j (the latest column is the lowest digit)
+    for (std::uint32_t idx = 0; idx < nd; ++idx) {
+        std::uint32_t cols[3], t = idx;
+        for (std::uint32_t j = 0; j < D; ++j) {
+            cols[j] = t % K;
+            t /= K;
+        }
+        std::uint32_t st = 0;
+        for (std::uint32_t j = D; j-- > 0;) st = delta[static_cast<std::size_t>(st) * K + cols[j]];
+        d.ctab[slots + idx] = sw_nfa[st];
+    }
+    d.ct_next.resize(static_cast<std::size_t>(S) * K);
+    parallel_for(S, 1 << 13, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo * K; i < hi * K; ++i) d.ct_next[i] = d.ct_sw[d.next[i]];
+    });
+    d.ct_slots = slots;
+    d.ct_D = D;
+    d.ct_hot = static_cast<std::uint32_t>(n_hot);
+}
+
 void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& d,
-                 std::uint32_t hot_limit) {
+                 std::uint32_t hot_limit, std::size_t ctab_budget_bytes) {
     Phase ph_all("compile_dfa (total)");
     Phase ph_ord("  hot order");
     const std::uint32_t S = nfa.state_count();
@@ -629,6 +772,7 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
             }
         });
     }
+    compile_ctab(nfa, hot_order, ctab_budget_bytes ? ctab_budget_bytes : hot_budget_bytes, d, hot_limit);
     d.id_bits = 1;
     while ((1ull << d.id_bits) < nfa.n_patterns) ++d.id_bits;
     d.halo = (nfa.max_len + 15u) & ~15u;

@@ -93,6 +93,14 @@ struct Dfa {
     // Generic alphabets (SPARSE-G walk): H*K u16 = longest hot suffix of the
     // target | 0x8000 when the true target is cold (empty = not available).
     std::vector<std::uint16_t> hotG;
+    // Compressed hot automaton (ctab.hpp; generic alphabets of <= 31 columns
+    // whose states do not all fit the dense hot rows): the shared-memory image
+    // = ct_slots row-displaced exception entries, then the K^ct_D default table.
+    std::vector<std::uint32_t> ctab;
+    std::uint32_t ct_slots = 0, ct_D = 0, ct_hot = 0;  // slots (= id space), default depth, hot states
+    std::vector<std::uint16_t> ct_rank;  // ct_slots: id -> output rank (kCtNoRank: none)
+    std::vector<std::uint32_t> ct_sw;    // S: device state -> state word
+    std::vector<std::uint32_t> ct_next;  // S*K: the dense table with state-word targets (cold steps: one load)
     std::vector<std::uint32_t> depth;    // S, device order
     std::vector<std::uint32_t> out_off;  // S+1 in device order
     std::vector<std::uint32_t> out_ids;  // ascending per state
@@ -130,7 +138,9 @@ struct Dfa {
 // Fold the NFA into the dense DFA image. `hot_budget_bytes` bounds the u16 hot
 // table kept in shared memory. `visits` (optional, NFA order) gives
 // profile-guided hotness; otherwise BFS order is used.
+// `ctab_budget_bytes` (0 = hot_budget_bytes) bounds the compressed hot
+// automaton's image (ctab.hpp).
 void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& out,
-                 std::uint32_t hot_limit = 0);
+                 std::uint32_t hot_limit = 0, std::size_t ctab_budget_bytes = 0);
 
 }  // namespace acg

@@ -29,6 +29,7 @@
 
 #include <type_traits>
 
+#include "ctab.hpp"
 #include "scan_kernels.cuh"
 
 namespace acg {
@@ -266,6 +267,210 @@ __global__ void __launch_bounds__(U <= 2 ? 2 * kTPB : kTPB, 1) exact_event_kerne
         if (act[u]) e.ev_count[cid[u]] = cnt[u];
 }
 
+// =================================================================== KC ==
+// The EXACT walk over the compressed hot automaton (ctab.hpp): same chunking,
+// event slabs and logging as KE (chunks of at most ~2 KiB walked in rounds,
+// see below), but the per-step lookup is one 32-bit
+// shared-memory load of the row-displaced exception table,
+//     e = tab[id + c];  next = column field of e == c ? e (tag cleared) : x
+// with x = T_D[last D columns] computed from the text alone (two multiply-adds
+// and one load per step, off the state's dependency chain). Cold state words
+// (rare: the table holds every state that matters) step through the dense
+// L2-resident table. Events carry the state word's value (hot: id, cold
+// output: slots + rank); E1 maps them to output ranks.
+struct CtabArgs {
+    const std::uint32_t* image;   // slots exception entries, then the K^D default table
+    std::uint32_t image_bytes;    // multiple of 16
+    std::uint32_t slots;
+    const std::uint32_t* next;    // S*K dense table, targets as state words (cold steps)
+    const std::uint16_t* rank;    // id -> output rank (E1)
+};
+
+// A cold state word's step: the dense L2-resident table of state words. Out of
+// line so the walk's straight-line code carries one branch, not its address
+// arithmetic (cold steps are rare: the table holds every state that matters).
+__device__ __noinline__ std::uint32_t ctab_cold_step(const std::uint32_t* next, std::uint32_t K, std::uint32_t slots,
+                                                     std::uint32_t Hn, std::uint32_t sw, std::uint32_t c4) {
+    const std::uint32_t v = sw & kCtValMask;
+    const std::uint32_t s = (sw & kCtOut) ? v - slots + Hn : v;
+    return __ldg(next + static_cast<std::size_t>(s) * K + (c4 >> 2));
+}
+
+// a value the compiler must keep in a register (no rematerialisation of the
+// shared-window address arithmetic inside the unrolled steps)
+__device__ __forceinline__ std::uint32_t pinned_reg(std::uint32_t v) {
+    std::uint32_t r;
+    asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+// Thread block: 1024 threads at one stream per thread, 512 above (the columns
+// of a whole group of steps are held in registers).
+template <int U, int D>
+__global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel(const ScanArgs a, const EventArgs e,
+                                                                                 const CtabArgs ct) {
+    constexpr int GL = U <= 2 ? 16 : 8;  // steps per group: their columns are looked up together, ahead of the walk
+    extern __shared__ __align__(16) std::uint8_t smem[];
+    {
+        std::uint8_t* smap4 = smem + ct.image_bytes;  // byte -> 4 * column
+        const uint4* src = reinterpret_cast<const uint4*>(ct.image);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (std::uint32_t i = threadIdx.x; i < ct.image_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+        for (std::uint32_t i = threadIdx.x; i < 256; i += blockDim.x) smap4[i] = static_cast<std::uint8_t>(4u * a.symmap[i]);
+    }
+    __syncthreads();
+    const std::uint32_t tab_s = pinned_reg(smem_u32(smem));
+    const std::uint32_t def_s = pinned_reg(tab_s + 4u * ct.slots);
+    const std::uint32_t map_s = pinned_reg(tab_s + ct.image_bytes);
+
+    const std::uint32_t K = pinned_reg(a.K), KK = pinned_reg(a.K * a.K), esc4 = 4u * (a.K - 1u);
+    const long long halo = a.halo, steps = a.halo + a.chunk, n = a.n;
+    std::uint32_t* __restrict__ ev = e.ev;
+    const std::uint32_t root = lds_u32(def_s + (D == 3 ? (KK + K + 1u) : (K + 1u)) * esc4);  // T_D[esc, .., esc]
+
+    // Rounds: in round r the grid walks the chunks [r, r+1) * gridDim * blockDim * U,
+    // neighbouring lanes on neighbouring chunks — the text a warp reads at any
+    // time lies within 32 * U chunks (with one long chunk per stream the lanes
+    // of a warp sit megabytes apart: every text load touches 32 pages).
+    const long long per_round = static_cast<long long>(gridDim.x) * blockDim.x * U;
+    for (long long cid0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * U; cid0 < a.n_chunks;
+         cid0 += per_round) {
+    long long cid[U];
+    bool act[U];
+    std::uint32_t live[U];  // kCtOut while the stream may log, else 0 (the log predicate is one AND)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        cid[u] = cid0 + u;
+        act[u] = cid[u] < a.n_chunks;
+        live[u] = act[u] ? kCtOut : 0u;
+    }
+
+    std::uint32_t st[U], wr[U], lim[U], cnt[U], p1[U], p2[U];  // p1/p2: 4 * the previous two columns
+    long long pos0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        st[u] = root;
+        cnt[u] = 0;
+        p1[u] = p2[u] = esc4;
+        wr[u] = act[u] ? slab_start(e, cid[u]) : 0u;
+        lim[u] = act[u] ? slab_end(e, cid[u]) - 1u : 0u;
+        pos0[u] = a.emit_from + cid[u] * a.chunk - halo;
+    }
+    uint4 w[U];
+    auto load = [&](long long off) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = pos0[u] + off;
+            w[u] = (act[u] && p >= 0 && p < n) ? ld_stream16(a.text + p) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    // the text-only default of a step: x = T_D[the step's last D columns]
+    auto default_of = [&](std::uint32_t q2, std::uint32_t q1, std::uint32_t c4) -> std::uint32_t {
+        const std::uint32_t r2 = q1 * K + (c4 + def_s);
+        return lds_u32(D == 3 ? q2 * KK + r2 : r2);
+    };
+    load(0);
+    for (long long off = 0; off < steps; off += 16) {
+        uint4 cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = w[u];
+        if (off + 16 < steps) load(off + 16);
+        const bool owned_blk = off >= halo;
+        std::uint32_t wr0[U];
+        if (owned_blk) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (live[u] && lim[u] - wr[u] < 16u) {  // close the region, continue in a pool block
+                    for (; wr[u] < lim[u]; ++wr[u], ++cnt[u]) ev[wr[u]] = kEvPad;
+                    const uint2 g = ev_grow(ev, e.pool_used, e.pool_base, e.pool_blocks, lim[u]);
+                    wr[u] = g.x;
+                    lim[u] = g.y;
+                    if (g.y == 0u) live[u] = 0u;
+                }
+                wr0[u] = wr[u];
+            }
+        }
+        bool fast = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = pos0[u] + off;
+            fast = fast && (!act[u] || (p >= 0 && p + 16 <= n));
+        }
+        std::uint32_t kk = owned_blk ? static_cast<std::uint32_t>(off - halo) << e.ob : 0u;
+        const std::uint32_t kinc = 1u << e.ob;
+        // One group of GL steps of all U streams. The columns of the whole group
+        // are looked up first (independent loads); each step's default is loaded
+        // one step ahead of its use; the state's own chain per step is the
+        // address multiply-add, the entry load, XOR, test, select.
+        auto group = [&](auto log_tag, auto fast_tag, const int k0) {
+            constexpr bool LOG = decltype(log_tag)::value;
+            constexpr bool FAST = decltype(fast_tag)::value;
+            std::uint32_t c4[U][GL];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int j = 0; j < GL; ++j) {
+                    const int k = k0 + j;
+                    const std::uint32_t word = k < 4 ? cur[u].x : k < 8 ? cur[u].y : k < 12 ? cur[u].z : cur[u].w;
+                    std::uint32_t c = lds_u8z(map_s + __byte_perm(word, 0u, 0x4440u + (k & 3)));
+                    if (!FAST) {  // a position outside the text reads as a byte outside the alphabet (root)
+                        const long long p = pos0[u] + off + k;
+                        if (!act[u] || p < 0 || p >= n) c = esc4;
+                    }
+                    c4[u][j] = c;
+                }
+            std::uint32_t xn[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) xn[u] = default_of(p2[u], p1[u], c4[u][0]);
+#pragma unroll
+            for (int j = 0; j < GL; ++j) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const std::uint32_t c = c4[u][j], x = xn[u];
+                    if (j + 1 < GL) xn[u] = default_of(j ? c4[u][j - 1] : p1[u], c, c4[u][j + 1]);
+                    const std::uint32_t sw = st[u];
+                    std::uint32_t v;
+                    if (__builtin_expect((sw & kCtCold) != 0u, 0)) {
+                        v = ctab_cold_step(ct.next, K, ct.slots, a.Hn, sw, c);
+                    } else {
+                        const std::uint32_t ent = lds_u32(sw * 4u + (c + tab_s));  // (bit 31 of sw falls off the multiply)
+                        const std::uint32_t diff = ent ^ (c << (kCtColShift - 2));
+                        v = (diff & kCtColMask) ? x : diff;
+                    }
+                    st[u] = v;
+                    if (LOG) {
+                        if (v & live[u]) ev[wr[u]++] = kk + (v & kCtValMask);
+                    }
+                }
+                if (LOG) kk += kinc;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                p2[u] = c4[u][GL - 2];
+                p1[u] = c4[u][GL - 1];
+            }
+        };
+#pragma unroll
+        for (int k0 = 0; k0 < 16; k0 += GL) {
+            if (fast) {
+                if (owned_blk) group(std::true_type{}, std::true_type{}, k0);
+                else group(std::false_type{}, std::true_type{}, k0);
+            } else {
+                if (owned_blk) group(std::true_type{}, std::false_type{}, k0);
+                else group(std::false_type{}, std::false_type{}, k0);
+            }
+        }
+        if (owned_blk) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) cnt[u] += wr[u] - wr0[u];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (act[u]) e.ev_count[cid[u]] = cnt[u];
+    }  // rounds
+}
+
 // ====================================================== SPARSE-G (generic) ==
 // EXACT mode for generic alphabets without L2 lookups in the lockstep walk.
 // hotG[s*K + c] (s hot) = the longest suffix of s.c in the hot set H (a BFS
@@ -467,7 +672,7 @@ __global__ void __launch_bounds__(256) event_slab_sizes_kernel(const std::uint32
 
 // Walks chunk c's event regions (primary slab, then linked pool blocks) in
 // warp-wide batches of up to 32 events: f(base_index, n_in_batch, event of
-// this lane or 0, lane valid).
+// this lane or 0, lane valid, the event's slot).
 template <typename F>
 __device__ __forceinline__ void for_event_batches(const EventArgs& e, long long c, std::uint32_t total, int lane, F f) {
     std::uint32_t p = slab_start(e, c), lim = slab_end(e, c) - 1u, done = 0;
@@ -477,7 +682,7 @@ __device__ __forceinline__ void for_event_batches(const EventArgs& e, long long 
             const std::uint32_t nb = min(32u, here - b);
             const bool ok = static_cast<std::uint32_t>(lane) < nb;
             const std::uint32_t v = ok ? __ldcs(e.ev + p + b + lane) : 0u;
-            f(done + b, nb, v, ok);
+            f(done + b, nb, v, ok, p + b + lane);
         }
         done += here;
         if (done < total) {
@@ -498,16 +703,26 @@ __device__ __forceinline__ std::uint32_t n_out_of(std::uint32_t s, unsigned long
 // prefix) and visits per output rank (shared-memory bins when they fit).
 // (SMEM_NOUT: each output state's output count, as a byte (255 = look it up),
 // staged after the bins: the events' record counts need no L2 lookups)
-template <bool SMEM_BINS, bool SMEM_NOUT>
-__global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, const EventArgs e) {
+// (XL: the walk was KC — event payloads are state-word values (ctab.hpp); they
+// are mapped to output ranks here, through the id -> rank table (staged in
+// shared memory when xl_smem), and the events rewritten in place for E2)
+template <bool SMEM_BINS, bool SMEM_NOUT, bool XL>
+__global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, const EventArgs e, const CtabArgs ct,
+                                                          const bool xl_smem) {
     extern __shared__ std::uint32_t bins[];
     std::uint8_t* nout8 = reinterpret_cast<std::uint8_t*>(bins + (SMEM_BINS ? e.n_out : 0u));
+    const std::uint16_t* xrank = ct.rank;
     if (SMEM_BINS)
         for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x) bins[i] = 0;
     if (SMEM_NOUT)
         for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x)
             nout8[i] = static_cast<std::uint8_t>(__ldg(a.outinfo + a.Hn + i) >> 32);
-    if (SMEM_BINS || SMEM_NOUT) __syncthreads();
+    if (XL && xl_smem) {
+        std::uint16_t* xs = reinterpret_cast<std::uint16_t*>(nout8 + (SMEM_NOUT ? ((e.n_out + 15u) & ~15u) : 0u));
+        for (std::uint32_t i = threadIdx.x; i < ct.slots; i += blockDim.x) xs[i] = __ldg(ct.rank + i);
+        xrank = xs;
+    }
+    if (SMEM_BINS || SMEM_NOUT || XL) __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long wpb = blockDim.x >> 5;
     const long long warps = static_cast<long long>(gridDim.x) * wpb;
@@ -520,9 +735,13 @@ __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, cons
         evs += total;
         unsigned long long recs = 0;
         if (total) {
-            for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t, std::uint32_t v, bool ok) {
+            for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t, std::uint32_t v, bool ok, std::uint32_t slot) {
                 if (!ok || v == kEvPad) return;
-                const std::uint32_t r = v & rmask;
+                std::uint32_t r = v & rmask;
+                if (XL) {
+                    r = r < ct.slots ? (xl_smem ? xrank[r] : __ldg(ct.rank + r)) : r - ct.slots;
+                    e.ev[slot] = (v & ~rmask) | r;
+                }
                 const std::uint32_t s = state_of_rank(r, H, Hn, Cn);
                 std::uint32_t no = SMEM_NOUT ? nout8[r] : 255u;
                 if (no == 255u) no = n_out_of(s, __ldg(a.outinfo + s), a);
@@ -559,7 +778,7 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
         if (!total) continue;
         unsigned long long o = a.chunk_offs[c];
         const unsigned long long cbase = a.base + static_cast<unsigned long long>(a.emit_from + c * a.chunk);
-        for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t nb, std::uint32_t v, bool ok) {
+        for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t nb, std::uint32_t v, bool ok, std::uint32_t) {
             std::uint32_t n = 0, lo = 0, first = 0;
             unsigned long long key = 0;
             if (ok && v != kEvPad) {

@@ -178,6 +178,17 @@ __device__ __forceinline__ std::uint32_t lds_u16z(std::uint32_t saddr) {
     return v;
 }
 
+__device__ __forceinline__ std::uint32_t lds_u32(std::uint32_t saddr) {
+    std::uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+    return v;
+}
+__device__ __forceinline__ std::uint32_t lds_u8z(std::uint32_t saddr) {
+    std::uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(saddr));
+    return v;
+}
+
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -47,7 +47,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
         _run(["g++", "-std=c++17", "-O3", "-fPIC", "-shared", "-pthread", "-o", synth, src])
 
     headers = [os.path.join(CSRC, h) for h in ("automaton.hpp", "scan_kernels.cuh", "filter_kernels.cuh",
-                                               "exact_kernels.cuh", "format_kernels.cuh", "partition.cuh", "qfilter.hpp", "parallel.hpp")] + [
+                                               "exact_kernels.cuh", "format_kernels.cuh", "partition.cuh", "qfilter.hpp", "ctab.hpp", "parallel.hpp")] + [
         os.path.join(ROOT, "include", "acg.h")]
     host_objs = []
     for name in HOST_SOURCES:
