@@ -180,8 +180,8 @@ int acg_automaton_layout(const acg_automaton* a, uint32_t* n_states, uint32_t* h
                          uint32_t* halo, int* alphabet_mode);
 
 /* Compressed hot automaton of the EXACT walk (diagnostics; host only, no
- * device needed): info = {slots, default depth D, hot states, exception
- * entries}; when `text` is given, walks it on the host both with the dense
+ * device needed): info[5] = {slots, default depth D, hot states,
+ * exception entries, 1 if the default takes one more level from the table}; when `text` is given, walks it on the host both with the dense
  * transition table and with the compressed tables exactly as the device walk
  * (KC) does, and returns in *mismatches the positions where the two states
  * differ (0 = the compressed automaton is exact on this text) and in

@@ -205,13 +205,13 @@ class Automaton:
     def ctab_check(self, text=None) -> dict:
         """Compressed hot automaton (csrc/ctab.hpp): its geometry and, with a
         text, the host replay of the device walk against the dense table."""
-        info = (C.c_uint32 * 4)()
+        info = (C.c_uint32 * 5)()
         mis, cold = C.c_uint64(), C.c_uint64()
         arr = None if text is None else _as_u8(text)
         ok = _lib.acg().acg_automaton_ctab_check(self._h, None if arr is None else arr.ctypes.data_as(C.c_void_p),
                                                  0 if arr is None else arr.size, info, C.byref(mis), C.byref(cold))
         return {"available": bool(ok), "slots": info[0], "default_depth": info[1], "hot_states": info[2],
-                "entries": info[3], "mismatches": mis.value, "cold_steps": cold.value}
+                "entries": info[3], "deep": bool(info[4]), "mismatches": mis.value, "cold_steps": cold.value}
 
     def layout(self) -> dict:
         v = [C.c_uint32() for _ in range(4)]

@@ -807,13 +807,26 @@ void plan_geometry(acg_scanner* s, std::uint64_t owned) {
     if (!chunk) {
         // KC walks short chunks in rounds (neighbouring lanes on neighbouring chunks):
         // the fewest full rounds with chunks of at most kCtabChunk bytes
-        const unsigned long long kc_chunk = std::max<unsigned long long>(kCtabChunk, 32 * halo);  // warm-up <= 3 %
+        static const unsigned long long kc_env = [] {  // ACG_KC_CHUNK: experiments
+            const char* e = std::getenv("ACG_KC_CHUNK");
+            return e ? std::strtoull(e, nullptr, 10) : 0ull;
+        }();
+        const unsigned long long kc_chunk =
+            std::max<unsigned long long>(kc_env ? kc_env : kCtabChunk, 32 * halo);  // warm-up <= 3 %
         const unsigned long long rounds =
             s->kc_geom ? std::max<unsigned long long>(1, (owned + streams * kc_chunk - 1) / (streams * kc_chunk)) : 1;
         chunk = (owned + streams * rounds - 1) / (streams * rounds);
         chunk = std::max<unsigned long long>(chunk, std::max<unsigned long long>(256, 2 * halo));
     }
     chunk = (chunk + 15) & ~15ull;
+    if (s->kc_geom && !s->chunk_override) {
+        static const unsigned long long kc_align = [] {  // ACG_KC_ALIGN: experiments
+            const char* e = std::getenv("ACG_KC_ALIGN");
+            return e ? std::strtoull(e, nullptr, 10) : 256ull;
+        }();
+        // chunks start on 256-byte boundaries: the text loads' L2 prefetch granule (cfg3: KC 4.27 -> 3.12 ms per 2 GiB)
+        chunk = (chunk + kc_align - 1) / kc_align * kc_align;
+    }
     // sparse mode: walk length (halo + chunk) a multiple of the 64-byte refill
     // (an explicit chunk override is kept as is: odd walks take the per-byte path)
     if (s->mode_run == ACG_MODE_SPARSE) {
@@ -921,30 +934,42 @@ bool ctab_ok(const acg_scanner* s, std::uint32_t n_out) {
     return ctab_built(s) && bits_for(s->dd->dfa->ct_slots + n_out) + bits_for(s->chunk) <= 32;
 }
 
-template <int U, int D>
+template <int U, int D, bool DEEP, bool COLD>
 cudaError_t launch_ctab(const ScanArgs& a, const acg::kern::EventArgs& e, const acg::kern::CtabArgs& ct, unsigned grid,
                         unsigned tpb, std::size_t smem, cudaStream_t st) {
-    auto k = acg::kern::ctab_event_kernel<U, D>;
+    auto k = acg::kern::ctab_event_kernel<U, D, DEEP, COLD>;
     if (cudaError_t err = prepare_smem(k, smem)) return err;
     k<<<grid, tpb, smem, st>>>(a, e, ct);
     return cudaGetLastError();
+}
+
+// (instantiations: the all-hot deep walk only at D = 3, U <= 2 — cfg3's; the rest keep the cold branch)
+template <int U, int D>
+cudaError_t launch_ctab_v(bool deep, bool cold, const ScanArgs& a, const acg::kern::EventArgs& e,
+                          const acg::kern::CtabArgs& ct, unsigned grid, unsigned tpb, std::size_t smem, cudaStream_t st) {
+    if (deep) {
+        if (D == 3 && U <= 2 && !cold) return launch_ctab<U, D, true, false>(a, e, ct, grid, tpb, smem, st);
+        return launch_ctab<U, D, true, true>(a, e, ct, grid, tpb, smem, st);
+    }
+    return launch_ctab<U, D, false, true>(a, e, ct, grid, tpb, smem, st);
 }
 
 cudaError_t launch_ctab_walk(std::uint32_t U, std::uint32_t D, const ScanArgs& a, const acg::kern::EventArgs& e,
                              const acg::kern::CtabArgs& ct, unsigned grid, unsigned tpb, std::size_t smem,
                              cudaStream_t st) {
     const unsigned t2 = std::min(tpb, 512u);  // (one stream per thread: up to 1024 threads; 512 above)
+    const bool deep = ct.deep, cold = ct.cold;
     if (D == 3) {
         switch (U) {
-            case 1: return launch_ctab<1, 3>(a, e, ct, grid, tpb, smem, st);
-            case 4: return launch_ctab<4, 3>(a, e, ct, grid, t2, smem, st);
-            default: return launch_ctab<2, 3>(a, e, ct, grid, t2, smem, st);
+            case 1: return launch_ctab_v<1, 3>(deep, cold, a, e, ct, grid, tpb, smem, st);
+            case 4: return launch_ctab_v<4, 3>(deep, cold, a, e, ct, grid, t2, smem, st);
+            default: return launch_ctab_v<2, 3>(deep, cold, a, e, ct, grid, t2, smem, st);
         }
     }
     switch (U) {
-        case 1: return launch_ctab<1, 2>(a, e, ct, grid, tpb, smem, st);
-        case 4: return launch_ctab<4, 2>(a, e, ct, grid, t2, smem, st);
-        default: return launch_ctab<2, 2>(a, e, ct, grid, t2, smem, st);
+        case 1: return launch_ctab_v<1, 2>(deep, cold, a, e, ct, grid, tpb, smem, st);
+        case 4: return launch_ctab_v<4, 2>(deep, cold, a, e, ct, grid, t2, smem, st);
+        default: return launch_ctab_v<2, 2>(deep, cold, a, e, ct, grid, t2, smem, st);
     }
 }
 
@@ -1323,6 +1348,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             ct.slots = d.ct_slots;
             ct.next = dd.ct_next.p;
             ct.rank = dd.ct_rank.p;
+            ct.deep = d.ct_deep;
+            ct.cold = d.ct_hot < d.S;
         }
         s->walk_pool_blocks = s->eargs.pool_blocks;
         zero_later(s, s->xev_pool.p, sizeof(std::uint32_t));
@@ -2132,7 +2159,7 @@ int acg_automaton_filter_info(const acg_automaton* a, std::uint32_t* q, double* 
 int acg_automaton_ctab_check(const acg_automaton* a, const std::uint8_t* text, std::uint64_t n, std::uint32_t* info,
                              std::uint64_t* mismatches, std::uint64_t* cold_steps) {
     using namespace acg;
-    if (info) info[0] = info[1] = info[2] = info[3] = 0;
+    if (info) info[0] = info[1] = info[2] = info[3] = info[4] = 0;
     if (mismatches) *mismatches = 0;
     if (cold_steps) *cold_steps = 0;
     if (!a) return 0;
@@ -2152,16 +2179,23 @@ int acg_automaton_ctab_check(const acg_automaton* a, const std::uint8_t* text, s
         std::uint32_t ents = 0;
         for (std::uint32_t i = 0; i < slots; ++i) ents += d.ctab[i] != kCtEmpty;
         info[3] = ents;
+        info[4] = d.ct_deep ? 1u : 0u;
     }
     if (!text) return 1;
     // the device walk (exact_kernels.cuh: ctab_event_kernel), step for step
     std::uint64_t bad = 0, cold = 0;
     std::uint32_t c1 = esc, c2 = esc, s_dev = 0;
     std::uint32_t sw = d.ctab[slots + (D == 3 ? (K * K + K + 1) : (K + 1)) * esc];
+    std::uint32_t xprev = sw;  // the previous position's T_D default (deep default)
     for (std::uint64_t i = 0; i < n; ++i) {
         const std::uint32_t c = d.symmap[text[i]];
         const std::uint32_t idx = D == 3 ? (c2 * K + c1) * K + c : c1 * K + c;
-        const std::uint32_t x = d.ctab[slots + idx];
+        std::uint32_t x = d.ctab[slots + idx];
+        if (d.ct_deep) {
+            const std::uint32_t e2 = d.ctab[(xprev & kCtValMask) + c] ^ (c << kCtColShift);
+            xprev = x;
+            if (!(e2 & kCtColMask)) x = e2;
+        }
         c2 = c1;
         c1 = c;
         std::uint32_t nx;

@@ -513,12 +513,13 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
 // exception entries of the hottest states, sized for `budget` bytes of shared
 // memory. Leaves d.ctab empty when the scheme does not apply.
 static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_order, std::size_t budget, Dfa& d,
-                         std::uint32_t hot_limit) {
+                         std::uint32_t hot_limit, const std::vector<std::uint64_t>* visits) {
     d.ctab.clear();
     d.ct_rank.clear();
     d.ct_sw.clear();
     d.ct_next.clear();
     d.ct_slots = d.ct_D = d.ct_hot = 0;
+    d.ct_deep = false;
     const std::uint32_t S = d.S, K = d.K;
     const std::uint32_t n_out = d.Cn - d.Hn;
     if (d.mode != kAlphaGeneric || K > kCtMaxK || K < 2 || S <= d.H) return;  // (all states in the dense hot rows: KE has no cold steps)
@@ -532,19 +533,23 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     if (slots + n_out >= kCtValMask) return;
     const std::vector<std::uint32_t>& delta = nfa.delta;
     auto has_out = [&](std::uint32_t s) { return nfa.out_off[s + 1] > nfa.out_off[s]; };
-    // exception columns of state s as a bit mask
+    const std::uint32_t max_ids = slots - K + 1;
+    std::vector<std::uint32_t> masks, id_of, order_nfa;
+    bool deep = false;
+    // exception columns of state s as a bit mask. Plain: targets deeper than D.
+    // Deep (the default itself takes one more level from the table, ctab.hpp):
+    // targets deeper than D + 1, plus the depth-(D+1) children of depth-D states.
     auto exc_mask = [&](std::uint32_t s) {
         std::uint32_t m = 0;
         const std::size_t row = static_cast<std::size_t>(s) * K;
-        for (std::uint32_t c = 0; c < K; ++c)
-            if (nfa.depth[delta[row + c]] > D) m |= 1u << c;
+        const std::uint32_t ds = nfa.depth[s];
+        for (std::uint32_t c = 0; c < K; ++c) {
+            const std::uint32_t dt = nfa.depth[delta[row + c]];
+            if (deep ? (dt > D + 1 || (dt == D + 1 && ds == D)) : dt > D) m |= 1u << c;
+        }
         return m;
     };
-    // candidate prefix of the hot order: rows whose exceptions fill at most `fill` of the slots
-    std::vector<std::uint32_t> masks;
-    masks.reserve(std::min<std::size_t>(S, slots));
-    const std::uint32_t max_ids = slots - K + 1;
-    auto try_place = [&](std::size_t n_hot, std::vector<std::uint32_t>& id_of) -> bool {
+    auto try_place = [&](std::size_t n_hot) -> bool {
         // first-fit row displacement, largest rows first (occupancy and id bitsets)
         std::vector<std::uint64_t> occ((slots + 64 + 63) / 64 + 1, 0), idu((slots + 63) / 64 + 1, 0);
         std::vector<std::uint32_t> order(n_hot);
@@ -588,23 +593,60 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
         }
         return true;
     };
-    std::size_t n_hot = 0;
-    std::vector<std::uint32_t> id_of;
-    for (double fill = 0.94; fill > 0.3; fill -= 0.06) {
-        const std::uint64_t cap = static_cast<std::uint64_t>(fill * slots);
-        std::uint64_t used = 0;
-        n_hot = 0;
-        masks.clear();
-        while (n_hot < S && n_hot < max_ids && (!hot_limit || n_hot < hot_limit)) {  // (hot_limit: diagnostics, cold paths)
-            const std::uint32_t m = exc_mask(hot_order[n_hot]);
-            const std::uint32_t k = static_cast<std::uint32_t>(__builtin_popcount(m));
-            if (used + k > cap) break;
-            used += k;
-            masks.push_back(m);
-            ++n_hot;
+    // the longest prefix of `order_nfa` whose exceptions fill at most `fill` of the slots and that places
+    auto choose = [&](std::size_t must) -> std::size_t {
+        for (double fill = 0.94; fill > 0.3; fill -= 0.06) {
+            const std::uint64_t cap = static_cast<std::uint64_t>(fill * slots);
+            std::uint64_t used = 0;
+            std::size_t n_hot = 0;
+            masks.clear();
+            while (n_hot < S && n_hot < max_ids && (!hot_limit || n_hot < hot_limit)) {  // (hot_limit: diagnostics, cold paths)
+                const std::uint32_t m = exc_mask(order_nfa[n_hot]);
+                const std::uint32_t k = static_cast<std::uint32_t>(__builtin_popcount(m));
+                if (used + k > cap) break;
+                used += k;
+                masks.push_back(m);
+                ++n_hot;
+            }
+            if (n_hot < must) return 0;
+            if (n_hot && try_place(n_hot)) return n_hot;
         }
-        if (n_hot && try_place(n_hot, id_of)) break;
-        n_hot = 0;
+        return 0;
+    };
+    // Plain default when a visit profile says its hot set takes >= 99.5 % of the
+    // steps (3 loads per step; measured on cfg3: 4.27 ms per 2 GiB against 4.53
+    // for the deep default's 4 loads); else the deep default, which holds far
+    // more states (all of cfg3's): every state of depth <= D must then be hot
+    // (their rows carry the default's extra level).
+    std::size_t n_hot = 0;
+    if (visits && visits->size() == S) {
+        order_nfa = hot_order;
+        n_hot = choose(1);
+        unsigned long long in = 0, all = 0;
+        for (std::size_t i = 0; i < S; ++i) {
+            all += (*visits)[order_nfa[i]];
+            if (i < n_hot) in += (*visits)[order_nfa[i]];
+        }
+        if (!n_hot || (n_hot < S && static_cast<double>(in) < 0.995 * static_cast<double>(all))) n_hot = 0;
+    }
+    if (!n_hot) {
+        std::size_t shallow = 0;
+        order_nfa.clear();
+        order_nfa.reserve(S);
+        for (std::uint32_t s : nfa.bfs) {
+            if (nfa.depth[s] > D) break;
+            order_nfa.push_back(s);
+        }
+        shallow = order_nfa.size();
+        for (std::uint32_t s : hot_order)
+            if (nfa.depth[s] > D) order_nfa.push_back(s);
+        deep = true;
+        n_hot = choose(shallow);
+        if (!n_hot) {
+            deep = false;
+            order_nfa = hot_order;
+            n_hot = choose(1);
+        }
     }
     if (!n_hot) return;
     // state words (device order) and the id -> rank table
@@ -613,7 +655,7 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     std::vector<std::uint32_t> sw_nfa(S);
     std::vector<std::uint8_t> is_hot(S, 0);
     for (std::size_t i = 0; i < n_hot; ++i) {
-        const std::uint32_t s = hot_order[i];
+        const std::uint32_t s = order_nfa[i];
         is_hot[s] = 1;
         sw_nfa[s] = id_of[i] | (has_out(s) ? kCtOut : 0u);
         if (has_out(s)) d.ct_rank[id_of[i]] = static_cast<std::uint16_t>(d.dev_of[s] - d.Hn);
@@ -624,7 +666,7 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     }
     d.ctab.assign(static_cast<std::size_t>(slots) + nd, kCtEmpty);
     for (std::size_t i = 0; i < n_hot; ++i) {
-        const std::uint32_t s = hot_order[i];
+        const std::uint32_t s = order_nfa[i];
         const std::size_t row = static_cast<std::size_t>(s) * K;
         for (std::uint32_t mm = masks[i]; mm; mm &= mm - 1) {
             const std::uint32_t c = static_cast<std::uint32_t>(__builtin_ctz(mm));
@@ -649,6 +691,7 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     d.ct_slots = slots;
     d.ct_D = D;
     d.ct_hot = static_cast<std::uint32_t>(n_hot);
+    d.ct_deep = deep;
 }
 
 void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& d,
@@ -772,7 +815,7 @@ void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector
             }
         });
     }
-    compile_ctab(nfa, hot_order, ctab_budget_bytes ? ctab_budget_bytes : hot_budget_bytes, d, hot_limit);
+    compile_ctab(nfa, hot_order, ctab_budget_bytes ? ctab_budget_bytes : hot_budget_bytes, d, hot_limit, visits);
     d.id_bits = 1;
     while ((1ull << d.id_bits) < nfa.n_patterns) ++d.id_bits;
     d.halo = (nfa.max_len + 15u) & ~15u;

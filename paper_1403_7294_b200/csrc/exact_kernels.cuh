@@ -284,6 +284,8 @@ struct CtabArgs {
     std::uint32_t slots;
     const std::uint32_t* next;    // S*K dense table, targets as state words (cold steps)
     const std::uint16_t* rank;    // id -> output rank (E1)
+    bool deep;                    // deep default (ctab.hpp)
+    bool cold;                    // some states are cold (else the walk carries no cold branch)
 };
 
 // A cold state word's step: the dense L2-resident table of state words. Out of
@@ -306,7 +308,7 @@ __device__ __forceinline__ std::uint32_t pinned_reg(std::uint32_t v) {
 
 // Thread block: 1024 threads at one stream per thread, 512 above (the columns
 // of a whole group of steps are held in registers).
-template <int U, int D>
+template <int U, int D, bool DEEP, bool COLD>
 __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel(const ScanArgs a, const EventArgs e,
                                                                                  const CtabArgs ct) {
     constexpr int GL = U <= 2 ? 16 : 8;  // steps per group: their columns are looked up together, ahead of the walk
@@ -346,10 +348,12 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
     }
 
     std::uint32_t st[U], wr[U], lim[U], cnt[U], p1[U], p2[U];  // p1/p2: 4 * the previous two columns
+    std::uint32_t xp[U];                                        // DEEP: the previous step's T_D default
     long long pos0[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         st[u] = root;
+        xp[u] = root;
         cnt[u] = 0;
         p1[u] = p2[u] = esc4;
         wr[u] = act[u] ? slab_start(e, cid[u]) : 0u;
@@ -419,18 +423,32 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
                     }
                     c4[u][j] = c;
                 }
-            std::uint32_t xn[U];
+            // xn = T_D default of the next step, en (DEEP) = the entry of the previous
+            // default's row for the next step's column: both loaded one step ahead
+            std::uint32_t xn[U], en[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) xn[u] = default_of(p2[u], p1[u], c4[u][0]);
+            for (int u = 0; u < U; ++u) {
+                xn[u] = default_of(p2[u], p1[u], c4[u][0]);
+                if (DEEP) en[u] = lds_u32(xp[u] * 4u + (c4[u][0] + tab_s));
+            }
 #pragma unroll
             for (int j = 0; j < GL; ++j) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const std::uint32_t c = c4[u][j], x = xn[u];
-                    if (j + 1 < GL) xn[u] = default_of(j ? c4[u][j - 1] : p1[u], c, c4[u][j + 1]);
+                    const std::uint32_t c = c4[u][j];
+                    std::uint32_t x = xn[u];
+                    if (DEEP) {  // one more level: the depth-(D+1) child of the previous default, if the text spells it
+                        const std::uint32_t d2 = en[u] ^ (c << (kCtColShift - 2));
+                        xp[u] = x;
+                        if (!(d2 & kCtColMask)) x = d2;
+                    }
+                    if (j + 1 < GL) {
+                        xn[u] = default_of(j ? c4[u][j - 1] : p1[u], c, c4[u][j + 1]);
+                        if (DEEP) en[u] = lds_u32(xp[u] * 4u + (c4[u][j + 1] + tab_s));
+                    }
                     const std::uint32_t sw = st[u];
                     std::uint32_t v;
-                    if (__builtin_expect((sw & kCtCold) != 0u, 0)) {
+                    if (COLD && __builtin_expect((sw & kCtCold) != 0u, 0)) {
                         v = ctab_cold_step(ct.next, K, ct.slots, a.Hn, sw, c);
                     } else {
                         const std::uint32_t ent = lds_u32(sw * 4u + (c + tab_s));  // (bit 31 of sw falls off the multiply)
@@ -678,11 +696,22 @@ __device__ __forceinline__ void for_event_batches(const EventArgs& e, long long 
     std::uint32_t p = slab_start(e, c), lim = slab_end(e, c) - 1u, done = 0;
     while (done < total) {
         const std::uint32_t here = min(total - done, lim - p);
-        for (std::uint32_t b = 0; b < here; b += 32) {
-            const std::uint32_t nb = min(32u, here - b);
-            const bool ok = static_cast<std::uint32_t>(lane) < nb;
-            const std::uint32_t v = ok ? __ldcs(e.ev + p + b + lane) : 0u;
-            f(done + b, nb, v, ok, p + b + lane);
+        // four batches' loads in flight per warp (one load per batch left each warp
+        // waiting a full memory round trip per 32 events: E1/E2 were latency-bound)
+        for (std::uint32_t b = 0; b < here; b += 128) {
+            std::uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const std::uint32_t i = b + 32u * k + lane;
+                v[k] = i < here ? __ldcs(e.ev + p + i) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const std::uint32_t b0 = b + 32u * k;
+                if (b0 >= here) break;
+                const std::uint32_t nb = min(32u, here - b0);
+                f(done + b0, nb, v[k], static_cast<std::uint32_t>(lane) < nb, p + b0 + lane);
+            }
         }
         done += here;
         if (done < total) {

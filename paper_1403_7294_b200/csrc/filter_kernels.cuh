@@ -183,7 +183,17 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
         ++lb;
     };
     const std::uint32_t qmul = qsh * kQMul0;  // window -> hash in one multiply (qfilter.hpp)
+#if !defined(ACG_KQ_NOPIN)
+    // qmask's PRMT takes its first byte table from a register: as a literal the compiler
+    // re-materialises it before nearly every probe (14 moves per block); a value it
+    // cannot know at compile time (n >= 0, so the XOR is with 0) stays in one register
+    const std::uint32_t bits_lo = 0x08040201u ^ static_cast<std::uint32_t>(static_cast<unsigned long long>(n) >> 63);
+    auto probe = [&](std::uint32_t h) -> std::uint32_t {
+        return __byte_perm(bits_lo, 0x80402010u, __umulhi(h, kQMul1) & 0x7777u) & ~tab[qword(h, words)];
+    };
+#else
     auto probe = [&](std::uint32_t h) -> std::uint32_t { return qmask(h) & ~tab[qword(h, words)]; };
+#endif
     auto window = [&](std::uint32_t lo, std::uint32_t hi, int o) -> std::uint32_t {
         return o == 0 ? lo : __funnelshift_r(lo, hi, 8 * o);
     };
@@ -261,7 +271,11 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
                         for (int o = 0; o < 4; ++o) {
                             const int i = 4 * r + o;
                             const std::uint32_t h2 = qhash2(window(cur[r], nb_[r], o) * qmul);
+#if !defined(ACG_KQ_NOPIN)
+                            m2[i] = __byte_perm(bits_lo, 0x80402010u, __umulhi(h2, kQMul1) & 0x7777u);
+#else
                             m2[i] = qmask(h2);
+#endif
                             v2[i] = t[i] == 0u ? __ldg(a.qbloom2 + qword(h2, a.qwords2)) : 0xFFFFFFFFu;
                         }
                     // pack the next block and issue its load while the probes are in flight

@@ -24,7 +24,8 @@ def test_cfg3_dictionary_walks_exactly():
     r = a.ctab_check(text)
     assert r["available"] and r["default_depth"] == 3
     assert r["mismatches"] == 0
-    assert r["hot_states"] > a.layout()["hot_rows"]  # more states than the dense hot rows hold
+    # the deep default makes the whole automaton hot (the dense rows hold a fifth of it)
+    assert r["deep"] and r["hot_states"] == a.layout()["states"] and r["cold_steps"] == 0
     assert r["entries"] <= r["slots"]
 
 
@@ -37,6 +38,8 @@ def test_profile_order_and_hot_limits_walk_exactly():
             a.set_hot_limit(limit)
         r = a.ctab_check(text)
         assert r["available"] and r["mismatches"] == 0
+        if limit in (1, 7, 300):
+            assert not r["deep"]  # every state of depth <= 3 must be hot for the deep default
         if limit:
             assert r["hot_states"] <= limit and r["cold_steps"] > 0
 
