@@ -200,6 +200,7 @@ struct DeviceDfa {
     // compressed hot automaton (ctab.hpp): shared-memory image, state words, id -> rank
     DevBuf<std::uint32_t> ctab, ct_next;
     DevBuf<std::uint16_t> ct_rank;
+    DevBuf<unsigned long long> ct_info;  // event payload (id, or slots + rank) -> packed output info
     std::uint32_t ctab_bytes = 0;
     int smem_optin = 0;
     int num_sms = 0;
@@ -313,6 +314,7 @@ struct acg_scanner {
     bool kc_geom = false;                                // ... and its geometry (short chunks walked in rounds)
     std::uint32_t walk_pool_blocks = 0;                  // pool blocks of the last walk's event slabs
     acg::kern::EventArgs eargs{};
+    acg::kern::CtabArgs cargs{};                         // KC's tables (E1/E2 map its event payloads)
     bool ev_run = false;
     unsigned long long xev_chunk = 0, xev_chunks = 0, xev_total = 0, xev_n = 0;
     std::uint32_t xev_min_pool = 0;
@@ -395,6 +397,14 @@ int get_device_dfa(const acg_automaton* a, int device, std::shared_ptr<DeviceDfa
         ACG_CUDA(upload(dd->ctab, img.data(), img.size(), up));
         ACG_CUDA(upload(dd->ct_next, d.ct_next.data(), d.ct_next.size(), up));
         ACG_CUDA(upload(dd->ct_rank, d.ct_rank.data(), d.ct_rank.size(), up));
+        {
+            const std::uint32_t n_out = d.Cn - d.Hn;
+            std::vector<unsigned long long> pinfo(static_cast<std::size_t>(d.ct_slots) + n_out, 0ull);
+            for (std::uint32_t i = 0; i < d.ct_slots; ++i)
+                if (d.ct_rank[i] != acg::kCtNoRank) pinfo[i] = d.outinfo[d.Hn + d.ct_rank[i]];
+            for (std::uint32_t r = 0; r < n_out; ++r) pinfo[d.ct_slots + r] = d.outinfo[d.Hn + r];
+            ACG_CUDA(upload(dd->ct_info, pinfo.data(), pinfo.size(), up));
+        }
     }
     if (!d.hotG.empty()) {
         dd->hotG_bytes = static_cast<std::uint32_t>((d.hotG.size() * 2 + 15) & ~std::size_t(15));
@@ -738,7 +748,21 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         // E2: events -> ordered records at each chunk's slot range
         const unsigned g = static_cast<unsigned>(
             std::max<unsigned long long>(1, std::min<unsigned long long>((s->n_chunks + 7) / 8, 16ull * dd.num_sms)));
-        acg::kern::event_expand_kernel<<<g, 256, 0, st>>>(wa, s->eargs);
+        // KC counted the records itself (no E1): E2 also takes the visit histogram, once
+        // (not when re-expanding after a record-buffer regrowth)
+        const bool vis = s->cargs.counted && (s->flags & ACG_SCAN_COUNTS) && !s->regrow;
+        if (vis) {
+            wa.visits = s->visits.p;
+            const std::size_t vb = static_cast<std::size_t>(s->eargs.n_out) * 4;
+            const unsigned gv = std::min<unsigned>(g, 4u * dd.num_sms);  // fewer blocks: each flushes its bins
+            auto k = acg::kern::event_expand_kernel<true, true>;
+            ACG_CUDA(prepare_smem(k, vb));
+            k<<<gv, 256, vb, st>>>(wa, s->eargs, s->cargs);
+        } else if (s->c_run) {
+            acg::kern::event_expand_kernel<true, false><<<g, 256, 0, st>>>(wa, s->eargs, s->cargs);
+        } else {
+            acg::kern::event_expand_kernel<false, false><<<g, 256, 0, st>>>(wa, s->eargs, s->cargs);
+        }
         ACG_CUDA(cudaGetLastError());
     } else if (s->scratch_run) {
         // slabs -> slot ranges; overflowed chunks are re-walked by the WRITE pass.
@@ -1340,7 +1364,8 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         s->g_run = sparseg_ok(s, n_out_states);
         s->c_run = !s->g_run && ctab_ok(s, n_out_states);
         ACG_CUDA(plan_events(s, s->g_run ? n_out_states + d.H : n_out_states, st));
-        acg::kern::CtabArgs ct{};
+        acg::kern::CtabArgs& ct = s->cargs;
+        ct = acg::kern::CtabArgs{};
         if (s->c_run) {  // event payloads are state-word values: ids, or slots + rank
             s->eargs.ob = bits_for(d.ct_slots + n_out_states);
             ct.image = dd.ctab.p;
@@ -1348,6 +1373,10 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             ct.slots = d.ct_slots;
             ct.next = dd.ct_next.p;
             ct.rank = dd.ct_rank.p;
+            ct.info = dd.ct_info.p;
+            ct.pay_mask = d.ct_cnt ? acg::kCtPayMask : acg::kCtValMask;
+            // list scans of counted words skip E1 (bins of the visit histogram must fit E2's shared memory)
+            ct.counted = d.ct_cnt && want_list && static_cast<std::size_t>(n_out_states) * 4 <= 96 * 1024;
             ct.deep = d.ct_deep;
             ct.cold = d.ct_hot < d.S;
         }
@@ -1403,6 +1432,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[1], st));
         }
         s->ev_run = true;
+        if (!(s->c_run && ct.counted)) {
         const std::size_t nb4 = static_cast<std::size_t>(n_out_states) * 4, nb1 = (n_out_states + 15u) & ~15u;
         const bool smem_bins = want_counts && nb4 <= kEventBinsMax;
         const bool smem_nout = (smem_bins ? nb4 : 0) + nb1 <= kEventBinsMax;
@@ -1429,6 +1459,7 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
         else ACG_CUDA(e1(acg::kern::event_count_kernel<false, false, false>));
         ACG_CUDA(cudaGetLastError());
         ++s->launches;
+        }
     } else {
         // single pass (count + per-chunk slabs) once the previous run told the
         // record density and the slabs fit the budget; count + write otherwise
@@ -2184,6 +2215,7 @@ int acg_automaton_ctab_check(const acg_automaton* a, const std::uint8_t* text, s
     if (!text) return 1;
     // the device walk (exact_kernels.cuh: ctab_event_kernel), step for step
     std::uint64_t bad = 0, cold = 0;
+    const std::uint32_t pay = d.ct_cnt ? kCtPayMask : kCtValMask;  // an id / payload without the count bits
     std::uint32_t c1 = esc, c2 = esc, s_dev = 0;
     std::uint32_t sw = d.ctab[slots + (D == 3 ? (K * K + K + 1) : (K + 1)) * esc];
     std::uint32_t xprev = sw;  // the previous position's T_D default (deep default)
@@ -2192,7 +2224,7 @@ int acg_automaton_ctab_check(const acg_automaton* a, const std::uint8_t* text, s
         const std::uint32_t idx = D == 3 ? (c2 * K + c1) * K + c : c1 * K + c;
         std::uint32_t x = d.ctab[slots + idx];
         if (d.ct_deep) {
-            const std::uint32_t e2 = d.ctab[(xprev & kCtValMask) + c] ^ (c << kCtColShift);
+            const std::uint32_t e2 = d.ctab[(xprev & pay) + c] ^ (c << kCtColShift);
             xprev = x;
             if (!(e2 & kCtColMask)) x = e2;
         }
@@ -2201,11 +2233,10 @@ int acg_automaton_ctab_check(const acg_automaton* a, const std::uint8_t* text, s
         std::uint32_t nx;
         if (sw & kCtCold) {
             ++cold;
-            const std::uint32_t v = sw & kCtValMask;
-            const std::uint32_t s = (sw & kCtOut) ? v - slots + d.Hn : v;
+            const std::uint32_t s = (sw & kCtOut) ? (sw & pay) - slots + d.Hn : (sw & kCtValMask);
             nx = d.ct_next[static_cast<std::size_t>(s) * K + c];
         } else {
-            const std::uint32_t ent = d.ctab[(sw & kCtValMask) + c];
+            const std::uint32_t ent = d.ctab[(sw & pay) + c];
             const std::uint32_t diff = ent ^ (c << kCtColShift);
             nx = (diff & kCtColMask) ? x : diff;
         }

@@ -520,6 +520,7 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     d.ct_next.clear();
     d.ct_slots = d.ct_D = d.ct_hot = 0;
     d.ct_deep = false;
+    d.ct_cnt = false;
     const std::uint32_t S = d.S, K = d.K;
     const std::uint32_t n_out = d.Cn - d.Hn;
     if (d.mode != kAlphaGeneric || K > kCtMaxK || K < 2 || S <= d.H) return;  // (all states in the dense hot rows: KE has no cold steps)
@@ -649,6 +650,13 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
         }
     }
     if (!n_hot) return;
+    // counted words: the output count above a 17-bit payload (cold non-output words keep a plain device id)
+    std::uint32_t max_out = 0;
+    for (std::uint32_t s = 0; s < S; ++s) max_out = std::max(max_out, nfa.out_off[s + 1] - nfa.out_off[s]);
+    const bool cnt = slots + n_out <= kCtPayMask && max_out < 255;
+    auto out_bits = [&](std::uint32_t s) {
+        return has_out(s) ? kCtOut | (cnt ? (nfa.out_off[s + 1] - nfa.out_off[s]) << kCtPayBits : 0u) : 0u;
+    };
     // state words (device order) and the id -> rank table
     d.ct_sw.assign(S, 0);
     d.ct_rank.assign(slots, static_cast<std::uint16_t>(kCtNoRank));
@@ -657,11 +665,11 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     for (std::size_t i = 0; i < n_hot; ++i) {
         const std::uint32_t s = order_nfa[i];
         is_hot[s] = 1;
-        sw_nfa[s] = id_of[i] | (has_out(s) ? kCtOut : 0u);
+        sw_nfa[s] = id_of[i] | out_bits(s);
         if (has_out(s)) d.ct_rank[id_of[i]] = static_cast<std::uint16_t>(d.dev_of[s] - d.Hn);
     }
     for (std::uint32_t s = 0; s < S; ++s) {
-        if (!is_hot[s]) sw_nfa[s] = kCtCold | (has_out(s) ? kCtOut | (slots + d.dev_of[s] - d.Hn) : d.dev_of[s]);
+        if (!is_hot[s]) sw_nfa[s] = kCtCold | (has_out(s) ? out_bits(s) | (slots + d.dev_of[s] - d.Hn) : d.dev_of[s]);
         d.ct_sw[d.dev_of[s]] = sw_nfa[s];
     }
     d.ctab.assign(static_cast<std::size_t>(slots) + nd, kCtEmpty);
@@ -692,6 +700,7 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     d.ct_D = D;
     d.ct_hot = static_cast<std::uint32_t>(n_hot);
     d.ct_deep = deep;
+    d.ct_cnt = cnt;
 }
 
 void compile_dfa(const Nfa& nfa, std::size_t hot_budget_bytes, const std::vector<std::uint64_t>* visits, Dfa& d,

@@ -98,6 +98,7 @@ struct Dfa {
     // = ct_slots row-displaced exception entries, then the K^ct_D default table.
     std::vector<std::uint32_t> ctab;
     std::uint32_t ct_slots = 0, ct_D = 0, ct_hot = 0;  // slots (= id space), default depth, hot states
+    bool ct_cnt = false;                 // counted state words (output count in bits 17-24, ctab.hpp)
     bool ct_deep = false;                // the default takes one more level from the rows of the depth-D states
     std::vector<std::uint16_t> ct_rank;  // ct_slots: id -> output rank (kCtNoRank: none)
     std::vector<std::uint32_t> ct_sw;    // S: device state -> state word

@@ -39,8 +39,13 @@
 // bit 30 cold, bit 31 has outputs.
 //   hot:  value = id (slot index < slots)
 //   cold: value = slots + output rank (output states), else the device id
-// An output visit logs the event payload `value` (hot: id, cold output: slots +
-// rank); E1 maps payloads back to output ranks (id -> rank table).
+// An output visit logs the event payload (hot: id, cold output: slots + rank);
+// E1 / E2 map payloads back to output ranks (id -> rank table).
+// Counted words (Dfa::ct_cnt: every payload < 2^16 and every output list
+// shorter than 255): byte 2 of an output state's word holds its output count,
+// the payload is bits 0-15 — the walk then sums each chunk's record count
+// itself (one PRMT and one add per logged step) and the separate counting pass
+// (E1) is not run for list scans; E2 takes the visit histogram.
 #pragma once
 
 #include <cstdint>
@@ -56,5 +61,7 @@ constexpr std::uint32_t kCtOut = 0x80000000u;
 constexpr std::uint32_t kCtEmpty = kCtColMask;   // column 31, value 0: matches no column
 constexpr std::uint32_t kCtDefaultMaxBytes = 40 * 1024;  // T_D table bound (K^D u32 entries)
 constexpr std::uint32_t kCtNoRank = 0xFFFFu;
+constexpr std::uint32_t kCtPayBits = 16;         // counted words: payload bits; the output count is byte 2
+constexpr std::uint32_t kCtPayMask = (1u << kCtPayBits) - 1u;
 
 }  // namespace acg

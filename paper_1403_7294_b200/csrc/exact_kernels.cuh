@@ -284,17 +284,20 @@ struct CtabArgs {
     std::uint32_t slots;
     const std::uint32_t* next;    // S*K dense table, targets as state words (cold steps)
     const std::uint16_t* rank;    // id -> output rank (E1)
+    const unsigned long long* info;  // event payload -> the state's packed output info (E2)
+    std::uint32_t pay_mask;       // payload bits of a state word (kCtPayMask for counted words, else kCtValMask)
     bool deep;                    // deep default (ctab.hpp)
     bool cold;                    // some states are cold (else the walk carries no cold branch)
+    bool counted;                 // counted words AND this run skips E1: the walk writes chunk_counts and the event total
 };
 
 // A cold state word's step: the dense L2-resident table of state words. Out of
 // line so the walk's straight-line code carries one branch, not its address
 // arithmetic (cold steps are rare: the table holds every state that matters).
 __device__ __noinline__ std::uint32_t ctab_cold_step(const std::uint32_t* next, std::uint32_t K, std::uint32_t slots,
-                                                     std::uint32_t Hn, std::uint32_t sw, std::uint32_t c4) {
-    const std::uint32_t v = sw & kCtValMask;
-    const std::uint32_t s = (sw & kCtOut) ? v - slots + Hn : v;
+                                                     std::uint32_t Hn, std::uint32_t pay_mask, std::uint32_t sw,
+                                                     std::uint32_t c4) {
+    const std::uint32_t s = (sw & kCtOut) ? (sw & pay_mask) - slots + Hn : (sw & kCtValMask);
     return __ldg(next + static_cast<std::size_t>(s) * K + (c4 >> 2));
 }
 
@@ -329,6 +332,10 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
     const long long halo = a.halo, steps = a.halo + a.chunk, n = a.n;
     std::uint32_t* __restrict__ ev = e.ev;
     const std::uint32_t root = lds_u32(def_s + (D == 3 ? (KK + K + 1u) : (K + 1u)) * esc4);  // T_D[esc, .., esc]
+    // a state word as the walk carries it: id / payload and the two flags (the
+    // count byte and the entry's column field are dropped before the next address)
+    const std::uint32_t amask = ct.pay_mask | kCtCold | kCtOut;
+    unsigned long long evs = 0;  // events logged by this thread (sizes the next run's slabs)
 
     // Rounds: in round r the grid walks the chunks [r, r+1) * gridDim * blockDim * U,
     // neighbouring lanes on neighbouring chunks — the text a warp reads at any
@@ -349,12 +356,14 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
 
     std::uint32_t st[U], wr[U], lim[U], cnt[U], p1[U], p2[U];  // p1/p2: 4 * the previous two columns
     std::uint32_t xp[U];                                        // DEEP: the previous step's T_D default
+    std::uint32_t recs[U];                                      // records of the chunk (counted words: byte 2)
     long long pos0[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        st[u] = root;
-        xp[u] = root;
+        st[u] = root & amask;
+        xp[u] = root & amask;
         cnt[u] = 0;
+        recs[u] = 0;
         p1[u] = p2[u] = esc4;
         wr[u] = act[u] ? slab_start(e, cid[u]) : 0u;
         lim[u] = act[u] ? slab_end(e, cid[u]) - 1u : 0u;
@@ -429,17 +438,17 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 xn[u] = default_of(p2[u], p1[u], c4[u][0]);
-                if (DEEP) en[u] = lds_u32(xp[u] * 4u + (c4[u][0] + tab_s));
+                if (DEEP) en[u] = lds_u32(xp[u] * 4u + (c4[u][0] + tab_s));  // (xp is masked: no count byte)
             }
 #pragma unroll
             for (int j = 0; j < GL; ++j) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const std::uint32_t c = c4[u][j];
-                    std::uint32_t x = xn[u];
+                    std::uint32_t x = xn[u];  // (full word: its count byte is read when the step logs)
                     if (DEEP) {  // one more level: the depth-(D+1) child of the previous default, if the text spells it
                         const std::uint32_t d2 = en[u] ^ (c << (kCtColShift - 2));
-                        xp[u] = x;
+                        xp[u] = x & amask;
                         if (!(d2 & kCtColMask)) x = d2;
                     }
                     if (j + 1 < GL) {
@@ -448,16 +457,23 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
                     }
                     const std::uint32_t sw = st[u];
                     std::uint32_t v;
+                    std::uint32_t full;  // the next state's full word (count byte included)
                     if (COLD && __builtin_expect((sw & kCtCold) != 0u, 0)) {
-                        v = ctab_cold_step(ct.next, K, ct.slots, a.Hn, sw, c);
+                        full = ctab_cold_step(ct.next, K, ct.slots, a.Hn, ct.pay_mask, sw, c);
+                        v = full & amask;
                     } else {
-                        const std::uint32_t ent = lds_u32(sw * 4u + (c + tab_s));  // (bit 31 of sw falls off the multiply)
-                        const std::uint32_t diff = ent ^ (c << (kCtColShift - 2));
-                        v = (diff & kCtColMask) ? x : diff;
+                        const std::uint32_t ent = lds_u32(sw * 4u + (c + tab_s));  // (bits 30-31 of sw fall off the multiply)
+                        const std::uint32_t cx = c << (kCtColShift - 2);
+                        const bool miss = ((ent ^ cx) & kCtColMask) != 0u;
+                        v = miss ? (x & amask) : ((ent ^ cx) & amask);
+                        full = miss ? x : ent;
                     }
                     st[u] = v;
                     if (LOG) {
-                        if (v & live[u]) ev[wr[u]++] = kk + (v & kCtValMask);
+                        if (v & live[u]) {
+                            ev[wr[u]++] = kk + (v & ct.pay_mask);
+                            recs[u] += __byte_perm(full, 0u, 0x4442u);
+                        }
                     }
                 }
                 if (LOG) kk += kinc;
@@ -485,8 +501,17 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (act[u]) e.ev_count[cid[u]] = cnt[u];
+        if (act[u]) {
+            e.ev_count[cid[u]] = cnt[u];
+            if (ct.counted) a.chunk_counts[cid[u]] = recs[u];  // (else E1 counts them)
+            evs += cnt[u];
+        }
     }  // rounds
+    if (ct.counted) {  // E1 is not run: the run's event total from here
+#pragma unroll
+        for (int o = 16; o; o >>= 1) evs += __shfl_xor_sync(0xFFFFFFFFu, evs, o);
+        if ((threadIdx.x & 31) == 0 && evs) atomicAdd(e.ev_total, evs);
+    }
 }
 
 // ====================================================== SPARSE-G (generic) ==
@@ -733,8 +758,8 @@ __device__ __forceinline__ std::uint32_t n_out_of(std::uint32_t s, unsigned long
 // (SMEM_NOUT: each output state's output count, as a byte (255 = look it up),
 // staged after the bins: the events' record counts need no L2 lookups)
 // (XL: the walk was KC — event payloads are state-word values (ctab.hpp); they
-// are mapped to output ranks here, through the id -> rank table (staged in
-// shared memory when xl_smem), and the events rewritten in place for E2)
+// are mapped to output ranks through the id -> rank table, staged in shared
+// memory when xl_smem)
 template <bool SMEM_BINS, bool SMEM_NOUT, bool XL>
 __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, const EventArgs e, const CtabArgs ct,
                                                           const bool xl_smem) {
@@ -767,10 +792,8 @@ __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, cons
             for_event_batches(e, c, total, lane, [&](std::uint32_t, std::uint32_t, std::uint32_t v, bool ok, std::uint32_t slot) {
                 if (!ok || v == kEvPad) return;
                 std::uint32_t r = v & rmask;
-                if (XL) {
-                    r = r < ct.slots ? (xl_smem ? xrank[r] : __ldg(ct.rank + r)) : r - ct.slots;
-                    e.ev[slot] = (v & ~rmask) | r;
-                }
+                if (XL) r = r < ct.slots ? (xl_smem ? xrank[r] : __ldg(ct.rank + r)) : r - ct.slots;
+                (void)slot;
                 const std::uint32_t s = state_of_rank(r, H, Hn, Cn);
                 std::uint32_t no = SMEM_NOUT ? nout8[r] : 255u;
                 if (no == 255u) no = n_out_of(s, __ldg(a.outinfo + s), a);
@@ -796,12 +819,21 @@ __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, cons
 // ===================================================================== E2 ==
 // One warp per chunk with records: the events' records at the chunk's slot
 // range, written by consecutive lanes (coalesced).
-__global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, const EventArgs e) {
+// (XL: KC's payloads index a payload -> output-info table directly)
+// (VIS: also the per-output-state visit histogram, in shared-memory bins —
+// when KC counted the records itself and E1 is not run)
+template <bool XL, bool VIS>
+__global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, const EventArgs e, const CtabArgs ct) {
+    extern __shared__ std::uint32_t vbins[];
+    if (VIS) {
+        for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x) vbins[i] = 0;
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31;
     const long long wpb = blockDim.x >> 5;
     const long long warps = static_cast<long long>(gridDim.x) * wpb;
     const std::uint32_t rmask = (1u << e.ob) - 1u, H = a.H, Hn = a.Hn, Cn = a.Cn;
-    if (!ev_pool_ok(e)) return;
+    if (!ev_pool_ok(e)) return;  // (block-uniform)
     for (long long c = static_cast<long long>(blockIdx.x) * wpb + (threadIdx.x >> 5); c < a.n_chunks; c += warps) {
         const std::uint32_t total = e.ev_count[c];
         if (!total) continue;
@@ -811,10 +843,15 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
             std::uint32_t n = 0, lo = 0, first = 0;
             unsigned long long key = 0;
             if (ok && v != kEvPad) {
-                const std::uint32_t s = state_of_rank(v & rmask, H, Hn, Cn);
-                const unsigned long long info = __ldg(a.outinfo + s);
+                const std::uint32_t pay = v & rmask;
+                const unsigned long long info = XL ? __ldg(ct.info + pay) : __ldg(a.outinfo + state_of_rank(pay, H, Hn, Cn));
                 lo = static_cast<std::uint32_t>(info);
-                n = n_out_of(s, info, a);
+                n = static_cast<std::uint32_t>(info >> 32) & 0xFFu;
+                if (n == 255u || VIS) {
+                    const std::uint32_t r = XL ? (pay < ct.slots ? __ldg(ct.rank + pay) : pay - ct.slots) : pay;
+                    if (n == 255u) n = n_out_of(state_of_rank(r, H, Hn, Cn), info, a);  // a long list: its length from the CSR offsets
+                    if (VIS) atomicAdd(&vbins[r], 1u);
+                }
                 first = static_cast<std::uint32_t>(info >> 40);
                 if (!(first || a.id_bits <= 24)) first = __ldg(a.out_ids + lo);
                 key = (cbase + (v >> e.ob)) << a.id_bits;
@@ -833,6 +870,21 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
                 if (lane >= d) incl += y;
             }
             const std::uint32_t T = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            // short output lists (cfg3: one to three ids per state): every lane writes
+            // its own event's records at its prefix — neighbouring lanes, neighbouring
+            // slots — in max(n) rounds; long lists (cfg4) take the balanced search below
+            const std::uint32_t nmax = __reduce_max_sync(0xFFFFFFFFu, n);
+            if (nmax <= 4u) {
+                const unsigned long long at = o + (incl - n);
+                for (std::uint32_t k = 0; k < nmax; ++k) {
+                    if (k < n) {
+                        const std::uint32_t id = k == 0 ? first : __ldg(a.out_ids + lo + k);
+                        if (at + k < a.rec_cap) a.records[at + k] = key | id;
+                    }
+                }
+                o += T;
+                return;
+            }
             for (std::uint32_t t0 = 0; t0 < T; t0 += 32) {
                 const std::uint32_t t = t0 + lane;
                 // owner j = the first lane with incl_j > t (binary search over the scan)
@@ -855,6 +907,11 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
             }
             o += T;
         });
+    }
+    if (VIS) {
+        __syncthreads();
+        for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x)
+            if (vbins[i]) atomicAdd(a.visits + i, static_cast<unsigned long long>(vbins[i]));
     }
 }
 
