@@ -54,7 +54,7 @@ METRIC = "AC text-scan GB/s"
 STAGES = {
     "filter": ("KQ_filter", "V1_confirm", "unused", "unused", "ORDER"),
     "sparse": ("K1s_walk", "K1f_fixup", "K2_prefix", "K3_write", "K4_counts"),
-    "exact": ("K1x_walk", "none", "K2_prefix", "K3_write", "K4_counts"),
+    "exact": ("walk", "E1_count", "K2_prefix", "E2_expand", "K4_counts"),
 }
 
 
@@ -390,6 +390,7 @@ def main() -> None:
     else:
         counts = sc.pattern_counts()
     mode_name, ev_rate = sc.last_mode()
+    walk_name = sc.last_walk()  # exact mode: dense hot rows (KE) or the compressed hot automaton (KC)
     geo = sc.geometry()
     # per-stage times: profiled steps right after the timed region (same scanner,
     # stream, inputs and pipeline; CUDA events between the stages)
@@ -465,7 +466,7 @@ def main() -> None:
     achieved = alg_bytes / (ms_per_step * 1e-3) / 1e9
     stage_names = STAGES.get(mode_name, STAGES["exact"])
     kname = {"sparse": "sparse_scan_kernel (K1s)", "filter": "qfilter_ldg_kernel (KQ)"}.get(
-        mode_name, "exact_scan_kernel (K1x)")
+        mode_name, "ctab_event_kernel (KC)" if walk_name == "ctab" else "exact_event_kernel (KE)")
     k_top = float(k_ms[0])
     traffic = None
     tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
@@ -496,6 +497,7 @@ def main() -> None:
                           else "text per GPU fits L2: no flush (small parity config)"),
                    "parallelism": f"text shards x{world} ({scaling} scaling, halo {lay['halo']} B), DFA replicated",
                    "scan_mode": mode_name, "mode_requested": args.mode,
+                   "exact_walk": walk_name if mode_name == "exact" else None,
                    "excursion_event_rate": round(ev_rate, 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,

@@ -754,7 +754,11 @@ int enqueue_write(acg_scanner* s, cudaStream_t st) {
         if (vis) {
             wa.visits = s->visits.p;
             const std::size_t vb = static_cast<std::size_t>(s->eargs.n_out) * 4;
-            const unsigned gv = std::min<unsigned>(g, 4u * dd.num_sms);  // fewer blocks: each flushes its bins
+            static const unsigned vis_bps = [] {  // ACG_E2_VIS_BLOCKS: experiments
+                const char* e = std::getenv("ACG_E2_VIS_BLOCKS");
+                return e ? static_cast<unsigned>(std::atoi(e)) : 8u;  // (cfg3: 2 -> 2.55 ms, 4 -> 1.48, 6 -> 1.82, 8 -> 1.45)
+            }();
+            const unsigned gv = std::min<unsigned>(g, vis_bps * dd.num_sms);  // fewer blocks: each flushes its bins
             auto k = acg::kern::event_expand_kernel<true, true>;
             ACG_CUDA(prepare_smem(k, vb));
             k<<<gv, 256, vb, st>>>(wa, s->eargs, s->cargs);

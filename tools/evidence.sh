@@ -18,11 +18,18 @@ if [ -z "$NO_NCU" ]; then
   timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg1.csv \
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_launch.log 2>&1
-  C3="python tools/exact_probe.py 3 256 exact both profile 2 1024"
-  timeout 300 $C3 > $O/plain_ke3.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"exact_event_kernel|event_count|event_expand" \
-      -s 12 -c 3 -o /tmp/ke3 -f $C3 > $O/ncu_ke3.log 2>&1
-  ncu -i /tmp/ke3.ncu-rep --page raw --csv > $O/ncu_ke3_raw.csv 2>/dev/null
-  ncu -i /tmp/ke3.ncu-rep --page details --csv > $O/ncu_ke3_details.csv 2>/dev/null
+  # --set full of the cfg1 step's kernels (KQ, V1, ORDER) at the bench's size
+  C1="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"qfilter_ldg|qconfirm_region|qorder_region" \
+      -s 9 -c 3 -o /tmp/kq1 -f $C1 > $O/ncu_kq1.log 2>&1
+  ncu -i /tmp/kq1.ncu-rep --page raw --csv > $O/ncu_cfg1_raw.csv 2>/dev/null
+  ncu -i /tmp/kq1.ncu-rep --page details --csv > $O/ncu_cfg1_details.csv 2>/dev/null
+  # --set full of the EXACT walk over the compressed hot automaton (KC) + E2 on cfg3 at the bench's full size
+  C3="python tools/exact_probe.py 3 2048 exact both profile 0"
+  timeout 300 $C3 > $O/plain_kc3.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ctab_event_kernel|exact_event_kernel|event_count|event_expand" \
+      -s 8 -c 2 -o /tmp/kc3 -f $C3 > $O/ncu_kc3.log 2>&1
+  ncu -i /tmp/kc3.ncu-rep --page raw --csv > $O/ncu_kc_cfg3_raw.csv 2>/dev/null
+  ncu -i /tmp/kc3.ncu-rep --page details --csv > $O/ncu_kc_cfg3_details.csv 2>/dev/null
 fi
 echo done
