@@ -593,14 +593,21 @@ double scratch_budget(double held) {
 // KQ geometry: NW warps per SM, R blocks in flight per warp. ACG_QKERNEL
 // picks another instantiation (experiments only).
 struct QKernelChoice {
-    int nw = 16, r = 2;
+    int nw = 20, r = 2;  // 20 warps at 96 registers: cfg1 0.2311 -> 0.2276 ms/step, cfg2 3.15 -> 3.07 against 16 at 118
 };
 QKernelChoice qfilter_choice() {
     static const QKernelChoice c = [] {
         QKernelChoice q;
         const char* e = std::getenv("ACG_QKERNEL");
-        if (e && std::strcmp(e, "16x3") == 0) q.r = 3;
+        if (e && std::strcmp(e, "16x3") == 0) q.nw = 16, q.r = 3;
         else if (e && std::strcmp(e, "24x2") == 0) q.nw = 24;
+        else if (e && std::strcmp(e, "24x1") == 0) q.nw = 24, q.r = 1;
+        else if (e && std::strcmp(e, "16x2") == 0) q.nw = 16;
+        // the experimental pipelines (fused / post-confirm / bitmap level 1) exist at 16x2 only
+        for (const char* sw : {"ACG_QFUSED", "ACG_QPOST", "ACG_QBITMAP"}) {
+            const char* v = std::getenv(sw);
+            if (v && v[0] == '1') q.nw = 16, q.r = 2;
+        }
         return q;
     }();
     return c;
@@ -682,10 +689,27 @@ cudaError_t launch_qfilter(const ScanArgs& a, int sms, cudaStream_t st) {
         if (a.qbm) return launch_q(qfilter_ldg_kernel<16, 2, false, false, true, true>, a, 32 * 16, bloom, sms, st);
         return launch_q(qfilter_ldg_kernel<16, 2, false, false, false, true>, a, 32 * 16, bloom, sms, st);
     }
-    if (a.qbloom2) return launch_q(qfilter_ldg_kernel<16, 2, true, false>, a, 32 * 16, bloom, sms, st);
+    if (a.qbloom2 && c.nw == 24 && c.r == 1) return launch_q(qfilter_ldg_kernel<24, 1, true, false, false, false, 25>, a, 32 * 24, bloom, sms, st);
+    if (a.qbloom2 && c.nw == 20) return launch_q(qfilter_ldg_kernel<20, 2, true, false, false, false, 25>, a, 32 * 20, bloom, sms, st);
+    if (a.qbloom2) {
+        static const int ldv = [] {  // ACG_Q2LD: level-2 probe load flavour (experiments)
+            const char* e = std::getenv("ACG_Q2LD");
+            return e ? std::atoi(e) : 25;  // .cg probes (no L1 allocation), L1::no_allocate text: cfg2 0.956 -> 0.80 ms per 2 GiB
+        }();
+        if (ldv == 0) return launch_q(qfilter_ldg_kernel<16, 2, true, false>, a, 32 * 16, bloom, sms, st);
+        return launch_q(qfilter_ldg_kernel<16, 2, true, false, false, false, 25>, a, 32 * 16, bloom, sms, st);
+    }
     if (a.qbm) return launch_q(qfilter_ldg_kernel<16, 2, false, false, true>, a, 32 * 16, bloom, sms, st);
     if (c.nw == 24) return launch_q(qfilter_ldg_kernel<24, 2, false, false>, a, 32 * 24, bloom, sms, st);
     if (c.r == 3) return launch_q(qfilter_ldg_kernel<16, 3, false, false>, a, 32 * 16, bloom, sms, st);
+    {
+        static const int tld = [] {  // ACG_QTLD: text load flavour (experiments)
+            const char* e = std::getenv("ACG_QTLD");
+            return e ? std::atoi(e) : 3;  // L1::no_allocate (cfg1 KQ 0.2188 -> 0.2166 ms against ld.global.cs)
+        }();
+        if (c.nw == 20) return launch_q(qfilter_ldg_kernel<20, 2, false, false, false, false, 24>, a, 32 * 20, bloom, sms, st);
+        if (tld == 3) return launch_q(qfilter_ldg_kernel<16, 2, false, false, false, false, 24>, a, 32 * 16, bloom, sms, st);
+    }
     return launch_q(qfilter_ldg_kernel<16, 2, false, false>, a, 32 * 16, bloom, sms, st);
 }
 

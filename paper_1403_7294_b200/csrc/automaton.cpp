@@ -466,8 +466,7 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
                 ++p2;
                 continue;
             }
-            const std::uint32_t h2 = qhash2(h), m2 = qmask(h2);
-            p2 += (d.qbloom2[qword(h2, words2)] & m2) == m2;
+            p2 += (d.qbloom2[qword(qhash2(h), words2)] & m) == m;  // level 2: its own word, level 1's mask
             }
           }
         });
@@ -488,8 +487,8 @@ void compile_qfilter(const Nfa& nfa, Dfa& d) {
         d.qbloom2.assign(w2, 0u);
         for (std::size_t i = 0; i < grams.size(); ++i) {
             if (i && grams[i].first == grams[i - 1].first) continue;
-            const std::uint32_t h2 = qhash2(qhash(qtop(grams[i].first, q)));
-            d.qbloom2[qword(h2, static_cast<std::uint32_t>(w2))] |= qmask(h2);
+            const std::uint32_t h = qhash(qtop(grams[i].first, q));
+            d.qbloom2[qword(qhash2(h), static_cast<std::uint32_t>(w2))] |= qmask(h);
         }
         pass_rates(d.filter_fp1, d.filter_fp);
     }

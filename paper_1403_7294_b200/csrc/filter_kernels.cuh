@@ -137,9 +137,13 @@ __device__ __forceinline__ void qconfirm_slot(const ScanArgs& a, long long w, un
 // row 0 of the next block (whose codes are computed one step ahead). 16
 // Bloom probes per lane and block; survivors go to the warp's region through
 // a shared-memory counter (no warp scan).
+template <int TLD = 0>  // text load flavour (TLD > 0: experiments)
 __device__ __forceinline__ uint4 ldg_stream(const std::uint8_t* p) {
     uint4 v;
-    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    if (TLD == 1) asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else if (TLD == 2) asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else if (TLD == 3) asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 
@@ -149,7 +153,19 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 __device__ __forceinline__ const std::uint32_t* tab_of() { return reinterpret_cast<const std::uint32_t*>(acg_hot_smem); }
 
-template <int NW, int R, bool L2F, bool FUSED, bool BM, bool POST>
+// level-2 probe load flavours (LDV; experiments: which path the L2-resident probes take)
+template <int LDV>
+__device__ __forceinline__ std::uint32_t q2_load(const std::uint32_t* p) {
+    std::uint32_t v;
+    if (LDV == 1) asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    else if (LDV == 2) asm volatile("ld.global.cv.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    else if (LDV == 3) asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    else if (LDV == 4) asm volatile("atom.global.or.b32 %0, [%1], 0;" : "=r"(v) : "l"(p) : "memory");
+    else v = __ldg(p);
+    return v;
+}
+
+template <int NW, int R, bool L2F, bool FUSED, bool BM, bool POST, int LDV = 0>
 __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::uint32_t* tab, std::uint32_t* wcnt,
                                                 std::uint32_t* pub, std::uint32_t* nfin) {
     constexpr long long kBlk = 2048;
@@ -172,17 +188,18 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
     auto load = [&](uint4 (&dst)[4]) {
         if (lb < nfull) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) dst[r] = ldg_stream(lp + 512 * r);
+            for (int r = 0; r < 4; ++r) dst[r] = ldg_stream<LDV / 8>(lp + 512 * r);
         } else {
             const long long off = lb * kBlk + 16 * lane;
 #pragma unroll
             for (int r = 0; r < 4; ++r)
-                dst[r] = (lb < nb && off + 512 * r < n) ? ldg_stream(lp + 512 * r) : make_uint4(0, 0, 0, 0);
+                dst[r] = (lb < nb && off + 512 * r < n) ? ldg_stream<LDV / 8>(lp + 512 * r) : make_uint4(0, 0, 0, 0);
         }
         lp += kBlk;
         ++lb;
     };
     const std::uint32_t qmul = qsh * kQMul0;  // window -> hash in one multiply (qfilter.hpp)
+    const std::uint32_t qmul2 = qmul * kQMul3;  // window -> level-2 word hash qhash2(h)
 #if !defined(ACG_KQ_NOPIN)
     // qmask's PRMT takes its first byte table from a register: as a literal the compiler
     // re-materialises it before nearly every probe (14 moves per block); a value it
@@ -191,8 +208,12 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
     auto probe = [&](std::uint32_t h) -> std::uint32_t {
         return __byte_perm(bits_lo, 0x80402010u, __umulhi(h, kQMul1) & 0x7777u) & ~tab[qword(h, words)];
     };
+    auto mask_of = [&](std::uint32_t h) -> std::uint32_t {
+        return __byte_perm(bits_lo, 0x80402010u, __umulhi(h, kQMul1) & 0x7777u);
+    };
 #else
     auto probe = [&](std::uint32_t h) -> std::uint32_t { return qmask(h) & ~tab[qword(h, words)]; };
+    auto mask_of = [&](std::uint32_t h) -> std::uint32_t { return qmask(h); };
 #endif
     auto window = [&](std::uint32_t lo, std::uint32_t hi, int o) -> std::uint32_t {
         return o == 0 ? lo : __funnelshift_r(lo, hi, 8 * o);
@@ -229,6 +250,7 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
                     nb_[r] = __shfl_sync(0xFFFFFFFFu, s, (lane + 1) & 31);
                 }
                 std::uint32_t t[16];
+                std::uint32_t m1[L2F ? 16 : 1];  // L2F: level 1's masks, tested again at level 2
                 std::uint32_t bm_hits = 0;  // BM: samples that pass both levels (bit 4r+o)
                 if (BM) {
                     // level 1: bit (c & 0xFFFFF) of a 2^20-bit bitmap of the keys' 10-gram
@@ -259,31 +281,35 @@ __device__ __forceinline__ void qfilter_produce(const ScanArgs& a, const std::ui
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
 #pragma unroll
-                    for (int o = 0; o < 4; ++o) t[4 * r + o] = probe(window(cur[r], nb_[r], o) * qmul);
+                    for (int o = 0; o < 4; ++o) {
+                        if (L2F) {
+                            const std::uint32_t h = window(cur[r], nb_[r], o) * qmul;
+                            m1[4 * r + o] = mask_of(h);
+                            t[4 * r + o] = m1[4 * r + o] & ~tab[qword(h, words)];
+                        } else {
+                            t[4 * r + o] = probe(window(cur[r], nb_[r], o) * qmul);
+                        }
+                    }
                 }
                 if (L2F) {
                     // level 2 for the samples level 1 passed: predicated L2-resident
                     // probes, issued together (one L2 latency per block)
-                    std::uint32_t v2[16], m2[16];
+                    std::uint32_t v2[16];
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
 #pragma unroll
                         for (int o = 0; o < 4; ++o) {
                             const int i = 4 * r + o;
-                            const std::uint32_t h2 = qhash2(window(cur[r], nb_[r], o) * qmul);
-#if !defined(ACG_KQ_NOPIN)
-                            m2[i] = __byte_perm(bits_lo, 0x80402010u, __umulhi(h2, kQMul1) & 0x7777u);
-#else
-                            m2[i] = qmask(h2);
-#endif
-                            v2[i] = t[i] == 0u ? __ldg(a.qbloom2 + qword(h2, a.qwords2)) : 0xFFFFFFFFu;
+                            // word from h2 = window * (qmul * kQMul3) (= qhash2(h)), the mask is level 1's
+                            const std::uint32_t h2 = window(cur[r], nb_[r], o) * qmul2;
+                            v2[i] = t[i] == 0u ? q2_load<LDV % 8>(a.qbloom2 + qword(h2, a.qwords2)) : 0u;
                         }
                     // pack the next block and issue its load while the probes are in flight
 #pragma unroll
                     for (int r = 1; r < 4; ++r) nxt[r] = qcodes(buf[sl][r]);
                     load(buf[sl]);  // block b + 1 + R
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) t[i] |= m2[i] & ~v2[i];
+                    for (int i = 0; i < 16; ++i) t[i] = m1[i] & ~v2[i];
                 }
                 bool hit;
                 if (BM) {
@@ -427,7 +453,7 @@ __device__ __forceinline__ unsigned long long bitonic32(unsigned long long v, in
 
 // POST: the CTA confirms its own warps' survivors right after streaming (V1
 // inside KQ, overlapping the other CTAs' streaming tails; no V1 launch).
-template <int NW, int R, bool L2F, bool FUSED, bool BM = false, bool POST = false>
+template <int NW, int R, bool L2F, bool FUSED, bool BM = false, bool POST = false, int LDV = 0>
 __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_kernel(const ScanArgs a) {
     __shared__ std::uint32_t wcnt[NW], pub[NW], done_sh[NW], nfin;
     {
@@ -442,7 +468,7 @@ __global__ void __launch_bounds__(32 * (NW + (FUSED ? 1 : 0)), 1) qfilter_ldg_ke
     if (FUSED && (threadIdx.x >> 5) == NW) {  // the consumer warp
         qfilter_consume<NW>(a, pub, done_sh, &nfin);
     } else {
-        qfilter_produce<NW, R, L2F, FUSED, BM, POST>(a, tab_of(), wcnt, pub, &nfin);
+        qfilter_produce<NW, R, L2F, FUSED, BM, POST, LDV>(a, tab_of(), wcnt, pub, &nfin);
     }
     if (!POST && !FUSED) pdl_trigger();  // V1 may be scheduled (it waits for this grid's results)
     if (POST) {

@@ -81,7 +81,8 @@ ACG_HD std::uint32_t qword(std::uint32_t h, std::uint32_t words) { return qmulhi
 ACG_HD std::uint32_t qmask(std::uint32_t h) {
     return qperm(0x08040201u, 0x80402010u, qmulhi(h, kQMul1) & 0x7777u);
 }
-// Level-2 filter: its own word/mask from h2 = h * kQMul3 (independent of level 1).
+// Level-2 filter: its own word from h2 = h * kQMul3; the mask tested is level 1's
+// (given the mask, the two words' contents are independent, so the pass rates multiply).
 constexpr std::uint32_t kQMul3 = 0x27D4EB2Fu;
 constexpr double kQLevel1Max = 0.30;  // a level-1 pass rate above this is not worth streaming
 ACG_HD std::uint32_t qhash2(std::uint32_t h) { return h * kQMul3; }
