@@ -78,31 +78,36 @@ class Automaton {
 public:
     std::size_t state_count() const noexcept { return h_ ? acg_state_count(h_.get()) : 0; }
 
-    const std::vector<Pattern>& patterns() const noexcept { return *patterns_; }
+    const std::vector<Pattern>& patterns() const noexcept {
+        static const std::vector<Pattern> none;  // (a default-constructed machine has no patterns)
+        return patterns_ ? *patterns_ : none;
+    }
 
     // Goto edge out of s on byte b, if any (:67-74).
     std::optional<StateId> goto_transition(StateId s, unsigned char b) const {
         StateId to = 0;
-        if (acg_goto_transition(h_.get(), s, b, &to)) return to;
+        if (h_ && acg_goto_transition(h_.get(), s, b, &to)) return to;
         return std::nullopt;
     }
 
     // Goto edges out of s, sorted by byte (:77-80).
     std::span<const std::pair<unsigned char, StateId>> transitions(StateId s) const {
+        if (!edge_off_) return {};
         const std::uint32_t lo = (*edge_off_)[s], hi = (*edge_off_)[s + 1];
         return {edges_->data() + lo, hi - lo};
     }
 
-    StateId failure(StateId s) const { return acg_failure(h_.get(), s); }  // :84-87
+    StateId failure(StateId s) const { return h_ ? acg_failure(h_.get(), s) : kRoot; }  // :84-87
 
     // Pattern ids ending at s, ascending, suffix-closed (:92-95).
     std::span<const std::uint32_t> outputs(StateId s) const {
+        if (!h_) return {};
         const std::uint32_t* ids = nullptr;
         const std::uint32_t n = acg_outputs(h_.get(), s, &ids);
         return {ids, n};
     }
 
-    std::uint32_t depth(StateId s) const { return acg_depth(h_.get(), s); }  // :98-101
+    std::uint32_t depth(StateId s) const { return h_ ? acg_depth(h_.get(), s) : 0; }  // :98-101
 
     // The C ABI handle (device-resident scanning: acg_scanner_*).
     const acg_automaton* handle() const noexcept { return h_.get(); }

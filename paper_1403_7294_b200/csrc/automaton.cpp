@@ -652,7 +652,9 @@ static void compile_ctab(const Nfa& nfa, const std::vector<std::uint32_t>& hot_o
     // counted words: the output count above a 17-bit payload (cold non-output words keep a plain device id)
     std::uint32_t max_out = 0;
     for (std::uint32_t s = 0; s < S; ++s) max_out = std::max(max_out, nfa.out_off[s + 1] - nfa.out_off[s]);
-    const bool cnt = slots + n_out <= kCtPayMask && max_out < 255;
+    // (S <= 2^16: a cold word without outputs carries its device id, whose byte 2 must stay 0 —
+    // the walk sums the count byte of every owned step's word)
+    const bool cnt = slots + n_out <= kCtPayMask && max_out < 255 && S <= (1u << kCtPayBits);
     auto out_bits = [&](std::uint32_t s) {
         return has_out(s) ? kCtOut | (cnt ? (nfa.out_off[s + 1] - nfa.out_off[s]) << kCtPayBits : 0u) : 0u;
     };

@@ -470,10 +470,19 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
                     }
                     st[u] = v;
                     if (LOG) {
-                        if (v & live[u]) {
-                            ev[wr[u]++] = kk + (v & ct.pay_mask);
-                            recs[u] += __byte_perm(full, 0u, 0x4442u);
-                        }
+                        // branch-free log (the walk is issue-bound: 97 % of the warp-steps have
+                        // a logging lane, so a branch costs its overhead on top of its body):
+                        // a predicated store, the slot index advanced by the hit bit. The count
+                        // byte of a word without outputs is 0 (counted words), so the records
+                        // are summed unconditionally.
+                        const std::uint32_t hit = v & live[u];  // bit 31 or nothing
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.u32 [%1], %2;\n\t}"
+                            :
+                            : "r"(hit), "l"(ev + wr[u]), "r"(kk | (v & ct.pay_mask))
+                            : "memory");
+                        wr[u] += hit >> 31;
+                        recs[u] += __byte_perm(full, 0u, 0x4442u);
                     }
                 }
                 if (LOG) kk += kinc;
