@@ -465,8 +465,13 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
                         const std::uint32_t ent = lds_u32(sw * 4u + (c + tab_s));  // (bits 30-31 of sw fall off the multiply)
                         const std::uint32_t cx = c << (kCtColShift - 2);
                         const bool miss = ((ent ^ cx) & kCtColMask) != 0u;
-                        v = miss ? (x & amask) : ((ent ^ cx) & amask);
-                        full = miss ? x : ent;
+                        if (DEEP) {  // (measured: the one-select form below costs the deep walk 13 %)
+                            v = miss ? (x & amask) : ((ent ^ cx) & amask);
+                            full = miss ? x : ent;
+                        } else {
+                            full = miss ? x : (ent ^ cx);  // (the XOR touches the column field only: the count byte stays)
+                            v = full & amask;
+                        }
                     }
                     st[u] = v;
                     if (LOG) {
@@ -475,13 +480,22 @@ __global__ void __launch_bounds__(U == 1 ? 2 * kTPB : kTPB, 1) ctab_event_kernel
                         // a predicated store, the slot index advanced by the hit bit. The count
                         // byte of a word without outputs is 0 (counted words), so the records
                         // are summed unconditionally.
-                        const std::uint32_t hit = v & live[u];  // bit 31 or nothing
-                        asm volatile(
-                            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.u32 [%1], %2;\n\t}"
-                            :
-                            : "r"(hit), "l"(ev + wr[u]), "r"(kk | (v & ct.pay_mask))
-                            : "memory");
-                        wr[u] += hit >> 31;
+                        if (DEEP) {
+                            const std::uint32_t hit = v & live[u];  // bit 31 or nothing
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.u32 [%1], %2;\n\t}"
+                                :
+                                : "r"(hit), "l"(ev + wr[u]), "r"(kk | (v & ct.pay_mask))
+                                : "memory");
+                            wr[u] += hit >> 31;
+                        } else {
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                                "@p st.global.u32 [%3], %4;\n\t@p add.u32 %0, %0, 1;\n\t}"
+                                : "+r"(wr[u])
+                                : "r"(v), "r"(live[u]), "l"(ev + wr[u]), "r"(kk | (v & ct.pay_mask))
+                                : "memory");
+                        }
                         recs[u] += __byte_perm(full, 0u, 0x4442u);
                     }
                 }
