@@ -918,6 +918,31 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
                 o += T;
                 return;
             }
+            // Events with outputs in the lanes [0, popc): the j-th of them is lane j, so the
+            // owner of output t is (events whose first output lies at or before t) - 1 — one
+            // warp OR of the window's start bits and a population count instead of the
+            // binary search (cfg4: every event has outputs; pads and a ragged last batch
+            // leave the top lanes empty, anything else takes the search below).
+            const std::uint32_t nz = __ballot_sync(0xFFFFFFFFu, n != 0u);
+            if ((nz & (nz + 1u)) == 0u) {
+                const std::uint32_t excl = incl - n, voff = v >> e.ob;
+                const std::uint32_t le = 0xFFFFFFFFu >> (31 - lane);
+                std::uint32_t jbase = 0;
+                for (std::uint32_t t0 = 0; t0 < T; t0 += 32) {
+                    const std::uint32_t rel = excl - t0;
+                    const std::uint32_t starts = __reduce_or_sync(0xFFFFFFFFu, (n != 0u && rel < 32u) ? 1u << rel : 0u);
+                    const int j = static_cast<int>(jbase + __popc(starts & le)) - 1;
+                    jbase += __popc(starts);
+                    const std::uint32_t ej = __shfl_sync(0xFFFFFFFFu, excl, j);
+                    const std::uint32_t loj = __shfl_sync(0xFFFFFFFFu, lo, j);
+                    const std::uint32_t vj = __shfl_sync(0xFFFFFFFFu, voff, j);
+                    const std::uint32_t t = t0 + lane;
+                    if (t < T && o + t < a.rec_cap)
+                        a.records[o + t] = ((cbase + vj) << a.id_bits) | __ldg(a.out_ids + loj + (t - ej));
+                }
+                o += T;
+                return;
+            }
             for (std::uint32_t t0 = 0; t0 < T; t0 += 32) {
                 const std::uint32_t t = t0 + lane;
                 // owner j = the first lane with incl_j > t (binary search over the scan)
