@@ -895,6 +895,26 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
                 o += nb;
                 return;
             }
+            // short output lists (cfg3: one to three ids per state): the prefix of the
+            // counts from four ballots (no shuffle chain); every lane writes its own event's
+            // records at its prefix — neighbouring lanes, neighbouring slots — in max(n)
+            // rounds; longer lists (cfg4) take the scan and the balanced assignment below
+            if (__ballot_sync(0xFFFFFFFFu, n > 4u) == 0u) {
+                const std::uint32_t m1 = __ballot_sync(0xFFFFFFFFu, n >= 1u), m2 = __ballot_sync(0xFFFFFFFFu, n >= 2u);
+                const std::uint32_t m3 = __ballot_sync(0xFFFFFFFFu, n >= 3u), m4 = __ballot_sync(0xFFFFFFFFu, n >= 4u);
+                const std::uint32_t lt = (1u << lane) - 1u;
+                const std::uint32_t excl = __popc(m1 & lt) + __popc(m2 & lt) + __popc(m3 & lt) + __popc(m4 & lt);
+                const std::uint32_t nmax = m4 ? 4u : m3 ? 3u : m2 ? 2u : 1u;
+                const unsigned long long at = o + excl;
+                for (std::uint32_t k = 0; k < nmax; ++k) {
+                    if (k < n) {
+                        const std::uint32_t id = k == 0 ? first : __ldg(a.out_ids + lo + k);
+                        if (at + k < a.rec_cap) a.records[at + k] = key | id;
+                    }
+                }
+                o += __popc(m1) + __popc(m2) + __popc(m3) + __popc(m4);
+                return;
+            }
             // inclusive scan of the output counts
             std::uint32_t incl = n;
 #pragma unroll
@@ -903,21 +923,6 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
                 if (lane >= d) incl += y;
             }
             const std::uint32_t T = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            // short output lists (cfg3: one to three ids per state): every lane writes
-            // its own event's records at its prefix — neighbouring lanes, neighbouring
-            // slots — in max(n) rounds; long lists (cfg4) take the balanced search below
-            const std::uint32_t nmax = __reduce_max_sync(0xFFFFFFFFu, n);
-            if (nmax <= 4u) {
-                const unsigned long long at = o + (incl - n);
-                for (std::uint32_t k = 0; k < nmax; ++k) {
-                    if (k < n) {
-                        const std::uint32_t id = k == 0 ? first : __ldg(a.out_ids + lo + k);
-                        if (at + k < a.rec_cap) a.records[at + k] = key | id;
-                    }
-                }
-                o += T;
-                return;
-            }
             // Events with outputs in the lanes [0, popc): the j-th of them is lane j, so the
             // owner of output t is (events whose first output lies at or before t) - 1 — one
             // warp OR of the window's start bits and a population count instead of the
