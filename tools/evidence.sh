@@ -31,5 +31,10 @@ if [ -z "$NO_NCU" ]; then
       -s 8 -c 2 -o /tmp/kc3 -f $C3 > $O/ncu_kc3.log 2>&1
   ncu -i /tmp/kc3.ncu-rep --page raw --csv > $O/ncu_kc_cfg3_raw.csv 2>/dev/null
   ncu -i /tmp/kc3.ncu-rep --page details --csv > $O/ncu_kc_cfg3_details.csv 2>/dev/null
+  # --set full of KQ with the two-level filter (cfg2) at the bench's full size
+  C2="python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"qfilter_ldg" -s 4 -c 1 -o /tmp/kq2 -f $C2 > $O/ncu_kq2.log 2>&1
+  ncu -i /tmp/kq2.ncu-rep --page raw --csv > $O/ncu_cfg2_raw.csv 2>/dev/null
+  ncu -i /tmp/kq2.ncu-rep --page details --csv > $O/ncu_cfg2_details.csv 2>/dev/null
 fi
 echo done
