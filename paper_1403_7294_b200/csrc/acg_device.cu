@@ -1322,7 +1322,12 @@ int scanner_run(acg_scanner* s, const std::uint8_t* d_text, std::uint64_t n, std
                     const int v = e ? std::atoi(e) : 0;
                     return v > 0 && v <= 64 ? static_cast<unsigned>(v) : 16u;  // (r02: 16 -> V1 20.5 us vs 24 at 8)
                 }();
-                ACG_CUDA(launch_pdl(qconfirm_region_kernel, v1_ctas * dd.num_sms, 256, st, a));
+                static const int v1_form = [] {  // ACG_V1_FORM=0: the slot-strided kernel
+                    const char* e = std::getenv("ACG_V1_FORM");
+                    return e ? std::atoi(e) : 1;
+                }();
+                if (v1_form == 0) ACG_CUDA(launch_pdl(qconfirm_region_kernel, v1_ctas * dd.num_sms, 256, st, a));
+                else ACG_CUDA(launch_pdl(qconfirm_cta_kernel, a.qwarps, v1_form == 2 ? 128 : 256, st, a));
             }
             if (prof) ACG_CUDA(cudaEventRecord(s->ev[2], st));
             ScanArgs oa = a;
@@ -1846,6 +1851,7 @@ void warm_up_device(int device) {
     load(reinterpret_cast<const void*>(scratch_copy_kernel<true>));
     load(reinterpret_cast<const void*>(qfilter_ldg_kernel<16, 2, false, false>));
     load(reinterpret_cast<const void*>(qconfirm_region_kernel));
+    load(reinterpret_cast<const void*>(qconfirm_cta_kernel));
     load(reinterpret_cast<const void*>(qorder_region_kernel));
     // CUB's scan kernels and the pinned scalar slab, by one tiny use
     unsigned long long* d = nullptr;

@@ -506,6 +506,20 @@ __global__ void __launch_bounds__(256) qconfirm_region_kernel(const ScanArgs a) 
     }
 }
 
+// V1, one CTA per survivor region (the default): the region's survivors on
+// consecutive threads — no slot -> region division, no lanes parked on empty
+// slots (the strided form above ran 11.9 active threads per warp, and its
+// instruction stream, not the lookups' latency, was V1's time).
+__global__ void __launch_bounds__(256) qconfirm_cta_kernel(const ScanArgs a) {
+    pdl_wait();  // (launched programmatically after KQ: its survivors are complete past this point)
+    pdl_trigger();  // ORDER may be scheduled (it waits for this grid's results)
+    for (long long w = blockIdx.x; w < static_cast<long long>(a.qwarps); w += gridDim.x) {
+        const std::uint32_t nw = min(a.qwarp_n[w], a.qcand_cap);
+        const unsigned long long t0 = static_cast<unsigned long long>(w) * a.qcand_cap;
+        for (std::uint32_t k = threadIdx.x; k < nw; k += blockDim.x) qconfirm_slot(a, w, t0 + k);
+    }
+}
+
 // ORDER: one warp per region. Its slot range starts at the sum of the
 // matches owned by earlier regions (summed directly from reg_n: no separate
 // scan pass); it reads its slab (every match ending in the region) and sorts
