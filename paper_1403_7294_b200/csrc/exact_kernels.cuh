@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(512) event_count_kernel(const ScanArgs a, cons
 // (VIS: also the per-output-state visit histogram, in shared-memory bins —
 // when KC counted the records itself and E1 is not run)
 template <bool XL, bool VIS>
-__global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, const EventArgs e, const CtabArgs ct) {
+__global__ void __launch_bounds__(256, VIS ? 5 : 4) event_expand_kernel(const ScanArgs a, const EventArgs e, const CtabArgs ct) {
     extern __shared__ std::uint32_t vbins[];
     if (VIS) {
         for (std::uint32_t i = threadIdx.x; i < e.n_out; i += blockDim.x) vbins[i] = 0;
@@ -933,17 +933,25 @@ __global__ void __launch_bounds__(256) event_expand_kernel(const ScanArgs a, con
                 const std::uint32_t excl = incl - n, voff = v >> e.ob;
                 const std::uint32_t le = 0xFFFFFFFFu >> (31 - lane);
                 std::uint32_t jbase = 0;
-                for (std::uint32_t t0 = 0; t0 < T; t0 += 32) {
-                    const std::uint32_t rel = excl - t0;
-                    const std::uint32_t starts = __reduce_or_sync(0xFFFFFFFFu, (n != 0u && rel < 32u) ? 1u << rel : 0u);
-                    const int j = static_cast<int>(jbase + __popc(starts & le)) - 1;
-                    jbase += __popc(starts);
-                    const std::uint32_t ej = __shfl_sync(0xFFFFFFFFu, excl, j);
-                    const std::uint32_t loj = __shfl_sync(0xFFFFFFFFu, lo, j);
-                    const std::uint32_t vj = __shfl_sync(0xFFFFFFFFu, voff, j);
-                    const std::uint32_t t = t0 + lane;
-                    if (t < T && o + t < a.rec_cap)
-                        a.records[o + t] = ((cbase + vj) << a.id_bits) | __ldg(a.out_ids + loj + (t - ej));
+                // two windows of 32 outputs per iteration: two independent vote / shuffle /
+                // gather chains in flight
+                for (std::uint32_t t0 = 0; t0 < T; t0 += 64) {
+                    const std::uint32_t rel0 = excl - t0, rel1 = rel0 - 32u;
+                    const std::uint32_t s0 = __reduce_or_sync(0xFFFFFFFFu, (n != 0u && rel0 < 32u) ? 1u << rel0 : 0u);
+                    const std::uint32_t s1 = __reduce_or_sync(0xFFFFFFFFu, (n != 0u && rel1 < 32u) ? 1u << rel1 : 0u);
+                    const int j0 = static_cast<int>(jbase + __popc(s0 & le)) - 1;
+                    jbase += __popc(s0);
+                    const int j1 = static_cast<int>(jbase + __popc(s1 & le)) - 1;
+                    jbase += __popc(s1);
+                    const std::uint32_t e0 = __shfl_sync(0xFFFFFFFFu, excl, j0), e1 = __shfl_sync(0xFFFFFFFFu, excl, j1);
+                    const std::uint32_t l0 = __shfl_sync(0xFFFFFFFFu, lo, j0), l1 = __shfl_sync(0xFFFFFFFFu, lo, j1);
+                    const std::uint32_t v0 = __shfl_sync(0xFFFFFFFFu, voff, j0), v1 = __shfl_sync(0xFFFFFFFFu, voff, j1);
+                    const std::uint32_t ta = t0 + lane, tb = ta + 32u;
+                    const bool wa = ta < T && o + ta < a.rec_cap, wb = tb < T && o + tb < a.rec_cap;
+                    const std::uint32_t ia = wa ? __ldg(a.out_ids + l0 + (ta - e0)) : 0u;
+                    const std::uint32_t ib = wb ? __ldg(a.out_ids + l1 + (tb - e1)) : 0u;
+                    if (wa) a.records[o + ta] = ((cbase + v0) << a.id_bits) | ia;
+                    if (wb) a.records[o + tb] = ((cbase + v1) << a.id_bits) | ib;
                 }
                 o += T;
                 return;
