@@ -153,7 +153,12 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 __device__ __forceinline__ const std::uint32_t* tab_of() { return reinterpret_cast<const std::uint32_t*>(acg_hot_smem); }
 
-// level-2 probe load flavours (LDV; experiments: which path the L2-resident probes take)
+// Load flavours, LDV = 8 * (text load) + (level-2 probe load). Defaults: 24 for the
+// single-level kernel (text L1::no_allocate), 25 with the level-2 filter (probes as
+// ld.global.cg: a probe must not allocate a line in the 23 KB of L1 left beside the
+// filter — with ld.global.nc every probe and every text line queued behind that
+// allocation: cfg2 0.956 -> 0.814 ms per 2 GiB). The other values are the measured
+// alternatives ("Measured and rejected").
 template <int LDV>
 __device__ __forceinline__ std::uint32_t q2_load(const std::uint32_t* p) {
     std::uint32_t v;
